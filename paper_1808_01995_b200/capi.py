@@ -1,0 +1,247 @@
+"""ctypes binding of include/sfb200.h (libsfb200.so).  Thin: no arithmetic happens here."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsfb200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+        "g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
+
+lib = C.CDLL(LIB_PATH)
+
+OK, ERR_PARAMETER, ERR_STABILITY, ERR_LOCATION, ERR_CAPABILITY, ERR_BINDING, ERR_CUDA, ERR_ORDER = range(8)
+CLOUD_SRC, CLOUD_REC = 0, 1
+OP_FORWARD, OP_ADJOINT, OP_GRADIENT, OP_TTI_FORWARD = 0, 1, 2, 3
+PART_ALL, PART_LOW, PART_HIGH, PART_INTERIOR = 0, 1, 2, 3
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("shape", C.c_int64 * 3), ("spacing", C.c_double * 3),
+                ("space_order", C.c_int32), ("dt", C.c_double), ("nt", C.c_int64),
+                ("device", C.c_int32), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64)]
+
+
+class FieldView(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("stride", C.c_int64 * 3)]
+
+
+class Report(C.Structure):
+    _fields_ = [("seconds", C.c_double), ("flops", C.c_longlong), ("gflops", C.c_double),
+                ("steps", C.c_long), ("gpts_per_s", C.c_double), ("kernel_launches", C.c_long)]
+
+
+# every symbol include/sfb200.h declares (tests/test_capi_cpu.py checks the list against
+# the header)
+SYMBOLS = [
+    "sfb_abi_version", "sfb_last_error", "sfb_device_count", "sfb_plan_create",
+    "sfb_plan_destroy", "sfb_fd_weights", "sfb_critical_dt", "sfb_set_model",
+    "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_adjoint",
+    "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
+    "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_step_begin", "sfb_step_compute",
+    "sfb_step_points", "sfb_step_end", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
+]
+
+lib.sfb_last_error.restype = C.c_char_p
+lib.sfb_last_error.argtypes = [C.c_void_p]
+lib.sfb_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]
+lib.sfb_plan_destroy.argtypes = [C.c_void_p]
+lib.sfb_set_model.argtypes = [C.c_void_p, C.POINTER(FieldView), C.POINTER(FieldView), C.c_double]
+lib.sfb_set_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
+lib.sfb_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Report)]
+lib.sfb_adjoint.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Report)]
+lib.sfb_gradient.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(FieldView), C.POINTER(Report)]
+lib.sfb_get_wavefield.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.POINTER(FieldView)]
+lib.sfb_upload_traces.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+lib.sfb_download_traces.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+lib.sfb_run_resident.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.POINTER(Report)]
+lib.sfb_run_steps.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.POINTER(Report)]
+lib.sfb_step_begin.argtypes = [C.c_void_p, C.c_int, C.c_int64]
+lib.sfb_step_compute.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
+lib.sfb_step_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
+lib.sfb_step_end.argtypes = [C.c_void_p, C.c_int]
+lib.sfb_halo_blocks.argtypes = [C.c_void_p, C.c_int, C.c_int64] + [C.POINTER(C.c_void_p)] * 4 + [C.POINTER(C.c_int64)]
+lib.sfb_stream_sync.argtypes = [C.c_void_p]
+lib.sfb_streams.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+lib.sfb_set_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+lib.sfb_copy_halo.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+lib.sfb_set_tile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
+lib.sfb_get_tile.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 6
+lib.sfb_fd_weights.argtypes = [C.c_int, C.c_int, C.c_void_p]
+lib.sfb_critical_dt.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double)]
+lib.sfb_locate.argtypes = [C.POINTER(PlanDesc), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+
+
+class SfbError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[sfb {code}] {msg}")
+        self.code = code
+
+
+def _view(a: np.ndarray) -> FieldView:
+    assert a.dtype == np.float64
+    v = FieldView()
+    v.ptr = a.ctypes.data
+    for d in range(a.ndim):
+        v.stride[d] = a.strides[d] // 8
+    return v
+
+
+def fd_weights(deriv, order):
+    out = np.zeros(order // 2 + 1)
+    rc = lib.sfb_fd_weights(deriv, order, out.ctypes.data)
+    if rc:
+        raise SfbError(rc, lib.sfb_last_error(None).decode())
+    return out
+
+
+def critical_dt(spacing, v_max, order):
+    h = np.asarray(spacing, dtype=np.float64)
+    out = C.c_double()
+    rc = lib.sfb_critical_dt(len(h), h.ctypes.data, v_max, order, C.byref(out))
+    if rc:
+        raise SfbError(rc, lib.sfb_last_error(None).decode())
+    return out.value
+
+
+def device_count():
+    n = C.c_int()
+    lib.sfb_device_count(C.byref(n))
+    return n.value
+
+
+class Plan:
+    """One operator context on one device (sfb_plan)."""
+
+    def __init__(self, shape, spacing, space_order, dt, nt, device=0, slab=None):
+        d = PlanDesc()
+        d.ndim = len(shape)
+        for a in range(len(shape)):
+            d.shape[a] = int(shape[a])
+            d.spacing[a] = float(spacing[a])
+        d.space_order = int(space_order)
+        d.dt = float(dt)
+        d.nt = int(nt)
+        d.device = int(device)
+        if slab is not None:
+            d.slab_lo, d.slab_hi = int(slab[0]), int(slab[1])
+        self.desc = d
+        self.shape = [int(s) for s in shape]
+        self.nt = int(nt)
+        self.h = C.c_void_p()
+        rc = lib.sfb_plan_create(C.byref(d), C.byref(self.h))
+        if rc:
+            raise SfbError(rc, lib.sfb_last_error(None).decode())
+        self.np = [0, 0]
+
+    def _chk(self, rc):
+        if rc:
+            raise SfbError(rc, lib.sfb_last_error(self.h).decode())
+
+    def close(self):
+        if self.h:
+            lib.sfb_plan_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_model(self, m, damp, v_max=0.0):
+        m = np.asarray(m, dtype=np.float64)
+        damp = np.asarray(damp, dtype=np.float64)
+        self._chk(lib.sfb_set_model(self.h, C.byref(_view(m)), C.byref(_view(damp)), float(v_max)))
+
+    def set_points(self, cloud, base, w):
+        base = np.ascontiguousarray(base, dtype=np.int64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        self.np[cloud] = base.shape[0]
+        self._chk(lib.sfb_set_points(self.h, cloud, base.shape[0], base.ctypes.data, w.ctypes.data))
+
+    def forward(self, src, save_every=0):
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        rec = np.empty((self.nt, self.np[CLOUD_REC]))
+        rep = Report()
+        self._chk(lib.sfb_forward(self.h, src.ctypes.data, rec.ctypes.data, save_every, C.byref(rep)))
+        return rec, rep
+
+    def adjoint(self, rec):
+        rec = np.ascontiguousarray(rec, dtype=np.float64)
+        srca = np.empty((self.nt, self.np[CLOUD_SRC]))
+        rep = Report()
+        self._chk(lib.sfb_adjoint(self.h, rec.ctypes.data, srca.ctypes.data, C.byref(rep)))
+        return srca, rep
+
+    def gradient(self, resid):
+        resid = np.ascontiguousarray(resid, dtype=np.float64)
+        grad = np.zeros(self.shape)
+        rep = Report()
+        self._chk(lib.sfb_gradient(self.h, resid.ctypes.data, C.byref(_view(grad)), C.byref(rep)))
+        return grad, rep
+
+    def wavefield(self, level, out=None):
+        out = np.zeros(self.shape) if out is None else out
+        self._chk(lib.sfb_get_wavefield(self.h, 0, level, C.byref(_view(out))))
+        return out
+
+    def upload_traces(self, cloud, tr):
+        tr = np.ascontiguousarray(tr, dtype=np.float64)
+        self._chk(lib.sfb_upload_traces(self.h, cloud, tr.ctypes.data))
+
+    def download_traces(self, cloud):
+        out = np.empty((self.nt, self.np[cloud]))
+        self._chk(lib.sfb_download_traces(self.h, cloud, out.ctypes.data))
+        return out
+
+    def run_resident(self, op, save_every=0):
+        rep = Report()
+        self._chk(lib.sfb_run_resident(self.h, op, save_every, C.byref(rep)))
+        return rep
+
+    def run_steps(self, op, t_from, t_to):
+        rep = Report()
+        self._chk(lib.sfb_run_steps(self.h, op, t_from, t_to, C.byref(rep)))
+        return rep
+
+    def set_tile(self, txv, ty, r, chunk=0):
+        self._chk(lib.sfb_set_tile(self.h, txv, ty, r, chunk))
+
+    def get_tile(self):
+        v = [C.c_int() for _ in range(6)]
+        self._chk(lib.sfb_get_tile(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(["txv", "ty", "r", "stages", "chunk", "sep"], [x.value for x in v]))
+
+    # slab stepping
+    def step_begin(self, op, save_every=0):
+        self._chk(lib.sfb_step_begin(self.h, op, save_every))
+
+    def step_compute(self, op, t, part):
+        self._chk(lib.sfb_step_compute(self.h, op, t, part))
+
+    def step_points(self, op, t, part):
+        self._chk(lib.sfb_step_points(self.h, op, t, part))
+
+    def step_end(self, op):
+        self._chk(lib.sfb_step_end(self.h, op))
+
+    def halo_blocks(self, op, t):
+        p = [C.c_void_p() for _ in range(4)]
+        n = C.c_int64()
+        self._chk(lib.sfb_halo_blocks(self.h, op, t, *[C.byref(x) for x in p], C.byref(n)))
+        return dict(send_lo=p[0].value, send_hi=p[1].value, recv_lo=p[2].value,
+                    recv_hi=p[3].value, count=n.value)
+
+    def copy_halo(self, dst, src, count):
+        self._chk(lib.sfb_copy_halo(self.h, dst, src, count))
+
+    def sync(self):
+        self._chk(lib.sfb_stream_sync(self.h))

@@ -1,0 +1,2 @@
+#include "variants.hpp"
+SFB_INSTANTIATE_K(7)

@@ -1,0 +1,1088 @@
+// capi.cu -- the extern "C" boundary of libsfb200.so (declared in include/sfb200.h) and
+// the host logic behind it: plan set-up, model / point-table upload, the time loops.
+//
+// The time loops restate run_wave / run_gradient / run_window of the reference
+// (proj/src/seismic_ops.cpp:44-54,137-147): zero the wavefield and the sampled traces,
+// then step t over [1, nt-1), ascending for the forward operator and descending for the
+// adjoint and gradient operators, each step being dense update -> scatter -> gather in
+// that order (proj/tests/test_compiler.cpp:109-120).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+
+#include "fdweights.hpp"
+#include "plan.hpp"
+#include "point_kernels.cuh"
+
+namespace sfb {
+
+std::vector<StepVariant>& step_variant_registry() {
+    static std::vector<StepVariant> reg;
+    return reg;
+}
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <typename F>
+int guarded(sfb_plan* plan, F&& f) {
+    try {
+        if (plan) {
+            cudaError_t e = cudaSetDevice(plan->device);
+            if (e != cudaSuccess)
+                throw Failure(SFB_ERR_CAPABILITY,
+                              std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+        }
+        f();
+        return SFB_OK;
+    } catch (const Failure& e) {
+        (plan ? plan->err : g_create_err) = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        (plan ? plan->err : g_create_err) = e.what();
+        return SFB_ERR_CUDA;
+    }
+}
+
+void require(bool ok, int code, const char* msg) {
+    if (!ok) throw Failure(code, msg);
+}
+
+long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+
+// ---- driver entry point for tensor maps (no link-time libcuda dependency) -------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw Failure(SFB_ERR_CAPABILITY, "driver lacks cuTensorMapEncodeTiled");
+    return fn;
+}
+
+void make_tensor_map(Plan& P, int which) {
+    const StepVariant& v = *P.variant;
+    cuuint64_t dims[3] = {cuuint64_t(P.N[2]), cuuint64_t(P.N[1]), cuuint64_t(P.n0 + 2 * P.K)};
+    cuuint64_t strides[2] = {cuuint64_t(P.pitch) * 4, cuuint64_t(P.plane) * 4};
+    cuuint32_t box[3] = {cuuint32_t(v.box_w), cuuint32_t(v.box_h), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult rc = encode_tiled()(&P.tm[which], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                 P.u[which].p, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS)
+        throw Failure(SFB_ERR_CUDA, "cuTensorMapEncodeTiled failed with code " +
+                                        std::to_string(int(rc)));
+}
+
+// ---- tile shape / chunk choice ----------------------------------------------------------
+
+void select_variant(Plan& P, int txv, int ty, int r) {
+    const StepVariant* best = nullptr;
+    for (const StepVariant& v : step_variant_registry()) {
+        if (v.K != P.K || v.sep != P.sep) continue;
+        if (txv > 0 && (v.TXV != txv || v.TY != ty || v.R != r)) continue;
+        if (!best) best = &v;
+    }
+    if (!best)
+        throw Failure(SFB_ERR_CAPABILITY, "no kernel image for space order " +
+                                              std::to_string(2 * P.K));
+    P.variant = best;
+    SFB_CUDA(cudaFuncSetAttribute(best->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(best->smem)));
+    int bps = 1;
+    SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, best->func, best->nthreads,
+                                                           best->smem));
+    if (bps < 1) bps = 1;
+    // split d0 into chunks so the grid fills whole waves; every chunk re-reads 2K planes
+    // of u[t] (4 of the 20 bytes per node), which the score charges
+    const long long tiles = ((P.N[2] + best->tile_x - 1) / best->tile_x) *
+                            ((P.N[1] + best->tile_y - 1) / best->tile_y);
+    const long long slots = (long long)P.sm_count * bps;
+    int best_nch = 1;
+    double best_score = -1;
+    const int max_nch = std::max(1, P.n0 / std::max(1, 2 * P.K));
+    for (int nch = 1; nch <= max_nch; ++nch) {
+        const int chunk = (P.n0 + nch - 1) / nch;
+        const int real = (P.n0 + chunk - 1) / chunk;
+        const long long total = tiles * real;
+        const long long waves = (total + slots - 1) / slots;
+        const double fill = double(total) / double(waves * slots);
+        const double extra = 1.0 + (2.0 * P.K / chunk) * 0.2;
+        const double score = fill / extra;
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best_nch = real;
+        }
+        if (total > 16 * slots) break;
+    }
+    P.chunk = (P.n0 + best_nch - 1) / best_nch;
+    if (P.u[0].p) {
+        make_tensor_map(P, 0);
+        make_tensor_map(P, 1);
+    }
+}
+
+// ---- host <-> device field movement --------------------------------------------------------
+
+struct IntView {
+    const double* ptr;
+    long long s[3];
+};
+
+IntView embed_view(const Plan& P, const double* ptr, const int64_t* stride) {
+    IntView v{ptr, {0, 0, 0}};
+    const int off = 3 - P.ndim;
+    for (int a = 0; a < P.ndim; ++a) v.s[off + a] = stride[a];
+    return v;
+}
+
+// owned planes of a strided host f64 field -> compact device f64 [n0][N1][N2]
+void upload_f64(Plan& P, const IntView& v, DevBuf& tmp) {
+    const size_t rowb = size_t(P.N[2]) * 8;
+    tmp.alloc(size_t(P.n0) * P.N[1] * rowb, false);
+    double* d = tmp.as<double>();
+    if (v.s[2] == 1 || P.N[2] == 1) {
+        for (long long z = 0; z < P.n0; ++z) {
+            const double* src = v.ptr + (P.z_lo + z) * v.s[0];
+            const size_t spitch = P.N[1] > 1 ? size_t(v.s[1]) * 8 : rowb;
+            SFB_CUDA(cudaMemcpy2DAsync(d + z * P.N[1] * P.N[2], rowb, src, spitch, rowb,
+                                       size_t(P.N[1]), cudaMemcpyHostToDevice, P.s_main));
+        }
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    } else {
+        std::vector<double> row(size_t(P.N[1]) * P.N[2]);
+        for (long long z = 0; z < P.n0; ++z) {
+            for (long long j = 0; j < P.N[1]; ++j)
+                for (long long l = 0; l < P.N[2]; ++l)
+                    row[j * P.N[2] + l] = v.ptr[(P.z_lo + z) * v.s[0] + j * v.s[1] + l * v.s[2]];
+            SFB_CUDA(cudaMemcpyAsync(d + z * P.N[1] * P.N[2], row.data(), row.size() * 8,
+                                     cudaMemcpyHostToDevice, P.s_main));
+            SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        }
+    }
+}
+
+// compact device f64 [n0][N1][N2] -> owned planes of a strided host f64 field
+void download_f64(Plan& P, const DevBuf& tmp, double* ptr, const int64_t* stride) {
+    long long s[3] = {0, 0, 0};
+    const int off = 3 - P.ndim;
+    for (int a = 0; a < P.ndim; ++a) s[off + a] = stride[a];
+    const size_t rowb = size_t(P.N[2]) * 8;
+    const double* d = tmp.as<double>();
+    if (s[2] == 1 || P.N[2] == 1) {
+        for (long long z = 0; z < P.n0; ++z) {
+            double* dst = ptr + (P.z_lo + z) * s[0];
+            const size_t dpitch = P.N[1] > 1 ? size_t(s[1]) * 8 : rowb;
+            SFB_CUDA(cudaMemcpy2DAsync(dst, dpitch, d + z * P.N[1] * P.N[2], rowb, rowb,
+                                       size_t(P.N[1]), cudaMemcpyDeviceToHost, P.s_main));
+        }
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    } else {
+        std::vector<double> row(size_t(P.N[1]) * P.N[2]);
+        for (long long z = 0; z < P.n0; ++z) {
+            SFB_CUDA(cudaMemcpyAsync(row.data(), d + z * P.N[1] * P.N[2], row.size() * 8,
+                                     cudaMemcpyDeviceToHost, P.s_main));
+            SFB_CUDA(cudaStreamSynchronize(P.s_main));
+            for (long long j = 0; j < P.N[1]; ++j)
+                for (long long l = 0; l < P.N[2]; ++l)
+                    ptr[(P.z_lo + z) * s[0] + j * s[1] + l * s[2]] = row[j * P.N[2] + l];
+        }
+    }
+}
+
+dim3 row_grid(const Plan& P, long long rows) {
+    unsigned gy = unsigned(std::min<long long>(rows, 32768));
+    unsigned gz = unsigned((rows + gy - 1) / gy);
+    unsigned gx = unsigned(std::max<long long>(1, std::min<long long>(8, (P.N[2] + 255) / 256)));
+    return dim3(gx, gy, gz);
+}
+
+// fp32 pitched compact array (no ghost planes) or wavefield level -> strided host f64
+void download_field(Plan& P, const float* dev, const sfb_field_mview* out) {
+    DevBuf tmp;
+    const long long rows = (long long)P.n0 * P.N[1];
+    tmp.alloc(size_t(rows) * P.N[2] * 8, false);
+    convert_f32_pitched_f64<<<row_grid(P, rows), 256, 0, P.s_main>>>(dev, tmp.as<double>(), rows,
+                                                                   int(P.N[2]), P.pitch);
+    SFB_CUDA(cudaGetLastError());
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    download_f64(P, tmp, out->ptr, out->stride);
+}
+
+// ---- point tables ------------------------------------------------------------------------
+
+void build_cloud(Plan& P, Cloud& c) {
+    const int nd = P.ndim, nc = 1 << nd, off = 3 - nd;
+    struct Ent {
+        long long key;  // compact node index
+        long long u;
+        int point;
+        float w;
+    };
+    std::vector<Ent> ents;
+    ents.reserve(size_t(c.np) * 2);
+    std::vector<long long> smp_idx(c.np, -1);
+    std::vector<float> smp_w(size_t(c.np) * nc);
+    for (long long p = 0; p < c.np; ++p) {
+        long long b[3] = {0, 0, 0};
+        for (int a = 0; a < nd; ++a) {
+            b[off + a] = c.base[p * nd + a];
+            if (b[off + a] < 0 || b[off + a] > P.N[off + a] - 2)
+                throw Failure(SFB_ERR_LOCATION, "point " + std::to_string(p) +
+                                                    ": base cell outside the grid");
+        }
+        if (b[0] >= P.z_lo && b[0] < P.z_hi)
+            smp_idx[p] = (b[0] - P.z_lo + P.K) * P.plane + b[1] * P.pitch + b[2];
+        for (int cc = 0; cc < nc; ++cc) {
+            const double w = c.w[p * nc + cc];
+            smp_w[p * nc + cc] = float(w);
+            if (w == 0.0) continue;
+            long long id[3] = {b[0], b[1], b[2]};
+            for (int a = 0; a < nd; ++a) id[off + a] += (cc >> a) & 1;
+            if (id[0] < P.z_lo || id[0] >= P.z_hi) continue;  // node owned by a neighbour slab
+            const long long z = id[0] - P.z_lo;
+            Ent e;
+            e.key = z * P.plane + id[1] * P.pitch + id[2];
+            e.u = (z + P.K) * P.plane + id[1] * P.pitch + id[2];
+            e.point = int(p);
+            e.w = float(w);
+            ents.push_back(e);
+        }
+    }
+    std::stable_sort(ents.begin(), ents.end(),
+                     [](const Ent& a, const Ent& b) { return a.key < b.key; });
+    std::vector<int> start;
+    std::vector<long long> cu, ck;
+    std::vector<int> ep(ents.size());
+    std::vector<float> ew(ents.size());
+    for (size_t i = 0; i < ents.size(); ++i) {
+        if (i == 0 || ents[i].key != ents[i - 1].key) {
+            start.push_back(int(i));
+            cu.push_back(ents[i].u);
+            ck.push_back(ents[i].key);
+        }
+        ep[i] = ents[i].point;
+        ew[i] = ents[i].w;
+    }
+    start.push_back(int(ents.size()));
+    c.ncell = (long long)cu.size();
+    c.nent = (long long)ents.size();
+    c.h_cell_start = start;
+    // node ranges lying in the low / high K boundary planes (slab stepping)
+    const long long lo_lim = (long long)std::min(P.K, P.n0) * P.plane;
+    const long long hi_lim = (long long)std::max(P.n0 - P.K, std::min(P.K, P.n0)) * P.plane;
+    c.cell_lo_end = std::lower_bound(ck.begin(), ck.end(), lo_lim) - ck.begin();
+    c.cell_hi_begin = std::lower_bound(ck.begin(), ck.end(), hi_lim) - ck.begin();
+
+    auto put = [&P](DevBuf& d, const void* src, size_t bytes) {
+        d.alloc(bytes, false);
+        if (bytes) SFB_CUDA(cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, P.s_main));
+    };
+    put(c.cell_start, start.data(), start.size() * sizeof(int));
+    put(c.cell_u, cu.data(), cu.size() * 8);
+    put(c.cell_c, ck.data(), ck.size() * 8);
+    put(c.ent_point, ep.data(), ep.size() * sizeof(int));
+    put(c.ent_w, ew.data(), ew.size() * sizeof(float));
+    put(c.smp_idx, smp_idx.data(), smp_idx.size() * 8);
+    put(c.smp_w, smp_w.data(), smp_w.size() * sizeof(float));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));  // the host tables above are locals
+    const size_t trb = size_t(P.desc.nt) * size_t(c.np) * sizeof(float);
+    c.tr_in.alloc(trb, true);
+    c.tr_out.alloc(trb, true);
+    c.has_in = false;
+    c.set = true;
+}
+
+void upload_traces(Plan& P, Cloud& c, const double* host) {
+    const long long n = P.desc.nt * c.np;
+    DevBuf tmp;
+    tmp.alloc(size_t(n) * 8, false);
+    SFB_CUDA(cudaMemcpyAsync(tmp.p, host, size_t(n) * 8, cudaMemcpyHostToDevice, P.s_main));
+    const int nb = int(std::min<long long>((n + 255) / 256, 148 * 16));
+    convert_f64_f32_flat<<<std::max(nb, 1), 256, 0, P.s_main>>>(tmp.as<double>(),
+                                                               c.tr_in.as<float>(), n);
+    SFB_CUDA(cudaGetLastError());
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    c.has_in = true;
+}
+
+void download_traces(Plan& P, Cloud& c, double* host) {
+    const long long n = P.desc.nt * c.np;
+    DevBuf tmp;
+    tmp.alloc(size_t(n) * 8, false);
+    const int nb = int(std::min<long long>((n + 255) / 256, 148 * 16));
+    convert_f32_f64_flat<<<std::max(nb, 1), 256, 0, P.s_main>>>(c.tr_out.as<float>(),
+                                                               tmp.as<double>(), n);
+    SFB_CUDA(cudaGetLastError());
+    SFB_CUDA(cudaMemcpyAsync(host, tmp.p, size_t(n) * 8, cudaMemcpyDeviceToHost, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+}
+
+// ---- stepping ------------------------------------------------------------------------------
+
+struct OpRoles {
+    bool backward;
+    int inj, smp;  // cloud indices, -1 = none
+    bool imaging;
+};
+
+OpRoles roles(int op) {
+    switch (op) {
+    case SFB_OP_FORWARD: return {false, SFB_CLOUD_SRC, SFB_CLOUD_REC, false};
+    case SFB_OP_ADJOINT: return {true, SFB_CLOUD_REC, SFB_CLOUD_SRC, false};
+    case SFB_OP_GRADIENT: return {true, SFB_CLOUD_REC, -1, true};
+    default: throw Failure(SFB_ERR_PARAMETER, "unknown operator id");
+    }
+}
+
+void step_begin(Plan& P, int op, long long save_every) {
+    const OpRoles ro = roles(op);
+    require(P.model_set, SFB_ERR_BINDING, "model fields are not bound (sfb_set_model)");
+    require(P.cloud[ro.inj].set, SFB_ERR_BINDING, "injected point cloud is not bound");
+    require(ro.smp < 0 || P.cloud[ro.smp].set, SFB_ERR_BINDING,
+            "sampled point cloud is not bound");
+    require(save_every >= 0, SFB_ERR_PARAMETER, "save_every must be >= 0");
+    // run_wave / run_gradient: zero the wavefield and the sampled traces
+    SFB_CUDA(cudaMemsetAsync(P.u[0].p, 0, size_t(P.ucount) * 4, P.s_main));
+    SFB_CUDA(cudaMemsetAsync(P.u[1].p, 0, size_t(P.ucount) * 4, P.s_main));
+    if (ro.smp >= 0) {
+        Cloud& c = P.cloud[ro.smp];
+        SFB_CUDA(cudaMemsetAsync(c.tr_out.p, 0, size_t(P.desc.nt) * c.np * 4, P.s_main));
+    }
+    if (op == SFB_OP_FORWARD) {
+        P.history_valid = false;
+        P.save_every = save_every;
+        if (save_every > 0) {
+            P.nslots = (P.desc.nt - 1) / save_every + 1;
+            P.snaps.alloc(size_t(P.nslots) * P.ccount * 4, false);
+            SFB_CUDA(cudaMemsetAsync(P.snaps.p, 0, size_t(P.nslots) * P.ccount * 4, P.s_main));
+        }
+    }
+    if (ro.imaging) {
+        require(P.history_valid && P.save_every > 0, SFB_ERR_PARAMETER,
+                "gradient_operator: saved forward history required");
+        P.grad.alloc(size_t(P.ccount) * 4, false);
+        SFB_CUDA(cudaMemsetAsync(P.grad.p, 0, size_t(P.ccount) * 4, P.s_main));
+    }
+    P.live_level[0] = P.live_level[1] = -1;
+    P.launches = 0;
+    P.main_pending = P.bnd_pending = false;
+}
+
+void part_range(const Plan& P, int part, int& lo, int& hi) {
+    const int K = P.K, n0 = P.n0;
+    switch (part) {
+    case SFB_PART_ALL: lo = 0; hi = n0; break;
+    case SFB_PART_LOW: lo = 0; hi = std::min(K, n0); break;
+    case SFB_PART_HIGH: lo = std::max(n0 - K, std::min(K, n0)); hi = n0; break;
+    case SFB_PART_INTERIOR: lo = std::min(K, n0); hi = std::max(n0 - K, std::min(K, n0)); break;
+    default: throw Failure(SFB_ERR_PARAMETER, "unknown slab part");
+    }
+}
+
+cudaStream_t part_stream(Plan& P, int part) {
+    const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH;
+    cudaStream_t st = bnd ? P.s_bnd : P.s_main;
+    // the other stream's last work of the previous step wrote planes this launch reads
+    if (bnd && P.main_pending) {
+        SFB_CUDA(cudaStreamWaitEvent(P.s_bnd, P.ev_main, 0));
+        P.main_pending = false;
+    }
+    if (!bnd && P.bnd_pending) {
+        SFB_CUDA(cudaStreamWaitEvent(P.s_main, P.ev_bnd, 0));
+        P.bnd_pending = false;
+    }
+    return st;
+}
+
+void mark_stream(Plan& P, int part) {
+    const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH;
+    if (P.s_bnd == P.s_main) return;
+    if (bnd) {
+        SFB_CUDA(cudaEventRecord(P.ev_bnd, P.s_bnd));
+        P.bnd_pending = true;
+    } else {
+        SFB_CUDA(cudaEventRecord(P.ev_main, P.s_main));
+        P.main_pending = true;
+    }
+}
+
+void step_compute(Plan& P, int op, long long t, int part) {
+    const OpRoles ro = roles(op);
+    require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
+    int lo, hi;
+    part_range(P, part, lo, hi);
+    if (hi <= lo) return;
+    const int cur = int(t & 1), oth = cur ^ 1;
+    const long long tnew = ro.backward ? t - 1 : t + 1;
+    StepParams sp{};
+    sp.k = P.coef;
+    sp.r = P.r.as<float>();
+    sp.damp = P.damp.as<float>();
+    sp.dz = P.dz.as<float>();
+    sp.dy = P.dy.as<float>();
+    sp.dx = P.dx.as<float>();
+    sp.uo = P.u[oth].as<float>();
+    sp.N1 = int(P.N[1]);
+    sp.N2 = int(P.N[2]);
+    sp.pitch = P.pitch;
+    sp.plane = P.plane;
+    sp.z_lo = lo;
+    sp.z_hi = hi;
+    sp.chunk = (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? P.chunk : (hi - lo);
+    if (op == SFB_OP_FORWARD && P.save_every > 0 && tnew % P.save_every == 0)
+        sp.snap = P.snaps.as<float>() + (tnew / P.save_every) * P.ccount;
+    if (ro.imaging && t % P.save_every == 0) {
+        sp.usave = P.snaps.as<float>() + (t / P.save_every) * P.ccount;
+        sp.grad = P.grad.as<float>();
+    }
+    const StepVariant& v = *P.variant;
+    dim3 grid(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x),
+              unsigned((P.N[1] + v.tile_y - 1) / v.tile_y),
+              unsigned((hi - lo + sp.chunk - 1) / sp.chunk));
+    cudaStream_t st = part_stream(P, part);
+    SFB_CUDA(v.launch(P.tm[cur], sp, grid, st));
+    ++P.launches;
+    mark_stream(P, part);
+    if (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) {
+        P.live_level[cur] = t;
+        P.live_level[oth] = tnew;
+    }
+}
+
+// part: SFB_PART_ALL = every node + gather; SFB_PART_LOW = nodes of both boundary plane
+// groups (boundary stream); SFB_PART_INTERIOR = remaining nodes + gather
+void step_points(Plan& P, int op, long long t, int part) {
+    const OpRoles ro = roles(op);
+    const int cur = int(t & 1), oth = cur ^ 1;
+    const long long tnew = ro.backward ? t - 1 : t + 1;
+    Cloud& ci = P.cloud[ro.inj];
+    require(ci.has_in, SFB_ERR_BINDING, "no traces uploaded for the injected cloud");
+    struct Range {
+        long long b, e;
+    };
+    Range rg[2] = {{0, 0}, {0, 0}};
+    int nr = 1;
+    bool gather = false;
+    if (part == SFB_PART_ALL) {
+        rg[0] = {0, ci.ncell};
+        gather = ro.smp >= 0;
+    } else if (part == SFB_PART_LOW || part == SFB_PART_HIGH) {
+        rg[0] = {0, ci.cell_lo_end};
+        rg[1] = {ci.cell_hi_begin, ci.ncell};
+        nr = 2;
+    } else {
+        rg[0] = {ci.cell_lo_end, ci.cell_hi_begin};
+        gather = ro.smp >= 0;
+    }
+    cudaStream_t st = part_stream(P, part);
+    for (int i = 0; i < nr; ++i) {
+        const bool do_gather = gather && i == 0;
+        const long long ncell = std::max<long long>(0, rg[i].e - rg[i].b);
+        if (ncell == 0 && !do_gather) continue;
+        PointParams pp{};
+        pp.ncell = int(ncell);
+        pp.cell_start = ci.cell_start.as<int>() + rg[i].b;
+        pp.cell_u = ci.cell_u.as<long long>() + rg[i].b;
+        pp.cell_c = ci.cell_c.as<long long>() + rg[i].b;
+        pp.ent_point = ci.ent_point.as<int>();
+        pp.ent_w = ci.ent_w.as<float>();
+        pp.inj_row = ci.tr_in.as<float>() + t * ci.np;
+        pp.target = P.u[oth].as<float>();
+        pp.r = P.r.as<float>();
+        pp.inv_dt2 = P.coef.inv_dt2;
+        if (op == SFB_OP_FORWARD && P.save_every > 0 && tnew % P.save_every == 0)
+            pp.snap = P.snaps.as<float>() + (tnew / P.save_every) * P.ccount;
+        if (ro.imaging && t % P.save_every == 0) {
+            pp.usave = P.snaps.as<float>() + (t / P.save_every) * P.ccount;
+            pp.grad = P.grad.as<float>();
+        }
+        int nb_smp = 0;
+        if (do_gather) {
+            Cloud& cs = P.cloud[ro.smp];
+            pp.nsmp = int(cs.np);
+            pp.smp_idx = cs.smp_idx.as<long long>();
+            pp.smp_w = cs.smp_w.as<float>();
+            pp.field = P.u[cur].as<float>();
+            pp.smp_row = cs.tr_out.as<float>() + t * cs.np;
+            pp.ncorner = 1 << P.ndim;
+            const int off = 3 - P.ndim;
+            for (int c = 0; c < pp.ncorner; ++c) {
+                long long o = 0;
+                for (int a = 0; a < P.ndim; ++a)
+                    if ((c >> a) & 1) o += (off + a == 0) ? P.plane : (off + a == 1 ? P.pitch : 1);
+                pp.corner_off[c] = o;
+            }
+            nb_smp = int((cs.np + kPointThreads - 1) / kPointThreads);
+        }
+        const int nb_inj = int((ncell + kPointThreads - 1) / kPointThreads);
+        if (nb_inj + nb_smp == 0) continue;
+        point_step_kernel<<<nb_inj + nb_smp, kPointThreads, 0, st>>>(pp, nb_inj);
+        SFB_CUDA(cudaGetLastError());
+        ++P.launches;
+    }
+    mark_stream(P, part);
+}
+
+void finite_guard(Plan& P, const char* what) {
+    P.flag.alloc(sizeof(int), false);
+    SFB_CUDA(cudaMemsetAsync(P.flag.p, 0, sizeof(int), P.s_main));
+    for (int b = 0; b < 2; ++b) {
+        finite_check_kernel<<<P.sm_count * 8, 256, 0, P.s_main>>>(P.u[b].as<float>(), P.ucount,
+                                                                 P.flag.as<int>());
+        SFB_CUDA(cudaGetLastError());
+    }
+    int bad = 0;
+    SFB_CUDA(cudaMemcpyAsync(&bad, P.flag.p, sizeof(int), cudaMemcpyDeviceToHost, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    if (bad) throw Failure(SFB_ERR_STABILITY, std::string(what) + ": wavefield went non-finite");
+}
+
+void run_op(Plan& P, int op, long long save_every, sfb_report* rep) {
+    const OpRoles ro = roles(op);
+    step_begin(P, op, save_every);
+    const long long nt = P.desc.nt;
+    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+    if (!ro.backward) {
+        for (long long t = 1; t < nt - 1; ++t) {
+            step_compute(P, op, t, SFB_PART_ALL);
+            step_points(P, op, t, SFB_PART_ALL);
+        }
+    } else {
+        for (long long t = nt - 2; t >= 1; --t) {
+            step_compute(P, op, t, SFB_PART_ALL);
+            step_points(P, op, t, SFB_PART_ALL);
+        }
+    }
+    SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    float ms = 0.f;
+    SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+    finite_guard(P, op == SFB_OP_FORWARD ? "forward" : (op == SFB_OP_ADJOINT ? "adjoint" : "gradient"));
+    if (op == SFB_OP_FORWARD && save_every > 0) P.history_valid = true;
+    if (rep) {
+        const long steps = long(std::max<long long>(0, nt - 2));
+        int D = P.ndim;
+        const long long fpp = 3LL * P.K * D + 3LL * D + 11 + (ro.imaging ? 7 : 0);
+        const double pts = double(P.N[0]) * double(P.N[1]) * double(P.N[2]);
+        const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
+        rep->seconds = ms * 1e-3;
+        rep->steps = steps;
+        rep->flops = (long long)(double(fpp) * own * steps);
+        rep->gflops = rep->seconds > 0 ? double(rep->flops) / rep->seconds / 1e9 : 0.0;
+        rep->gpts_per_s = rep->seconds > 0 ? own * steps / rep->seconds / 1e9 : 0.0;
+        rep->kernel_launches = P.launches;
+        (void)pts;
+    }
+}
+
+}  // namespace
+}  // namespace sfb
+
+using namespace sfb;
+
+extern "C" {
+
+SFB_API int sfb_abi_version(void) { return SFB_ABI_VERSION; }
+
+SFB_API const char* sfb_last_error(const sfb_plan* plan) {
+    return plan ? plan->err.c_str() : g_create_err.c_str();
+}
+
+SFB_API int sfb_device_count(int* count) {
+    if (!count) return SFB_ERR_PARAMETER;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    *count = n;
+    return SFB_OK;
+}
+
+SFB_API int sfb_fd_weights(int deriv_order, int space_order, double* out) {
+    std::vector<Frac> w;
+    if (!out || !centred_weights(deriv_order, space_order, w)) {
+        g_create_err = "centered stencils require an even accuracy order in [2, 16]";
+        return SFB_ERR_ORDER;
+    }
+    for (size_t j = 0; j < w.size(); ++j) out[j] = to_double(w[j]);
+    return SFB_OK;
+}
+
+SFB_API int sfb_critical_dt(int ndim, const double* spacing, double v_max, int space_order,
+                    double* out) {
+    // SeismicModel::critical_dt, proj/src/model.cpp:103-111 (gamma = 1)
+    std::vector<Frac> w;
+    if (!out || !spacing || ndim < 1 || ndim > 3 || !(v_max > 0.0) ||
+        !centred_weights(2, space_order, w)) {
+        g_create_err = "critical_dt: bad arguments";
+        return SFB_ERR_PARAMETER;
+    }
+    double wsum = std::abs(to_double(w[0]));
+    for (size_t j = 1; j < w.size(); ++j) wsum += 2.0 * std::abs(to_double(w[j]));
+    double h_min = spacing[0];
+    for (int a = 1; a < ndim; ++a) h_min = std::min(h_min, spacing[a]);
+    const double m_min = 1.0 / (v_max * v_max);
+    *out = h_min * std::sqrt(m_min) / std::sqrt(double(ndim) * wsum / 2.0);
+    return SFB_OK;
+}
+
+SFB_API int sfb_locate(const sfb_plan_desc* desc, const double* origin, int64_t np,
+               const double* coords, int64_t* base, double* w) {
+    // SparseFunction::locate, proj/src/sparse.cpp:36-70
+    if (!desc || !origin || !coords || !base || !w || desc->ndim < 1 || desc->ndim > 3) {
+        g_create_err = "locate: bad arguments";
+        return SFB_ERR_PARAMETER;
+    }
+    const int nd = desc->ndim, nc = 1 << nd;
+    for (int64_t p = 0; p < np; ++p) {
+        double frac[3];
+        for (int d = 0; d < nd; ++d) {
+            double rel = (coords[p * nd + d] - origin[d]) / desc->spacing[d];
+            const double last = double(desc->shape[d] - 1);
+            const double tol = 1e-9 * std::max(1.0, last);
+            if (rel < -tol || rel > last + tol) {
+                char buf[160];
+                std::snprintf(buf, sizeof buf, "point %ld axis %d: coordinate %g outside domain",
+                              long(p), d, coords[p * nd + d]);
+                g_create_err = buf;
+                return SFB_ERR_LOCATION;
+            }
+            rel = std::min(std::max(rel, 0.0), last);
+            int64_t b = int64_t(std::floor(rel));
+            if (b > desc->shape[d] - 2) b = desc->shape[d] - 2;
+            base[p * nd + d] = b;
+            frac[d] = rel - double(b);
+        }
+        for (int c = 0; c < nc; ++c) {
+            double ww = 1.0;
+            for (int d = 0; d < nd; ++d) ww *= ((c >> d) & 1) ? frac[d] : 1.0 - frac[d];
+            w[p * nc + c] = ww;
+        }
+    }
+    return SFB_OK;
+}
+
+SFB_API int sfb_plan_create(const sfb_plan_desc* desc, sfb_plan** out) {
+    if (out) *out = nullptr;
+    sfb_plan* plan = nullptr;
+    int rc = guarded(nullptr, [&] {
+        require(desc && out, SFB_ERR_PARAMETER, "plan_create: null argument");
+        require(desc->ndim >= 1 && desc->ndim <= 3, SFB_ERR_PARAMETER,
+                "grid rank must be 1, 2 or 3");
+        for (int a = 0; a < desc->ndim; ++a) {
+            require(desc->shape[a] >= 2, SFB_ERR_PARAMETER, "grid extent must be >= 2 nodes");
+            require(desc->spacing[a] > 0.0, SFB_ERR_PARAMETER, "grid spacing must be positive");
+            require(desc->shape[a] < (1LL << 30), SFB_ERR_PARAMETER, "grid extent too large");
+        }
+        if (desc->space_order < 2 || desc->space_order % 2 != 0)
+            throw Failure(SFB_ERR_ORDER, "space order must be a positive even number");
+        if (desc->space_order > 2 * kMaxK)
+            throw Failure(SFB_ERR_ORDER, "space orders above 16 are not built");
+        require(desc->dt > 0.0 && desc->nt >= 1, SFB_ERR_PARAMETER, "bad time axis");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            throw Failure(SFB_ERR_CAPABILITY,
+                          "no CUDA device: this engine has no CPU fallback");
+        }
+        require(desc->device >= 0 && desc->device < ndev, SFB_ERR_PARAMETER,
+                "device ordinal out of range");
+        cudaDeviceProp prop;
+        SFB_CUDA(cudaGetDeviceProperties(&prop, desc->device));
+        if (prop.major != 10)
+            throw Failure(SFB_ERR_CAPABILITY,
+                          std::string("device ") + prop.name +
+                              " is not sm_100: kernels are built for sm_100a only");
+        SFB_CUDA(cudaSetDevice(desc->device));
+
+        plan = new sfb_plan_s();
+        Plan& P = *plan;
+        P.desc = *desc;
+        P.device = desc->device;
+        P.sm_count = prop.multiProcessorCount;
+        P.ndim = desc->ndim;
+        P.K = desc->space_order / 2;
+        const int off = 3 - P.ndim;
+        for (int a = 0; a < P.ndim; ++a) {
+            P.N[off + a] = desc->shape[a];
+            P.h[off + a] = desc->spacing[a];
+            P.act[off + a] = true;
+        }
+        P.z_lo = desc->slab_lo;
+        P.z_hi = desc->slab_hi;
+        if (P.z_lo == 0 && P.z_hi == 0) P.z_hi = P.N[0];
+        require(P.z_lo >= 0 && P.z_lo < P.z_hi && P.z_hi <= P.N[0], SFB_ERR_PARAMETER,
+                "slab range outside the slowest axis");
+        P.n0 = int(P.z_hi - P.z_lo);
+        if (P.n0 != P.N[0])
+            require(P.n0 >= 2 * P.K, SFB_ERR_PARAMETER,
+                    "a slab must hold at least space_order planes");
+        P.pitch = int(round_up(P.N[2], 32));
+        P.plane = (long long)P.N[1] * P.pitch;
+        P.ucount = (long long)(P.n0 + 2 * P.K) * P.plane;
+        P.ccount = (long long)P.n0 * P.plane;
+
+        std::vector<Frac> w;
+        centred_weights(2, desc->space_order, w);
+        for (int j = 0; j <= P.K; ++j) P.w2[j] = to_double(w[j]);
+        double ih2[3];
+        double c0 = 0.0;
+        for (int d = 0; d < 3; ++d) {
+            ih2[d] = P.act[d] ? 1.0 / (P.h[d] * P.h[d]) : 0.0;
+            c0 += P.w2[0] * ih2[d];
+        }
+        P.coef.c0 = float(c0);
+        for (int j = 1; j <= P.K; ++j) {
+            P.coef.cz[j - 1] = float(P.w2[j] * ih2[0]);
+            P.coef.cy[j - 1] = float(P.w2[j] * ih2[1]);
+            P.coef.cx[j - 1] = float(P.w2[j] * ih2[2]);
+        }
+        P.coef.qscale = float(0.5 / desc->dt);
+        P.coef.inv_dt2 = float(1.0 / (desc->dt * desc->dt));
+
+        SFB_CUDA(cudaStreamCreateWithFlags(&P.s_main, cudaStreamNonBlocking));
+        int lo_pri = 0, hi_pri = 0;
+        SFB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+        SFB_CUDA(cudaStreamCreateWithPriority(&P.s_bnd, cudaStreamNonBlocking, hi_pri));
+        SFB_CUDA(cudaEventCreateWithFlags(&P.ev_main, cudaEventDisableTiming));
+        SFB_CUDA(cudaEventCreateWithFlags(&P.ev_bnd, cudaEventDisableTiming));
+        SFB_CUDA(cudaEventCreate(&P.ev_t0));
+        SFB_CUDA(cudaEventCreate(&P.ev_t1));
+        P.u[0].alloc(size_t(P.ucount) * 4);
+        P.u[1].alloc(size_t(P.ucount) * 4);
+        select_variant(P, 0, 0, 0);
+        *out = plan;
+    });
+    if (rc != SFB_OK && plan) {
+        std::string keep = g_create_err;
+        sfb_plan_destroy(plan);
+        g_create_err = keep;
+    }
+    return rc;
+}
+
+SFB_API int sfb_plan_destroy(sfb_plan* plan) {
+    if (!plan) return SFB_OK;
+    cudaSetDevice(plan->device);
+    cudaDeviceSynchronize();
+    if (plan->own_streams) {
+        if (plan->s_main) cudaStreamDestroy(plan->s_main);
+        if (plan->s_bnd) cudaStreamDestroy(plan->s_bnd);
+    }
+    if (plan->ev_main) cudaEventDestroy(plan->ev_main);
+    if (plan->ev_bnd) cudaEventDestroy(plan->ev_bnd);
+    if (plan->ev_t0) cudaEventDestroy(plan->ev_t0);
+    if (plan->ev_t1) cudaEventDestroy(plan->ev_t1);
+    delete plan;
+    return SFB_OK;
+}
+
+SFB_API int sfb_set_model(sfb_plan* plan, const sfb_field_view* m, const sfb_field_view* damp,
+                  double v_max) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(m && damp && m->ptr && damp->ptr, SFB_ERR_PARAMETER, "set_model: null field");
+        if (v_max > 0.0) {
+            // check_cfl, proj/src/seismic_ops.cpp:15-22
+            double crit = 0;
+            sfb_critical_dt(P.ndim, P.desc.spacing, v_max, P.desc.space_order, &crit);
+            if (P.desc.dt > crit * (1.0 + 1e-12))
+                throw Failure(SFB_ERR_STABILITY,
+                              "dt " + std::to_string(P.desc.dt) + " exceeds the stable limit " +
+                                  std::to_string(crit) + " at order " +
+                                  std::to_string(P.desc.space_order));
+        }
+        P.v_max = v_max;
+        const long long rows = (long long)P.n0 * P.N[1];
+        DevBuf tmp;
+        P.r.alloc(size_t(P.ccount) * 4);
+        P.damp.alloc(size_t(P.ccount) * 4);
+        upload_f64(P, embed_view(P, m->ptr, m->stride), tmp);
+        convert_r_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(
+            tmp.as<double>(), P.r.as<float>(), rows, int(P.N[2]), P.pitch,
+            P.desc.dt * P.desc.dt);
+        SFB_CUDA(cudaGetLastError());
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        upload_f64(P, embed_view(P, damp->ptr, damp->stride), tmp);
+        convert_f64_f32_pitched<<<row_grid(P, rows), 256, 0, P.s_main>>>(
+            tmp.as<double>(), P.damp.as<float>(), rows, int(P.N[2]), P.pitch);
+        SFB_CUDA(cudaGetLastError());
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        P.model_set = true;
+        P.history_valid = false;
+    });
+}
+
+SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view*, const sfb_field_view*,
+                      const sfb_field_view*, const sfb_field_view*) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    plan->err = "TTI operator is not built in this round";
+    return SFB_ERR_CAPABILITY;
+}
+
+SFB_API int sfb_set_points(sfb_plan* plan, int cloud, int64_t np, const int64_t* base,
+                   const double* w) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(cloud == SFB_CLOUD_SRC || cloud == SFB_CLOUD_REC, SFB_ERR_PARAMETER,
+                "unknown cloud id");
+        require(np >= 1 && base && w, SFB_ERR_PARAMETER, "set_points: empty point table");
+        require(np < (1LL << 31), SFB_ERR_PARAMETER, "too many points");
+        Cloud& c = P.cloud[cloud];
+        c.np = np;
+        c.base.assign(base, base + np * P.ndim);
+        c.w.assign(w, w + np * (1 << P.ndim));
+        build_cloud(P, c);
+    });
+}
+
+SFB_API int sfb_upload_traces(sfb_plan* plan, int cloud, const double* traces) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        require(cloud == 0 || cloud == 1, SFB_ERR_PARAMETER, "unknown cloud id");
+        require(plan->cloud[cloud].set && traces, SFB_ERR_BINDING, "point cloud is not bound");
+        upload_traces(*plan, plan->cloud[cloud], traces);
+    });
+}
+
+SFB_API int sfb_download_traces(sfb_plan* plan, int cloud, double* traces) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        require(cloud == 0 || cloud == 1, SFB_ERR_PARAMETER, "unknown cloud id");
+        require(plan->cloud[cloud].set && traces, SFB_ERR_BINDING, "point cloud is not bound");
+        download_traces(*plan, plan->cloud[cloud], traces);
+    });
+}
+
+SFB_API int sfb_run_resident(sfb_plan* plan, int op, int64_t save_every, sfb_report* report) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] { run_op(*plan, op, save_every, report); });
+}
+
+SFB_API int sfb_run_steps(sfb_plan* plan, int op, int64_t t_from, int64_t t_to, sfb_report* report) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        const OpRoles ro = roles(op);
+        require(t_from >= 1 && t_to <= P.desc.nt - 1 && t_from <= t_to, SFB_ERR_PARAMETER,
+                "run_steps: window outside [1, nt-1)");
+        const long before = P.launches;
+        SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+        if (!ro.backward) {
+            for (long long t = t_from; t < t_to; ++t) {
+                step_compute(P, op, t, SFB_PART_ALL);
+                step_points(P, op, t, SFB_PART_ALL);
+            }
+        } else {
+            for (long long t = t_to - 1; t >= t_from; --t) {
+                step_compute(P, op, t, SFB_PART_ALL);
+                step_points(P, op, t, SFB_PART_ALL);
+            }
+        }
+        SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        float ms = 0.f;
+        SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+        if (report) {
+            const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
+            const long long fpp = 3LL * P.K * P.ndim + 3LL * P.ndim + 11 + (ro.imaging ? 7 : 0);
+            report->seconds = ms * 1e-3;
+            report->steps = long(t_to - t_from);
+            report->flops = (long long)(double(fpp) * own * double(report->steps));
+            report->gflops = ms > 0 ? double(report->flops) / (ms * 1e-3) / 1e9 : 0.0;
+            report->gpts_per_s = ms > 0 ? own * double(report->steps) / (ms * 1e-3) / 1e9 : 0.0;
+            report->kernel_launches = P.launches - before;
+        }
+    });
+}
+
+SFB_API int sfb_forward(sfb_plan* plan, const double* src, double* rec, int64_t save_every,
+                sfb_report* report) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(src && rec, SFB_ERR_PARAMETER, "forward: null trace table");
+        require(P.cloud[0].set && P.cloud[1].set, SFB_ERR_BINDING, "point clouds are not bound");
+        upload_traces(P, P.cloud[SFB_CLOUD_SRC], src);
+        run_op(P, SFB_OP_FORWARD, save_every, report);
+        download_traces(P, P.cloud[SFB_CLOUD_REC], rec);
+    });
+}
+
+SFB_API int sfb_adjoint(sfb_plan* plan, const double* rec, double* srca, sfb_report* report) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(rec && srca, SFB_ERR_PARAMETER, "adjoint: null trace table");
+        require(P.cloud[0].set && P.cloud[1].set, SFB_ERR_BINDING, "point clouds are not bound");
+        upload_traces(P, P.cloud[SFB_CLOUD_REC], rec);
+        run_op(P, SFB_OP_ADJOINT, 0, report);
+        download_traces(P, P.cloud[SFB_CLOUD_SRC], srca);
+    });
+}
+
+SFB_API int sfb_gradient(sfb_plan* plan, const double* resid, const sfb_field_mview* grad,
+                 sfb_report* report) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(resid && grad && grad->ptr, SFB_ERR_PARAMETER, "gradient: null argument");
+        require(P.cloud[1].set, SFB_ERR_BINDING, "receiver cloud is not bound");
+        require(P.history_valid && P.save_every > 0, SFB_ERR_PARAMETER,
+                "gradient_operator: saved forward history required");
+        upload_traces(P, P.cloud[SFB_CLOUD_REC], resid);
+        run_op(P, SFB_OP_GRADIENT, P.save_every, report);
+        download_field(P, P.grad.as<float>(), grad);
+    });
+}
+
+SFB_API int sfb_tti_forward(sfb_plan* plan, const double*, double*, sfb_report*) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    plan->err = "TTI operator is not built in this round";
+    return SFB_ERR_CAPABILITY;
+}
+
+SFB_API int sfb_get_wavefield(sfb_plan* plan, int field, int64_t level, const sfb_field_mview* out) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(out && out->ptr && field == 0, SFB_ERR_PARAMETER, "get_wavefield: bad argument");
+        for (int b = 0; b < 2; ++b)
+            if (P.live_level[b] == level) {
+                download_field(P, P.u[b].as<float>() + (long long)P.K * P.plane, out);
+                return;
+            }
+        if (P.history_valid && P.save_every > 0 && level >= 0 && level % P.save_every == 0 &&
+            level / P.save_every < P.nslots) {
+            download_field(P, P.snaps.as<float>() + (level / P.save_every) * P.ccount, out);
+            return;
+        }
+        throw Failure(SFB_ERR_PARAMETER, "time level " + std::to_string(level) +
+                                             " is neither live nor saved");
+    });
+}
+
+SFB_API int sfb_step_begin(sfb_plan* plan, int op, int64_t save_every) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        if (op == SFB_OP_GRADIENT) save_every = plan->save_every;
+        step_begin(*plan, op, save_every);
+    });
+}
+
+SFB_API int sfb_step_compute(sfb_plan* plan, int op, int64_t t, int part) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] { step_compute(*plan, op, t, part); });
+}
+
+SFB_API int sfb_step_points(sfb_plan* plan, int op, int64_t t, int part) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] { step_points(*plan, op, t, part); });
+}
+
+SFB_API int sfb_step_end(sfb_plan* plan, int op) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        if (P.s_bnd != P.s_main) SFB_CUDA(cudaStreamSynchronize(P.s_bnd));
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        finite_guard(P, "slab step");
+        if (op == SFB_OP_FORWARD && P.save_every > 0) P.history_valid = true;
+    });
+}
+
+SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, void** send_hi,
+                    void** recv_lo, void** recv_hi, int64_t* count) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        roles(op);
+        // both operators write the new level into the buffer of parity (t+1)&1
+        float* u = P.u[(t + 1) & 1].as<float>();
+        const long long blk = (long long)P.K * P.plane;
+        if (recv_lo) *recv_lo = u;
+        if (send_lo) *send_lo = u + blk;
+        if (send_hi) *send_hi = u + (long long)P.n0 * P.plane;
+        if (recv_hi) *recv_hi = u + (long long)(P.n0 + P.K) * P.plane;
+        if (count) *count = blk;
+    });
+}
+
+SFB_API int sfb_stream_sync(sfb_plan* plan) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        if (plan->s_bnd != plan->s_main) SFB_CUDA(cudaStreamSynchronize(plan->s_bnd));
+        SFB_CUDA(cudaStreamSynchronize(plan->s_main));
+    });
+}
+
+SFB_API int sfb_streams(sfb_plan* plan, void** main_stream, void** boundary_stream) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    if (main_stream) *main_stream = plan->s_main;
+    if (boundary_stream) *boundary_stream = plan->s_bnd;
+    return SFB_OK;
+}
+
+SFB_API int sfb_set_streams(sfb_plan* plan, void* main_stream, void* boundary_stream) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        SFB_CUDA(cudaDeviceSynchronize());
+        if (P.own_streams) {
+            cudaStreamDestroy(P.s_main);
+            cudaStreamDestroy(P.s_bnd);
+        }
+        P.own_streams = false;
+        P.s_main = static_cast<cudaStream_t>(main_stream);
+        P.s_bnd = static_cast<cudaStream_t>(boundary_stream);
+    });
+}
+
+SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_t count) {
+    if (!dst_plan) return SFB_ERR_PARAMETER;
+    return guarded(dst_plan, [&] {
+        SFB_CUDA(cudaMemcpyAsync(dst, src, size_t(count) * 4, cudaMemcpyDeviceToDevice,
+                                 dst_plan->s_main));
+    });
+}
+
+SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int r, int chunk) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        select_variant(*plan, txv, ty, r);
+        if (chunk > 0) plan->chunk = std::min(chunk, plan->n0);
+    });
+}
+
+SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* r, int* nst, int* chunk, int* sep) {
+    if (!plan || !plan->variant) return SFB_ERR_PARAMETER;
+    if (txv) *txv = plan->variant->TXV;
+    if (ty) *ty = plan->variant->TY;
+    if (r) *r = plan->variant->R;
+    if (nst) *nst = plan->variant->NST;
+    if (chunk) *chunk = plan->chunk;
+    if (sep) *sep = plan->variant->sep ? 1 : 0;
+    return SFB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// plan.hpp -- host-side state behind an sfb_plan handle.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sfb200.h"
+#include "acoustic_kernel.cuh"
+#include "variants.hpp"
+
+namespace sfb {
+
+struct Failure : std::runtime_error {
+    int code;
+    Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SFB_CUDA(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw sfb::Failure(SFB_ERR_CUDA, std::string(#expr) + ": " +                \
+                                                 cudaGetErrorString(e_));               \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void alloc(size_t n, bool zero = true) {
+        if (n > bytes || !p) {
+            release();
+            if (n == 0) n = 16;
+            cudaError_t e = cudaMalloc(&p, n);
+            if (e != cudaSuccess)
+                throw Failure(SFB_ERR_CUDA, "cudaMalloc of " + std::to_string(n) +
+                                                " bytes: " + cudaGetErrorString(e));
+            bytes = n;
+        }
+        if (zero) {
+            SFB_CUDA(cudaMemsetAsync(p, 0, bytes, cudaStreamPerThread));
+            SFB_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+        }
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// One sparse point cloud (sources or receivers) in both of its roles.
+struct Cloud {
+    long long np = 0;
+    bool set = false;
+    std::vector<long long> base;  // [np][ndim] global
+    std::vector<double> w;        // [np][2^ndim]
+    // scatter role (CSR by destination node, nodes sorted by compact index)
+    long long ncell = 0, nent = 0;
+    long long cell_lo_end = 0, cell_hi_begin = 0;  // nodes in the low / high boundary planes
+    DevBuf cell_start, cell_u, cell_c, ent_point, ent_w;
+    std::vector<int> h_cell_start;
+    // gather role
+    DevBuf smp_idx, smp_w;
+    // traces, fp32 [nt][np]
+    DevBuf tr_in, tr_out;
+    bool has_in = false;
+};
+
+struct Plan {
+    sfb_plan_desc desc{};
+    int K = 0;
+    int ndim = 0;
+    long long N[3] = {1, 1, 1};   // embedded global extents
+    double h[3] = {1, 1, 1};
+    bool act[3] = {false, false, false};
+    long long z_lo = 0, z_hi = 0; // owned planes of embedded axis 0
+    int n0 = 0;                   // owned plane count
+    int pitch = 0;
+    long long plane = 0;          // floats per plane
+    long long ucount = 0;         // floats per wavefield buffer (with ghost planes)
+    long long ccount = 0;         // floats per compact array
+    double w2[kMaxK + 1] = {0};
+    StencilCoef coef{};
+
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t s_main = nullptr, s_bnd = nullptr;
+    bool own_streams = true;
+    cudaEvent_t ev_main = nullptr, ev_bnd = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    bool main_pending = false, bnd_pending = false;
+
+    DevBuf u[2], r, damp, dz, dy, dx, grad, snaps, flag;
+    CUtensorMap tm[2];
+    bool model_set = false, sep = false;
+    double v_max = 0;
+
+    Cloud cloud[2];
+
+    const StepVariant* variant = nullptr;       // chosen tile shape
+    int chunk = 0;                              // output planes per block
+
+    // history of the last forward run
+    long long save_every = 0, nslots = 0;
+    bool history_valid = false;
+    long long live_level[2] = {-1, -1};         // time level held by u[0], u[1]
+    long long step_save_every = 0;              // save_every of the op being stepped
+    long launches = 0;
+
+    std::string err;
+};
+
+}  // namespace sfb
+
+struct sfb_plan_s : sfb::Plan {};

@@ -1,0 +1,200 @@
+"""GPU parity: CUDA path (through the C-ABI) vs the f64 CPU oracle on the same seeded inputs.
+
+Tolerances are BASELINE.json's: wavefields and traces rel-L2 <= 1e-5 after 100 steps and
+<= 1e-4 after a full run; gradients <= 1e-3; dot test <= 1e-4 (fp32 arithmetic against an
+f64 oracle)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+from tests.common import make_plan, make_problem, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _forward_both(shape, h, nbl, order, nsteps, **kw):
+    model, geom = make_problem(shape, h, nbl, order, nsteps, **kw)
+    ref = o.forward(model, geom, order, want_final=True)
+    plan = make_plan(model, geom, order)
+    rec, rep = plan.forward(geom.src)
+    u = plan.wavefield(geom.nt - 1)
+    up = plan.wavefield(geom.nt - 2)
+    return model, geom, ref, plan, rec, u, up, rep
+
+
+@pytest.mark.parametrize("order", [2, 4, 6, 8, 10, 12, 14, 16])
+def test_forward_parity_3d_orders(order):
+    _, geom, ref, plan, rec, u, up, rep = _forward_both([40, 36, 44], 10.0, 8, order, 100)
+    assert rep.steps == 100 and rep.kernel_launches == 200
+    assert np.abs(ref["smp"]).max() > 0
+    assert rel_l2(rec, ref["smp"]) <= 1e-5
+    assert rel_l2(u, ref["final"]) <= 1e-5
+    assert rel_l2(up, ref["prev"]) <= 1e-5
+    assert (rec[[0, 1, geom.nt - 1]] == 0.0).all()  # structural zeros, seismic_ops.hpp:13-16
+    plan.close()
+
+
+def test_forward_parity_ragged_sizes():
+    # extents that are not multiples of any tile or of 4
+    _, _, ref, plan, rec, u, _, _ = _forward_both([37, 45, 53], 12.5, 9, 8, 80)
+    assert rel_l2(rec, ref["smp"]) <= 1e-5 and rel_l2(u, ref["final"]) <= 1e-5
+    plan.close()
+
+
+def test_forward_parity_2d():
+    _, _, ref, plan, rec, u, _, _ = _forward_both([70, 90], 10.0, 10, 4, 120)
+    assert rel_l2(rec, ref["smp"]) <= 1e-5 and rel_l2(u, ref["final"]) <= 1e-5
+    plan.close()
+
+
+def test_forward_long_run_two_layer():
+    # config-1 style medium (two layers split on the depth axis), 400 steps
+    shape = [41, 41, 41]
+    vel = np.empty(shape)
+    vel[..., :20] = 1.5
+    vel[..., 20:] = 2.5
+    _, _, ref, plan, rec, u, _, _ = _forward_both(shape, 10.0, 20, 4, 400, vel=vel, f0=0.01)
+    assert rel_l2(rec, ref["smp"]) <= 1e-4 and rel_l2(u, ref["final"]) <= 1e-4
+    plan.close()
+
+
+def test_tile_shapes_agree_bitwise():
+    model, geom = make_problem([40, 36, 44], 10.0, 8, 8, 40)
+    plan = make_plan(model, geom, 8)
+    base, _ = plan.forward(geom.src)
+    u0 = plan.wavefield(geom.nt - 1)
+    for tile in [(16, 32, 1), (32, 8, 1), (16, 32, 2)]:
+        for chunk in (0, 7, 60):
+            plan.set_tile(*tile, chunk)
+            rec, _ = plan.forward(geom.src)
+            assert np.array_equal(rec, base)
+            assert np.array_equal(plan.wavefield(geom.nt - 1), u0)
+    plan.close()
+
+
+def test_zero_source_gives_zero_receivers():  # proj/tests/test_seismic.cpp:165-174
+    model, geom = make_problem([24, 24, 24], 10.0, 6, 8, 50)
+    plan = make_plan(model, geom, 8)
+    rec, _ = plan.forward(np.zeros_like(geom.src))
+    assert (rec == 0.0).all() and (plan.wavefield(geom.nt - 1) == 0.0).all()
+    plan.close()
+
+
+def test_adjoint_parity_and_dot_test():  # proj/src/verify.cpp:201-253
+    model, geom = make_problem([36, 32, 40], 10.0, 8, 6, 120, f0=0.01, dt_frac=0.8)
+    o.forward(model, geom, 6)
+    ref = o.adjoint(model, geom, 6, want_final=True)
+    plan = make_plan(model, geom, 6)
+    rec, _ = plan.forward(geom.src)
+    assert rel_l2(rec, geom.rec) <= 1e-5
+    srca, _ = plan.adjoint(geom.rec)
+    assert rel_l2(srca, ref["smp"]) <= 1e-4
+    assert rel_l2(plan.wavefield(0), ref["final"]) <= 1e-4
+    # <F q, d> vs <q, F^T d> with d = F q, all on the GPU path
+    srca_gpu, _ = plan.adjoint(rec)
+    fdot = float((rec ** 2).sum())
+    adot = float((geom.src * srca_gpu).sum())
+    assert fdot > 0 and abs(fdot - adot) / fdot <= 1e-4
+    plan.close()
+
+
+@pytest.mark.parametrize("save_every", [1, 4])
+def test_gradient_parity(save_every):
+    model, geom = make_problem([30, 28, 34], 10.0, 8, 8, 96, dt_frac=0.9)
+    o.forward(model, geom, 8)
+    rng = np.random.default_rng(5)
+    observed = geom.rec + 0.1 * np.abs(geom.rec).max() * rng.standard_normal(geom.rec.shape)
+    observed[[0, 1, geom.nt - 1]] = 0.0
+    phi, gref, resid = o.fwi_gradient(model, geom, observed, 8, save_every)
+    plan = make_plan(model, geom, 8)
+    rec, _ = plan.forward(geom.src, save_every=save_every)
+    g, rep = plan.gradient(rec - observed)
+    gfold = o.fold_gradient(model, g)
+    assert np.abs(gref).max() > 0
+    assert rel_l2(gfold, gref) <= 1e-3
+    assert o.objective(rec, observed) == pytest.approx(phi, rel=1e-4)
+    plan.close()
+
+
+def test_zero_residual_gives_zero_gradient():  # proj/tests/test_seismic.cpp:247-260
+    model, geom = make_problem([20, 20, 20], 10.0, 6, 8, 40)
+    plan = make_plan(model, geom, 8)
+    rec, _ = plan.forward(geom.src, save_every=1)
+    g, _ = plan.gradient(np.zeros_like(rec))
+    assert (g == 0.0).all()
+    plan.close()
+
+
+def test_gradient_requires_history():  # proj/src/seismic_ops.cpp:113-114
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([20, 20, 20], 10.0, 6, 8, 10)
+    plan = make_plan(model, geom, 8)
+    plan.forward(geom.src)
+    with pytest.raises(capi.SfbError) as e:
+        plan.gradient(np.zeros((geom.nt, geom.n_rec)))
+    assert e.value.code == capi.ERR_PARAMETER
+    plan.close()
+
+
+def test_unstable_dt_and_nan_guard():
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([20, 20, 20], 10.0, 6, 8, 60)
+    plan = capi.Plan(model.N, model.spacing, 8, geom.dt * 1.5, geom.nt)
+    with pytest.raises(capi.SfbError) as e:  # check_cfl, seismic_ops.cpp:15-22
+        plan.set_model(model.m, model.damp, model.v_max)
+    assert e.value.code == capi.ERR_STABILITY
+    # with the gate skipped the run itself blows up and the NaN guard fires
+    plan2 = capi.Plan(model.N, model.spacing, 8, geom.dt * 4.0, 400)
+    plan2.set_model(model.m, model.damp, 0.0)
+    plan2.set_points(capi.CLOUD_SRC, geom.src_base, geom.src_w)
+    plan2.set_points(capi.CLOUD_REC, geom.rec_base, geom.rec_w)
+    with pytest.raises(capi.SfbError) as e:
+        plan2.forward(np.ones((400, 1)))
+    assert e.value.code == capi.ERR_STABILITY
+    plan.close()
+    plan2.close()
+
+
+def _run_slabs(model, geom, order, cuts, op_forward=True):
+    """N plans on one device stepping in lockstep with device-to-device ghost copies:
+    the single-GPU emulation of the multi-GPU slab protocol."""
+    from paper_1808_01995_b200 import capi
+    plans = [make_plan(model, geom, order, slab=(cuts[i], cuts[i + 1])) for i in range(len(cuts) - 1)]
+    op = capi.OP_FORWARD
+    for p in plans:
+        p.upload_traces(capi.CLOUD_SRC, geom.src)
+        p.step_begin(op)
+    for t in range(1, geom.nt - 1):
+        for p in plans:
+            p.step_compute(op, t, capi.PART_LOW)
+            p.step_compute(op, t, capi.PART_HIGH)
+            p.step_points(op, t, capi.PART_LOW)
+            p.step_compute(op, t, capi.PART_INTERIOR)
+            p.step_points(op, t, capi.PART_INTERIOR)
+        for p in plans:
+            p.sync()
+        for i in range(len(plans) - 1):
+            a, b = plans[i].halo_blocks(op, t), plans[i + 1].halo_blocks(op, t)
+            plans[i + 1].copy_halo(b["recv_lo"], a["send_hi"], a["count"])
+            plans[i].copy_halo(a["recv_hi"], b["send_lo"], a["count"])
+        for p in plans:
+            p.sync()
+    rec = np.zeros((geom.nt, geom.n_rec))
+    u = np.zeros(model.N)
+    for p in plans:
+        p.step_end(op)
+        rec += p.download_traces(capi.CLOUD_REC)
+        p.wavefield(geom.nt - 1, out=u)
+        p.close()
+    return rec, u
+
+
+def test_slab_decomposition_matches_single_domain_bitwise():
+    model, geom = make_problem([48, 30, 34], 10.0, 8, 8, 60)
+    plan = make_plan(model, geom, 8)
+    rec1, _ = plan.forward(geom.src)
+    u1 = plan.wavefield(geom.nt - 1)
+    plan.close()
+    n0 = model.N[0]
+    rec3, u3 = _run_slabs(model, geom, 8, [0, 20, 41, n0])
+    assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
