@@ -194,11 +194,15 @@ SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_
 
 /* ---- tile shape (the counterpart of the reference's loop-blocking autotune,
  * proj/include/sf/execute.hpp:56): threads along the contiguous axis (x4 nodes each),
- * tile rows, rows per thread, output planes per block (0 = keep).  Only compiled shapes
- * are accepted. */
-SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int rows_per_thread, int chunk);
-SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* rows_per_thread, int* stages,
-                 int* chunk, int* separable_damping);
+ * tile rows, ring stages (0 = any), output planes per block (0 = automatic).  Only
+ * compiled shapes are accepted. */
+SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk);
+SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* stages, int* chunk,
+                         int* separable_damping);
+/* on != 0: always stream the dense damp array, even when it is a sum of 1-D profiles
+ * (build_damping, proj/src/model.cpp:35-56) that the kernel could rebuild on the fly.
+ * Call before sfb_set_model. */
+SFB_API int sfb_set_dense_damping(sfb_plan* plan, int on);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,7 @@ SYMBOLS = [
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_step_begin", "sfb_step_compute",
     "sfb_step_points", "sfb_step_end", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
+    "sfb_set_dense_damping",
 ]
 
 lib.sfb_last_error.restype = C.c_char_p
@@ -73,7 +74,8 @@ lib.sfb_streams.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_voi
 lib.sfb_set_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 lib.sfb_copy_halo.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
 lib.sfb_set_tile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
-lib.sfb_get_tile.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 6
+lib.sfb_get_tile.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 5
+lib.sfb_set_dense_damping.argtypes = [C.c_void_p, C.c_int]
 lib.sfb_fd_weights.argtypes = [C.c_int, C.c_int, C.c_void_p]
 lib.sfb_critical_dt.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double)]
 lib.sfb_locate.argtypes = [C.POINTER(PlanDesc), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -120,7 +122,8 @@ def device_count():
 class Plan:
     """One operator context on one device (sfb_plan)."""
 
-    def __init__(self, shape, spacing, space_order, dt, nt, device=0, slab=None):
+    def __init__(self, shape, spacing, space_order, dt, nt, device=0, slab=None,
+                 dense_damping=False):
         d = PlanDesc()
         d.ndim = len(shape)
         for a in range(len(shape)):
@@ -140,6 +143,8 @@ class Plan:
         if rc:
             raise SfbError(rc, lib.sfb_last_error(None).decode())
         self.np = [0, 0]
+        if dense_damping:
+            self.set_dense_damping(True)
 
     def _chk(self, rc):
         if rc:
@@ -212,13 +217,16 @@ class Plan:
         self._chk(lib.sfb_run_steps(self.h, op, t_from, t_to, C.byref(rep)))
         return rep
 
-    def set_tile(self, txv, ty, r, chunk=0):
-        self._chk(lib.sfb_set_tile(self.h, txv, ty, r, chunk))
+    def set_tile(self, txv, ty, stages=0, chunk=0):
+        self._chk(lib.sfb_set_tile(self.h, txv, ty, stages, chunk))
 
     def get_tile(self):
-        v = [C.c_int() for _ in range(6)]
+        v = [C.c_int() for _ in range(5)]
         self._chk(lib.sfb_get_tile(self.h, *[C.byref(x) for x in v]))
-        return dict(zip(["txv", "ty", "r", "stages", "chunk", "sep"], [x.value for x in v]))
+        return dict(zip(["txv", "ty", "stages", "chunk", "sep"], [x.value for x in v]))
+
+    def set_dense_damping(self, on=True):
+        self._chk(lib.sfb_set_dense_damping(self.h, int(on)))
 
     # slab stepping
     def step_begin(self, op, save_every=0):

@@ -10,15 +10,23 @@
 // The adjoint update (proj/src/seismic_ops.cpp:97-100) is the same expression with the
 // roles of t-1 and t+1 swapped, so this kernel serves forward, adjoint and gradient.
 //
-// Data movement.  u[t] is streamed along the slowest axis d0 in (d1,d2) tiles: a producer
-// warp issues one TMA box load (cp.async.bulk.tensor.3d, zero fill outside the grid =
-// the reference's zero halo, proj/include/sf/function.hpp:17) per plane into a shared
-// memory ring; consumer threads keep the 2K+1 d0 neighbours of their own points in a
-// register queue and read the in-plane neighbours of the centre plane from the ring.
-// u[t-1], r and damp are read once with 128-bit loads and u[t+1] overwrites u[t-1] in
-// place, so a node costs its compulsory 20 bytes (16 with the separable damping
-// profiles).  Optional fused outputs: forward snapshot (save) and the imaging
-// condition grad -= u_saved * v.dt2 (proj/src/seismic_ops.cpp:132).
+// Data movement.  Every global read is a TMA box load (cp.async.bulk.tensor.3d) issued by
+// one producer lane and landing in shared memory behind an mbarrier; out-of-grid elements
+// are zero-filled by the TMA unit, which is the reference's zero halo
+// (proj/include/sf/function.hpp:17).  u[t] is streamed along the slowest axis d0 in
+// (d1,d2) tiles with a (K, KP) halo into a ring of NST planes; consumer threads keep the
+// 2K+1 d0 neighbours of their four nodes in a register queue and read the in-plane
+// neighbours of the centre plane from the ring.  u[t-1], r (and damp) tiles of the output
+// plane go through a second, NAUX-deep ring, so they are prefetched NAUX planes ahead
+// without holding registers.  u[t+1] overwrites u[t-1] in place with one 128-bit store.
+// A node therefore costs its compulsory 20 bytes of HBM traffic (16 when damping is
+// rebuilt from its three 1-D profiles).  Optional fused outputs: forward snapshot and the
+// imaging condition grad -= u_saved * v.dt2 (proj/src/seismic_ops.cpp:132).
+//
+// Synchronisation.  full[s]: TMA completion of ring stage s (+ the aux stage issued with
+// it).  done[i % NAUX]: all consumer warps finished the shared-memory reads of iteration
+// i, which frees u plane i-K's stage and the aux stage of iteration i (NAUX = NST - K
+// makes both the same event).  No block-wide barrier inside the plane loop.
 #pragma once
 
 #include <cuda.h>
@@ -40,12 +48,10 @@ struct StencilCoef {
 
 struct StepParams {
     StencilCoef k;
-    const float* r;      // dt^2/m, compact [n0][N1][pitch]
-    const float* damp;   // dense damping (null when separable)
-    const float* dz;     // separable profiles: damp = dz[i0] + dy[i1] + dx[i2]
+    const float* dz;     // separable damping profiles: damp = dz[i0] + dy[i1] + dx[i2]
     const float* dy;
     const float* dx;
-    float* uo;           // in: level t-1 (t+1 for the adjoint); out: the new level; has K ghost planes per side
+    float* uo;           // level being overwritten (ghost planes included)
     float* snap;         // optional copy of the new level (compact)
     const float* usave;  // optional saved forward level (compact) -> imaging
     float* grad;         // imaging accumulator (compact)
@@ -54,6 +60,11 @@ struct StepParams {
     long long plane;     // floats per plane
     int z_lo, z_hi;      // owned output planes [z_lo, z_hi) handled by this launch
     int chunk;           // output planes per block
+};
+
+// the four tensor maps of one launch: u[t] with halo box; u[t-1], r, damp with plain box
+struct StepMaps {
+    CUtensorMap u, o, r, d;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -94,64 +105,87 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+// 1/x: MUFU.RCP plus one Newton step (branch free; error below 1 ulp for x >= 1)
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return fmaf(y, fmaf(-x, y, 1.f), y);
+}
 
-template <int K, int TXV, int TY, int R, int NST>
+template <int K, int TXV, int TY, int NST, bool SEP>
 struct StepShape {
     static constexpr int KP = (K + 3) & ~3;       // x halo rounded to a float4
     static constexpr int TX = TXV * 4;
     static constexpr int SW = TX + 2 * KP;        // ring row width (floats)
     static constexpr int SH = TY + 2 * K;         // ring rows
-    static constexpr int BOX = SW * SH;           // floats moved per TMA box
+    static constexpr int BOX = SW * SH;           // floats moved per u box
     static constexpr int STAGE = ((BOX + 31) / 32) * 32;
-    static constexpr int NCONS = TXV * (TY / R);  // consumer threads
+    static constexpr int NAUX = NST - K;          // aux ring depth == planes of lookahead + 1
+    static constexpr int NARR = SEP ? 2 : 3;      // aux arrays: u[t-1], r, (damp)
+    static constexpr int ABOX = TX * TY;          // floats per aux box
+    static constexpr int NCONS = TXV * TY;        // consumer threads, four nodes each
     static constexpr int NTHREADS = NCONS + 32;   // + producer warp
-    static constexpr size_t SMEM = size_t(NST) * STAGE * 4 + 2 * NST * 8 + 128;
-    static_assert(TY % R == 0 && NCONS % 32 == 0, "tile shape");
-    static_assert(NST >= K + 2, "ring must hold the centre plane and the newest plane");
+    static constexpr size_t SMEM =
+        size_t(NST) * STAGE * 4 + size_t(NAUX) * NARR * ABOX * 4 + (NST + NAUX) * 8 + 128;
+    static_assert(NCONS % 32 == 0, "tile shape");
+    static_assert(NAUX >= 2, "need at least one plane of lookahead");
+    static_assert((ABOX * 4) % 128 == 0, "aux boxes must keep 128-byte alignment");
 };
 
-template <int K, int TXV, int TY, int R, int NST, bool SEP>
-__global__ void __launch_bounds__(StepShape<K, TXV, TY, R, NST>::NTHREADS)
-acoustic_step_kernel(const __grid_constant__ CUtensorMap tmU,
-                     const __grid_constant__ StepParams p) {
-    using S = StepShape<K, TXV, TY, R, NST>;
+template <int K, int TXV, int TY, int NST, bool SEP>
+__global__ void __launch_bounds__(StepShape<K, TXV, TY, NST, SEP>::NTHREADS)
+acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant__ StepParams p) {
+    using S = StepShape<K, TXV, TY, NST, SEP>;
     constexpr int KP = S::KP, SW = S::SW, STAGE = S::STAGE, Q = 2 * K + 1;
+    constexpr int NAUX = S::NAUX, NARR = S::NARR, ABOX = S::ABOX, TX = S::TX;
     constexpr int NCW = S::NCONS / 32;
 
     extern __shared__ unsigned char smem_raw[];
     const uint32_t mis = smem_u32(smem_raw) & 127u;
     float* ring = reinterpret_cast<float*>(smem_raw + ((128u - mis) & 127u));
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + NST * STAGE);
-    uint64_t* empty = full + NST;
+    float* aux = ring + NST * STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(aux + NAUX * NARR * ABOX);
+    uint64_t* done = full + NST;
 
     const int tid = threadIdx.x;
-    const int x0 = blockIdx.x * S::TX, y0 = blockIdx.y * TY;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const int zb = p.z_lo + blockIdx.z * p.chunk;
     const int ze = min(zb + p.chunk, p.z_hi);
-    const int nplanes = (ze - zb) + 2 * K;  // buffer planes zb .. ze+2K-1 (ghost offset K)
+    const int nplanes = (ze - zb) + 2 * K;  // u buffer planes zb .. ze+2K-1 (ghost offset K)
 
     if (tid == 0) {
 #pragma unroll
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, NCW);
-        }
+        for (int s = 0; s < NST; ++s) mbar_init(full + s, 1);
+#pragma unroll
+        for (int s = 0; s < NAUX; ++s) mbar_init(done + s, NCW);
         mbar_fence_init();
     }
     __syncthreads();
 
     if (tid >= S::NCONS) {
-        // ---- producer warp: one elected lane streams the planes of this block -------
+        // ---- producer warp: one lane streams the planes of this block ----------------
         if (tid == S::NCONS) {
-            int s = 0;
-            uint32_t ph = 0;  // parity of the release that must precede refill
+            int s = 0, a = 0, dph = 0;
             for (int n = 0; n < nplanes; ++n) {
-                if (n >= NST) mbar_wait(empty + s, ph);
-                mbar_arrive_expect_tx(full + s, S::BOX * 4);
-                tma_load_3d(ring + s * STAGE, &tmU, x0 - KP, y0 - K, zb + n, full + s);
-                if (++s == NST) {
-                    s = 0;
-                    if (n >= NST) ph ^= 1;
+                if (n >= NAUX) mbar_wait(done + a, dph);  // iteration n - NAUX is finished
+                const bool out = n >= 2 * K;
+                mbar_arrive_expect_tx(full + s, (S::BOX + (out ? NARR * ABOX : 0)) * 4);
+                tma_load_3d(ring + s * STAGE, &tm.u, x0 - KP, y0 - K, zb + n, full + s);
+                if (out) {
+                    // iteration n uses aux stage (n - 2K) % NAUX; 2K % NAUX is folded into a0
+                    constexpr int A0 = (NAUX - (2 * K) % NAUX) % NAUX;
+                    int as = a + A0;
+                    if (as >= NAUX) as -= NAUX;
+                    float* ad = aux + as * NARR * ABOX;
+                    const int zo = zb + n - 2 * K;
+                    tma_load_3d(ad, &tm.o, x0, y0, zo + K, full + s);
+                    tma_load_3d(ad + ABOX, &tm.r, x0, y0, zo, full + s);
+                    if (!SEP) tma_load_3d(ad + 2 * ABOX, &tm.d, x0, y0, zo, full + s);
+                }
+                if (++s == NST) s = 0;
+                if (++a == NAUX) {
+                    a = 0;
+                    if (n >= NAUX) dph ^= 1;
                 }
             }
         }
@@ -159,197 +193,186 @@ acoustic_step_kernel(const __grid_constant__ CUtensorMap tmU,
     }
 
     // ---- consumers -------------------------------------------------------------------
-    const int tx = tid % TXV, ty0 = (tid / TXV) * R;
-    const int x = x0 + 4 * tx;
-    const bool xin = x < p.N2;
-    bool rin[R];
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) rin[rr] = xin && (y0 + ty0 + rr) < p.N1;
-    const long long rowoff = (long long)(y0 + ty0) * p.pitch + x;
+    const int tx = tid % TXV, ty = tid / TXV;
+    const int x = x0 + 4 * tx, y = y0 + ty;
+    const bool rin = x < p.N2 && y < p.N1;
+    const bool lane0 = (tid & 31) == 0;
 
-    float dxy[R][4];
+    float dxy[4] = {0.f, 0.f, 0.f, 0.f};
+    bool warp_dxy = false;
     if (SEP) {
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
-            float4 dx4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            float dyv = 0.f;
-            if (rin[rr]) {
-                dx4 = __ldg(reinterpret_cast<const float4*>(p.dx + x));
-                dyv = __ldg(p.dy + y0 + ty0 + rr);
-            }
-            dxy[rr][0] = dx4.x + dyv;
-            dxy[rr][1] = dx4.y + dyv;
-            dxy[rr][2] = dx4.z + dyv;
-            dxy[rr][3] = dx4.w + dyv;
+        if (rin) {
+            const float4 dx4 = __ldg(reinterpret_cast<const float4*>(p.dx + x));
+            const float dyv = __ldg(p.dy + y);
+            dxy[0] = dx4.x + dyv;
+            dxy[1] = dx4.y + dyv;
+            dxy[2] = dx4.z + dyv;
+            dxy[3] = dx4.w + dyv;
         }
+        warp_dxy = __any_sync(0xffffffffu, (dxy[0] + dxy[1]) + (dxy[2] + dxy[3]) != 0.f);
     }
 
-    float q[R][Q][4];
+    float q[Q][4];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr)
+    for (int j = 0; j < Q; ++j)
 #pragma unroll
-        for (int j = 0; j < Q; ++j)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) q[rr][j][c] = 0.f;
+        for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
 
-    int s = 0, cs = K;     // ring stage of the newest plane / of the centre plane (plane K is the first centre)
-    uint32_t fph = 0;      // parity of the fill we wait for on stage s
-    const int own = (ty0 + K) * SW + KP + 4 * tx;  // own point inside a stage
+    const int own = (ty + K) * SW + KP + 4 * tx;  // own float4 inside a u stage
+    const int aown = ty * TX + 4 * tx;            // own float4 inside an aux box
+    int s = 0;
+    uint32_t fph = 0;
 
-    for (int n = 0; n < nplanes; ++n) {
+    // prologue: the first 2K planes only fill the register queue
+    for (int n = 0; n < 2 * K; ++n) {
         mbar_wait(full + s, fph);
-        const float* sp = ring + s * STAGE;
+        const float4 v = *reinterpret_cast<const float4*>(ring + s * STAGE + own);
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
-            const float4 v = *reinterpret_cast<const float4*>(sp + own + rr * SW);
-            q[rr][Q - 1][0] = v.x;
-            q[rr][Q - 1][1] = v.y;
-            q[rr][Q - 1][2] = v.z;
-            q[rr][Q - 1][3] = v.w;
-        }
-        if (n < K) {  // the first K planes are d0 halo only: never a centre
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(empty + s);
-        }
-        if (n >= 2 * K) {
-            const int zo = zb + n - 2 * K;
-            const long long gc = (long long)zo * p.plane + rowoff;         // compact arrays
-            const long long gu = (long long)(zo + K) * p.plane + rowoff;   // u buffers
-            float4 r4[R], o4[R], d4[R], g4[R], s4[R];
-            const bool img = p.usave != nullptr;
+        for (int j = 0; j < Q - 1; ++j)
 #pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-                r4[rr] = o4[rr] = d4[rr] = g4[rr] = s4[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (rin[rr]) {
-                    const long long o = (long long)rr * p.pitch;
-                    r4[rr] = __ldcs(reinterpret_cast<const float4*>(p.r + gc + o));
-                    o4[rr] = __ldcs(reinterpret_cast<const float4*>(p.uo + gu + o));
-                    if (!SEP) d4[rr] = __ldcs(reinterpret_cast<const float4*>(p.damp + gc + o));
-                    if (img) {
-                        g4[rr] = __ldcs(reinterpret_cast<const float4*>(p.grad + gc + o));
-                        s4[rr] = __ldcs(reinterpret_cast<const float4*>(p.usave + gc + o));
-                    }
-                }
-            }
-            float dzv = 0.f;
-            if (SEP) dzv = __ldg(p.dz + zo);
-
-            const float* cp = ring + cs * STAGE;
-            float acc[R][4];
-            // centre and streaming-axis neighbours from the register queue
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float a = p.k.c0 * q[rr][K][c];
-#pragma unroll
-                    for (int j = 1; j <= K; ++j)
-                        a = fmaf(p.k.cz[j - 1], q[rr][K - j][c] + q[rr][K + j][c], a);
-                    acc[rr][c] = a;
-                }
-            // contiguous-axis neighbours: one aligned row segment per own row
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-                float xr[2 * KP + 4];
-                const float* rowp = cp + (ty0 + rr + K) * SW + 4 * tx;
-#pragma unroll
-                for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
-                    if (v == KP / 4) {  // own float4: already in the queue
-                        xr[4 * v + 0] = q[rr][K][0];
-                        xr[4 * v + 1] = q[rr][K][1];
-                        xr[4 * v + 2] = q[rr][K][2];
-                        xr[4 * v + 3] = q[rr][K][3];
-                    } else {
-                        const float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
-                        xr[4 * v + 0] = t4.x;
-                        xr[4 * v + 1] = t4.y;
-                        xr[4 * v + 2] = t4.z;
-                        xr[4 * v + 3] = t4.w;
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int j = 1; j <= K; ++j)
-                        acc[rr][c] = fmaf(p.k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], acc[rr][c]);
-            }
-            // d1 neighbours: a column strip of R + 2K rows shared by the R own rows
-            {
-                float col[R + 2 * K][4];
-                const float* colp = cp + ty0 * SW + KP + 4 * tx;
-#pragma unroll
-                for (int i = 0; i < R + 2 * K; ++i) {
-                    if (i >= K && i < K + R) {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) col[i][c] = q[i - K][K][c];
-                    } else {
-                        const float4 t4 = *reinterpret_cast<const float4*>(colp + i * SW);
-                        col[i][0] = t4.x;
-                        col[i][1] = t4.y;
-                        col[i][2] = t4.z;
-                        col[i][3] = t4.w;
-                    }
-                }
-#pragma unroll
-                for (int rr = 0; rr < R; ++rr)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int j = 1; j <= K; ++j)
-                            acc[rr][c] = fmaf(p.k.cy[j - 1],
-                                              col[rr + K - j][c] + col[rr + K + j][c], acc[rr][c]);
-            }
-            // centre plane fully read: hand its stage back to the producer
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(empty + cs);
-            if (++cs == NST) cs = 0;
-
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-                if (!rin[rr]) continue;
-                const float rv[4] = {r4[rr].x, r4[rr].y, r4[rr].z, r4[rr].w};
-                const float ov[4] = {o4[rr].x, o4[rr].y, o4[rr].z, o4[rr].w};
-                const float dv[4] = {d4[rr].x, d4[rr].y, d4[rr].z, d4[rr].w};
-                float un[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float dmp = SEP ? (dxy[rr][c] + dzv) : dv[c];
-                    const float qq = dmp * rv[c] * p.k.qscale;
-                    const float c1 = __frcp_rn(1.f + qq);
-                    const float c2 = (1.f - qq) * c1;
-                    const float t = fmaf(rv[c], acc[rr][c], 2.f * q[rr][K][c]);
-                    un[c] = fmaf(c1, t, -c2 * ov[c]);
-                }
-                const long long o = (long long)rr * p.pitch;
-                __stcs(reinterpret_cast<float4*>(p.uo + gu + o),
-                       make_float4(un[0], un[1], un[2], un[3]));
-                if (p.snap)
-                    __stcs(reinterpret_cast<float4*>(p.snap + gc + o),
-                           make_float4(un[0], un[1], un[2], un[3]));
-                if (img) {
-                    const float gv[4] = {g4[rr].x, g4[rr].y, g4[rr].z, g4[rr].w};
-                    const float sv[4] = {s4[rr].x, s4[rr].y, s4[rr].z, s4[rr].w};
-                    float gn[4];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        gn[c] = fmaf(-sv[c] * p.k.inv_dt2,
-                                     (un[c] - 2.f * q[rr][K][c]) + ov[c], gv[c]);
-                    __stcs(reinterpret_cast<float4*>(p.grad + gc + o),
-                           make_float4(gn[0], gn[1], gn[2], gn[3]));
-                }
-            }
-        }
-        // slide the register queue one plane along d0
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr)
-#pragma unroll
-            for (int j = 0; j < Q - 1; ++j)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) q[rr][j][c] = q[rr][j + 1][c];
+            for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
+        q[Q - 1][0] = v.x;
+        q[Q - 1][1] = v.y;
+        q[Q - 1][2] = v.z;
+        q[Q - 1][3] = v.w;
+        __syncwarp();
+        if (lane0) mbar_arrive(done + (n % NAUX));
         if (++s == NST) {
             s = 0;
             fph ^= 1;
         }
+    }
+
+    // running element offset of this thread's float4 in the output plane
+    long long gc = (long long)zb * p.plane + (long long)y * p.pitch + x;  // compact arrays
+    float* po = p.uo + gc + (long long)K * p.plane;
+    int cs = K % NST;  // stage of the centre plane (plane K is the first centre)
+    int as = 0;        // aux stage / done slot of this iteration: (n - 2K) % NAUX ...
+    int ds = (2 * K) % NAUX;  // ... and n % NAUX
+    float dzn = 0.f;
+    if (SEP) dzn = __ldg(p.dz + zb);
+
+    for (int n = 2 * K; n < nplanes; ++n) {
+        mbar_wait(full + s, fph);
+        {
+            const float4 v = *reinterpret_cast<const float4*>(ring + s * STAGE + own);
+#pragma unroll
+            for (int j = 0; j < Q - 1; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
+            q[Q - 1][0] = v.x;
+            q[Q - 1][1] = v.y;
+            q[Q - 1][2] = v.z;
+            q[Q - 1][3] = v.w;
+        }
+        const float* ap = aux + as * NARR * ABOX + aown;
+        const float4 o4 = *reinterpret_cast<const float4*>(ap);
+        const float4 r4 = *reinterpret_cast<const float4*>(ap + ABOX);
+        float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!SEP) d4 = *reinterpret_cast<const float4*>(ap + 2 * ABOX);
+        const float dzv = dzn;
+        if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
+
+        const float* cp = ring + cs * STAGE;
+        float acc[4];
+        // centre and streaming-axis neighbours from the register queue
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float a = p.k.c0 * q[K][c];
+#pragma unroll
+            for (int j = 1; j <= K; ++j) a = fmaf(p.k.cz[j - 1], q[K - j][c] + q[K + j][c], a);
+            acc[c] = a;
+        }
+        // contiguous-axis neighbours: one aligned row segment
+        {
+            float xr[2 * KP + 4];
+            const float* rowp = cp + (ty + K) * SW + 4 * tx;
+#pragma unroll
+            for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
+                if (v == KP / 4) {  // own float4: already in the queue
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) xr[4 * v + c] = q[K][c];
+                } else {
+                    const float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
+                    xr[4 * v + 0] = t4.x;
+                    xr[4 * v + 1] = t4.y;
+                    xr[4 * v + 2] = t4.z;
+                    xr[4 * v + 3] = t4.w;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int j = 1; j <= K; ++j)
+                    acc[c] = fmaf(p.k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], acc[c]);
+        }
+        // d1 neighbours: the column strip above and below
+        {
+            const float* colp = cp + ty * SW + KP + 4 * tx;
+#pragma unroll
+            for (int j = 1; j <= K; ++j) {
+                const float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
+                const float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
+                acc[0] = fmaf(p.k.cy[j - 1], lo.x + hi.x, acc[0]);
+                acc[1] = fmaf(p.k.cy[j - 1], lo.y + hi.y, acc[1]);
+                acc[2] = fmaf(p.k.cy[j - 1], lo.z + hi.z, acc[2]);
+                acc[3] = fmaf(p.k.cy[j - 1], lo.w + hi.w, acc[3]);
+            }
+        }
+        // all shared-memory reads of this iteration are done
+        __syncwarp();
+        if (lane0) mbar_arrive(done + ds);
+
+        const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
+        const float ov[4] = {o4.x, o4.y, o4.z, o4.w};
+        float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+        bool damped;
+        if (SEP) {
+            damped = warp_dxy || dzv != 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dv[c] = dxy[c] + dzv;
+        } else {
+            damped = __any_sync(0xffffffffu, (dv[0] + dv[1]) + (dv[2] + dv[3]) != 0.f);
+        }
+        float un[4];
+        if (damped) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float qq = dv[c] * rv[c] * p.k.qscale;
+                const float c1 = fast_rcp(1.f + qq);
+                const float c2 = (1.f - qq) * c1;
+                const float t = fmaf(rv[c], acc[c], 2.f * q[K][c]);
+                un[c] = fmaf(c1, t, -c2 * ov[c]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) un[c] = fmaf(rv[c], acc[c], 2.f * q[K][c]) - ov[c];
+        }
+        if (rin) {
+            __stcs(reinterpret_cast<float4*>(po), make_float4(un[0], un[1], un[2], un[3]));
+            if (p.snap)
+                __stcs(reinterpret_cast<float4*>(p.snap + gc),
+                       make_float4(un[0], un[1], un[2], un[3]));
+            if (p.usave) {
+                const float4 g4 = __ldcs(reinterpret_cast<const float4*>(p.grad + gc));
+                const float4 s4 = __ldcs(reinterpret_cast<const float4*>(p.usave + gc));
+                float4 gn;
+                gn.x = fmaf(-s4.x * p.k.inv_dt2, (un[0] - 2.f * q[K][0]) + ov[0], g4.x);
+                gn.y = fmaf(-s4.y * p.k.inv_dt2, (un[1] - 2.f * q[K][1]) + ov[1], g4.y);
+                gn.z = fmaf(-s4.z * p.k.inv_dt2, (un[2] - 2.f * q[K][2]) + ov[2], g4.z);
+                gn.w = fmaf(-s4.w * p.k.inv_dt2, (un[3] - 2.f * q[K][3]) + ov[3], g4.w);
+                __stcs(reinterpret_cast<float4*>(p.grad + gc), gn);
+            }
+        }
+        po += p.plane;
+        gc += p.plane;
+        if (++s == NST) {
+            s = 0;
+            fph ^= 1;
+        }
+        if (++cs == NST) cs = 0;
+        if (++as == NAUX) as = 0;
+        if (++ds == NAUX) ds = 0;
     }
 }
 

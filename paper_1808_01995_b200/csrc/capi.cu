@@ -74,15 +74,14 @@ EncodeTiledFn encode_tiled() {
     return fn;
 }
 
-void make_tensor_map(Plan& P, int which) {
-    const StepVariant& v = *P.variant;
-    cuuint64_t dims[3] = {cuuint64_t(P.N[2]), cuuint64_t(P.N[1]), cuuint64_t(P.n0 + 2 * P.K)};
-    cuuint64_t strides[2] = {cuuint64_t(P.pitch) * 4, cuuint64_t(P.plane) * 4};
-    cuuint32_t box[3] = {cuuint32_t(v.box_w), cuuint32_t(v.box_h), 1};
+void encode_map(CUtensorMap* tm, void* base, long long n2, long long n1, long long n0,
+                long long pitch, long long plane, int box_w, int box_h) {
+    cuuint64_t dims[3] = {cuuint64_t(n2), cuuint64_t(n1), cuuint64_t(n0)};
+    cuuint64_t strides[2] = {cuuint64_t(pitch) * 4, cuuint64_t(plane) * 4};
+    cuuint32_t box[3] = {cuuint32_t(box_w), cuuint32_t(box_h), 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult rc = encode_tiled()(&P.tm[which], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                                 P.u[which].p, dims, strides, box, estr,
-                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    CUresult rc = encode_tiled()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rc != CUDA_SUCCESS)
@@ -90,13 +89,30 @@ void make_tensor_map(Plan& P, int which) {
                                         std::to_string(int(rc)));
 }
 
+// (re)build every tensor map of the plan for the current tile shape
+void make_tensor_maps(Plan& P) {
+    const StepVariant& v = *P.variant;
+    for (int b = 0; b < 2; ++b) {
+        if (!P.u[b].p) continue;
+        encode_map(&P.tm_u[b], P.u[b].p, P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
+                   v.box_w, v.box_h);
+        encode_map(&P.tm_o[b], P.u[b].p, P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
+                   v.tile_x, v.tile_y);
+    }
+    if (P.r.p)
+        encode_map(&P.tm_r, P.r.p, P.N[2], P.N[1], P.n0, P.pitch, P.plane, v.tile_x, v.tile_y);
+    if (P.damp.p)
+        encode_map(&P.tm_d, P.damp.p, P.N[2], P.N[1], P.n0, P.pitch, P.plane, v.tile_x,
+                   v.tile_y);
+}
+
 // ---- tile shape / chunk choice ----------------------------------------------------------
 
-void select_variant(Plan& P, int txv, int ty, int r) {
+void select_variant(Plan& P, int txv, int ty, int nst) {
     const StepVariant* best = nullptr;
     for (const StepVariant& v : step_variant_registry()) {
         if (v.K != P.K || v.sep != P.sep) continue;
-        if (txv > 0 && (v.TXV != txv || v.TY != ty || v.R != r)) continue;
+        if (txv > 0 && (v.TXV != txv || v.TY != ty || (nst > 0 && v.NST != nst))) continue;
         if (!best) best = &v;
     }
     if (!best)
@@ -132,10 +148,7 @@ void select_variant(Plan& P, int txv, int ty, int r) {
         if (total > 16 * slots) break;
     }
     P.chunk = (P.n0 + best_nch - 1) / best_nch;
-    if (P.u[0].p) {
-        make_tensor_map(P, 0);
-        make_tensor_map(P, 1);
-    }
+    make_tensor_maps(P);
 }
 
 // ---- host <-> device field movement --------------------------------------------------------
@@ -223,6 +236,66 @@ void download_field(Plan& P, const float* dev, const sfb_field_mview* out) {
     SFB_CUDA(cudaGetLastError());
     SFB_CUDA(cudaStreamSynchronize(P.s_main));
     download_f64(P, tmp, out->ptr, out->stride);
+}
+
+// ---- separable damping -----------------------------------------------------------------------
+// build_damping (proj/src/model.cpp:35-56) is a sum of three 1-D profiles.  When the bound
+// damp field has that structure (checked on the device against the field itself), the
+// kernel rebuilds it from the profiles and never streams the dense array.
+__global__ void sep_check_kernel(const double* __restrict__ damp, const double* __restrict__ pz,
+                                 const double* __restrict__ py, const double* __restrict__ px,
+                                 long long n0, long long n1, long long n2,
+                                 unsigned long long* maxdev, unsigned long long* maxabs) {
+    const long long total = n0 * n1 * n2;
+    double dev = 0.0, mx = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long l = i % n2, j = (i / n2) % n1, z = i / (n2 * n1);
+        const double v = damp[i];
+        dev = fmax(dev, fabs(v - (pz[z] + py[j] + px[l])));
+        mx = fmax(mx, fabs(v));
+    }
+    atomicMax(maxdev, (unsigned long long)__double_as_longlong(dev));
+    atomicMax(maxabs, (unsigned long long)__double_as_longlong(mx));
+}
+
+void detect_separable_damping(Plan& P, const IntView& v, const DevBuf& damp_f64) {
+    P.sep = false;
+    if (P.force_dense_damp) return;
+    // lines through the grid centre; the centre value is counted once (in px)
+    const long long c[3] = {P.N[0] / 2, P.N[1] / 2, P.N[2] / 2};
+    auto at = [&](long long i, long long j, long long l) {
+        return v.ptr[i * v.s[0] + j * v.s[1] + l * v.s[2]];
+    };
+    const double base = at(c[0], c[1], c[2]);
+    std::vector<double> pz(P.n0), py(P.N[1]), px(P.pitch, 0.0);
+    for (long long z = 0; z < P.n0; ++z) pz[z] = at(P.z_lo + z, c[1], c[2]) - base;
+    for (long long j = 0; j < P.N[1]; ++j) py[j] = at(c[0], j, c[2]) - base;
+    for (long long l = 0; l < P.N[2]; ++l) px[l] = at(c[0], c[1], l);
+    DevBuf dpz, dpy, dpx, stat;
+    auto put = [&P](DevBuf& d, const void* src, size_t bytes) {
+        d.alloc(bytes, false);
+        SFB_CUDA(cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, P.s_main));
+    };
+    put(dpz, pz.data(), pz.size() * 8);
+    put(dpy, py.data(), py.size() * 8);
+    put(dpx, px.data(), px.size() * 8);
+    stat.alloc(16, false);
+    SFB_CUDA(cudaMemsetAsync(stat.p, 0, 16, P.s_main));
+    sep_check_kernel<<<P.sm_count * 8, 256, 0, P.s_main>>>(
+        damp_f64.as<double>(), dpz.as<double>(), dpy.as<double>(), dpx.as<double>(), P.n0, P.N[1],
+        P.N[2], stat.as<unsigned long long>(), stat.as<unsigned long long>() + 1);
+    SFB_CUDA(cudaGetLastError());
+    double res[2];
+    SFB_CUDA(cudaMemcpyAsync(res, stat.p, 16, cudaMemcpyDeviceToHost, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    if (!(res[0] <= 1e-7 * res[1] || res[1] == 0.0)) return;
+    std::vector<float> fz(pz.begin(), pz.end()), fy(py.begin(), py.end()), fx(px.begin(), px.end());
+    put(P.dz, fz.data(), fz.size() * 4);
+    put(P.dy, fy.data(), fy.size() * 4);
+    put(P.dx, fx.data(), fx.size() * 4);
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    P.sep = true;
 }
 
 // ---- point tables ------------------------------------------------------------------------
@@ -433,8 +506,6 @@ void step_compute(Plan& P, int op, long long t, int part) {
     const long long tnew = ro.backward ? t - 1 : t + 1;
     StepParams sp{};
     sp.k = P.coef;
-    sp.r = P.r.as<float>();
-    sp.damp = P.damp.as<float>();
     sp.dz = P.dz.as<float>();
     sp.dy = P.dy.as<float>();
     sp.dx = P.dx.as<float>();
@@ -457,7 +528,12 @@ void step_compute(Plan& P, int op, long long t, int part) {
               unsigned((P.N[1] + v.tile_y - 1) / v.tile_y),
               unsigned((hi - lo + sp.chunk - 1) / sp.chunk));
     cudaStream_t st = part_stream(P, part);
-    SFB_CUDA(v.launch(P.tm[cur], sp, grid, st));
+    StepMaps maps;
+    maps.u = P.tm_u[cur];
+    maps.o = P.tm_o[oth];
+    maps.r = P.tm_r;
+    maps.d = P.sep ? P.tm_r : P.tm_d;
+    SFB_CUDA(v.launch(maps, sp, grid, st));
     ++P.launches;
     mark_stream(P, part);
     if (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) {
@@ -827,6 +903,9 @@ SFB_API int sfb_set_model(sfb_plan* plan, const sfb_field_view* m, const sfb_fie
             tmp.as<double>(), P.damp.as<float>(), rows, int(P.N[2]), P.pitch);
         SFB_CUDA(cudaGetLastError());
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        detect_separable_damping(P, embed_view(P, damp->ptr, damp->stride), tmp);
+        if (P.sep) P.damp.release();
+        select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST);
         P.model_set = true;
         P.history_valid = false;
     });
@@ -1066,19 +1145,24 @@ SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_
     });
 }
 
-SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int r, int chunk) {
+SFB_API int sfb_set_dense_damping(sfb_plan* plan, int on) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    plan->force_dense_damp = on != 0;
+    return SFB_OK;
+}
+
+SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
-        select_variant(*plan, txv, ty, r);
+        select_variant(*plan, txv, ty, stages);
         if (chunk > 0) plan->chunk = std::min(chunk, plan->n0);
     });
 }
 
-SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* r, int* nst, int* chunk, int* sep) {
+SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* nst, int* chunk, int* sep) {
     if (!plan || !plan->variant) return SFB_ERR_PARAMETER;
     if (txv) *txv = plan->variant->TXV;
     if (ty) *ty = plan->variant->TY;
-    if (r) *r = plan->variant->R;
     if (nst) *nst = plan->variant->NST;
     if (chunk) *chunk = plan->chunk;
     if (sep) *sep = plan->variant->sep ? 1 : 0;

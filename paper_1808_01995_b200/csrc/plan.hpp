@@ -102,8 +102,9 @@ struct Plan {
     bool main_pending = false, bnd_pending = false;
 
     DevBuf u[2], r, damp, dz, dy, dx, grad, snaps, flag;
-    CUtensorMap tm[2];
+    CUtensorMap tm_u[2], tm_o[2], tm_r, tm_d;  // halo box on u[b]; plain box on u[b], r, damp
     bool model_set = false, sep = false;
+    bool force_dense_damp = false;              // keep streaming the dense damp array
     double v_max = 0;
 
     Cloud cloud[2];

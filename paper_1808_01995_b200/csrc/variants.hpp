@@ -11,52 +11,55 @@
 namespace sfb {
 
 struct StepVariant {
-    int K, TXV, TY, R, NST;
+    int K, TXV, TY, NST;
     bool sep;
     int tile_x, tile_y;   // output tile (d2, d1)
-    int box_w, box_h;     // TMA box (d2, d1)
+    int box_w, box_h;     // TMA box of u[t] (d2, d1)
     int halo_x;           // KP
     int nthreads;
     size_t smem;
     const void* func;
-    cudaError_t (*launch)(const CUtensorMap&, const StepParams&, dim3, cudaStream_t);
+    cudaError_t (*launch)(const StepMaps&, const StepParams&, dim3, cudaStream_t);
 };
 
 std::vector<StepVariant>& step_variant_registry();
 
-template <int K, int TXV, int TY, int R, int NST, bool SEP>
-cudaError_t launch_step(const CUtensorMap& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
-    using S = StepShape<K, TXV, TY, R, NST>;
-    acoustic_step_kernel<K, TXV, TY, R, NST, SEP><<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
+template <int K, int TXV, int TY, int NST, bool SEP>
+cudaError_t launch_step(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
+    using S = StepShape<K, TXV, TY, NST, SEP>;
+    acoustic_step_kernel<K, TXV, TY, NST, SEP><<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
     return cudaGetLastError();
 }
 
-template <int K, int TXV, int TY, int R, int NST, bool SEP>
+template <int K, int TXV, int TY, int NST, bool SEP>
 void register_step() {
-    using S = StepShape<K, TXV, TY, R, NST>;
-    StepVariant v;
-    v.K = K; v.TXV = TXV; v.TY = TY; v.R = R; v.NST = NST; v.sep = SEP;
-    v.tile_x = S::TX; v.tile_y = TY; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
-    v.nthreads = S::NTHREADS; v.smem = S::SMEM;
-    v.func = reinterpret_cast<const void*>(&acoustic_step_kernel<K, TXV, TY, R, NST, SEP>);
-    v.launch = &launch_step<K, TXV, TY, R, NST, SEP>;
-    step_variant_registry().push_back(v);
+    using S = StepShape<K, TXV, TY, NST, SEP>;
+    if constexpr (S::SMEM <= 227 * 1024) {
+        StepVariant v;
+        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NST; v.sep = SEP;
+        v.tile_x = S::TX; v.tile_y = TY; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
+        v.nthreads = S::NTHREADS; v.smem = S::SMEM;
+        v.func = reinterpret_cast<const void*>(&acoustic_step_kernel<K, TXV, TY, NST, SEP>);
+        v.launch = &launch_step<K, TXV, TY, NST, SEP>;
+        step_variant_registry().push_back(v);
+    }
 }
 
-// the tile shapes built for every half-order K (dense and separable damping)
+template <int K, int TXV, int TY, int NST>
+void register_pair() {
+    register_step<K, TXV, TY, NST, false>();
+    register_step<K, TXV, TY, NST, true>();
+}
+
+// the tile shapes built for every half-order K (dense and separable damping); the first
+// entry is the default, sfb_set_tile / sfb_autotune pick among the rest
 template <int K>
 void register_all_for_K() {
-    // the first entry is the default; sfb_set_tile / the autotuner pick among the rest
-    register_step<K, 16, 16, 1, K + 3, false>();
-    register_step<K, 16, 16, 1, K + 3, true>();
-    register_step<K, 16, 32, 1, K + 3, false>();
-    register_step<K, 16, 32, 1, K + 3, true>();
-    register_step<K, 32, 8, 1, K + 3, false>();
-    register_step<K, 32, 8, 1, K + 3, true>();
-    if constexpr (K <= 4) {  // two rows per thread: the register queue doubles
-        register_step<K, 16, 32, 2, K + 3, false>();
-        register_step<K, 16, 32, 2, K + 3, true>();
-    }
+    register_pair<K, 16, 16, K + 3>();
+    register_pair<K, 16, 16, K + 4>();
+    register_pair<K, 32, 8, K + 3>();
+    register_pair<K, 16, 32, K + 3>();
+    register_pair<K, 32, 16, K + 3>();
 }
 
 struct VariantRegistrar {

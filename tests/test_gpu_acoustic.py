@@ -63,13 +63,39 @@ def test_tile_shapes_agree_bitwise():
     plan = make_plan(model, geom, 8)
     base, _ = plan.forward(geom.src)
     u0 = plan.wavefield(geom.nt - 1)
-    for tile in [(16, 32, 1), (32, 8, 1), (16, 32, 2)]:
+    for tile in [(16, 16, 8), (32, 8, 0), (16, 32, 0), (32, 16, 0)]:
         for chunk in (0, 7, 60):
             plan.set_tile(*tile, chunk)
             rec, _ = plan.forward(geom.src)
             assert np.array_equal(rec, base)
             assert np.array_equal(plan.wavefield(geom.nt - 1), u0)
     plan.close()
+
+
+def test_dense_and_separable_damping_agree():
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([40, 36, 44], 10.0, 8, 8, 60)
+    plan = make_plan(model, geom, 8)
+    assert plan.get_tile()["sep"] == 1  # build_damping is a sum of 1-D profiles
+    rec_s, _ = plan.forward(geom.src)
+    u_s = plan.wavefield(geom.nt - 1)
+    plan.close()
+    dense = capi.Plan(model.N, model.spacing, 8, geom.dt, geom.nt, dense_damping=True)
+    dense.set_model(model.m, model.damp, model.v_max)
+    dense.set_points(capi.CLOUD_SRC, geom.src_base, geom.src_w)
+    dense.set_points(capi.CLOUD_REC, geom.rec_base, geom.rec_w)
+    assert dense.get_tile()["sep"] == 0
+    rec_d, _ = dense.forward(geom.src)
+    ref = o.forward(model, geom, 8, want_final=True)
+    assert rel_l2(rec_d, ref["smp"]) <= 1e-5 and rel_l2(dense.wavefield(geom.nt - 1), ref["final"]) <= 1e-5
+    assert rel_l2(rec_s, rec_d) <= 1e-6 and rel_l2(u_s, dense.wavefield(geom.nt - 1)) <= 1e-6
+    # a damping field that is not separable must fall back to the dense stream
+    bumpy = model.damp.copy()
+    bumpy[5, 7, 9] += 0.01
+    dense.set_dense_damping(False)
+    dense.set_model(model.m, bumpy, model.v_max)
+    assert dense.get_tile()["sep"] == 0
+    dense.close()
 
 
 def test_zero_source_gives_zero_receivers():  # proj/tests/test_seismic.cpp:165-174

@@ -19,7 +19,8 @@ m = (1.0 / rng.uniform(1.5, vmax, size=n * n).reshape(1, n, n) ** 2) * np.ones((
 damp = np.zeros(N)
 damp[:40] += 0.01; damp[-40:] += 0.01
 print("host arrays", time.time() - t0, flush=True)
-plan = capi.Plan(N, [h] * 3, order, dt, nt)
+dense = len(sys.argv) > 4 and sys.argv[4] == "dense"
+plan = capi.Plan(N, [h] * 3, order, dt, nt, dense_damping=dense)
 plan.set_model(m, damp, vmax)
 print("model up", time.time() - t0, flush=True)
 nr = min(512, n - 82)
@@ -34,10 +35,14 @@ src = np.sin(np.arange(nt) * 0.1).reshape(nt, 1)
 plan.upload_traces(capi.CLOUD_SRC, src)
 print("points up", time.time() - t0, flush=True)
 K = order // 2
-tiles = [(16, 16, 1), (16, 32, 1), (32, 8, 1)] + ([(16, 32, 2)] if K <= 4 else [])
+tiles = [(16, 16, K + 3), (16, 16, K + 4), (32, 8, 0), (16, 32, 0), (32, 16, 0)]
 for tile in tiles:
     for chunk in (0,):
-        plan.set_tile(*tile, chunk)
+        try:
+            plan.set_tile(*tile, chunk)
+        except capi.SfbError as e:
+            print("skip", tile, e)
+            continue
         plan.step_begin(capi.OP_FORWARD)
         plan.run_steps(capi.OP_FORWARD, 1, 11)
         rep = plan.run_steps(capi.OP_FORWARD, 11, 11 + steps)
