@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the wave-propagator path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+Metric (BASELINE.json): GPts/s = padded grid points x time steps / seconds of the stepping
+loop, acoustic forward operator.  A "step" is one time step of the propagator (dense
+update + source scatter + receiver gather).  Workload at every N: BASELINE.json configs[1]
+(512^3 physical + 40-node layer = 592^3, space order 8, 512x512 receivers, one off-node
+Ricker source, seeded smoothed-noise velocity); at N > 1 the same grid is cut into N slabs
+along the slowest axis (strong scaling, as configs[1] asks) and ghost planes travel over
+NCCL send/recv each step.
+
+One JSON line on stdout (rank 0).  `value` is timed with CUDA events on the plan's own
+stream with all inputs resident in HBM; `e2e` is the same metric through the C-ABI call
+sfb_forward with host buffers (source traces H2D, receiver traces D2H inside the timed
+region); `roofline` is the dense-update kernel alone; `cpu_baseline` is the f64 oracle on
+the host cores.  `--impl reference` times the CPU implementation (oracle/_ref when the
+reference's own sources were compiled here, else the oracle port).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+BYTES_PER_POINT = 20.0   # u[t], u[t-1], u[t+1], m, damp, one touch each
+N_PHYS, ORDER, NBL, H = 512, 8, 40, 12.5
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---- clocks ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.rows, self.proc, self.index = [], None, index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE, text=True)
+            self.th = threading.Thread(target=self._pump, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.th.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for n, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        busy = [s for s in sm if s > 0.6 * mx] or sm
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- workload -------------------------------------------------------------------------
+
+def build_workload(nsteps_total):
+    """configs[1] through the C++ host layer (SeismicModel / AcquisitionGeometry)."""
+    from paper_1808_01995_b200 import _sfb_host as Hst
+    from paper_1808_01995_b200 import synthetic as syn
+    cfg = syn.config(2, N_PHYS)
+    t0 = time.time()
+    vel = cfg["velocity"]()
+    log(f"[bench] velocity {vel.shape} in {time.time() - t0:.1f}s "
+        f"[{vel.min():.3f}, {vel.max():.3f}]")
+    t0 = time.time()
+    model = Hst.SeismicModel(cfg["shape"], [H] * 3, [0.0] * 3, vel, NBL, ORDER)
+    del vel
+    dt, tn = syn.time_axis(model.critical_dt(ORDER), nsteps_total)
+    geom = Hst.AcquisitionGeometry(model, np.asarray(cfg["src"]).ravel(), cfg["rec"].ravel(),
+                                   0.0, tn, dt, cfg["f0"])
+    assert geom.nt == nsteps_total + 2, (geom.nt, nsteps_total)
+    log(f"[bench] model + geometry in {time.time() - t0:.1f}s: N={model.grid.shape} dt={dt:.6f} "
+        f"nt={geom.nt} n_rec={geom.n_rec}")
+    return cfg, model, geom
+
+
+def make_plan(model, geom, device=0, slab=None):
+    from paper_1808_01995_b200 import capi
+    plan = capi.Plan(model.grid.shape, model.grid.spacing, ORDER, geom.dt, geom.nt, device, slab)
+    plan.set_model(model.m.array(), model.damp.array(), model.v_max)
+    nd = 3
+    plan.set_points(capi.CLOUD_SRC, np.array(geom.src.base_table).reshape(-1, nd),
+                    np.array(geom.src.weight_table).reshape(-1, 8))
+    plan.set_points(capi.CLOUD_REC, np.array(geom.rec.base_table).reshape(-1, nd),
+                    np.array(geom.rec.weight_table).reshape(-1, 8))
+    return plan
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---- CPU arm ----------------------------------------------------------------------------
+
+def cpu_run(model_shape, vmax_dt, steps, threads=None):
+    """Oracle (f64 port of the reference's loop nest, all host threads) on the same 592^3
+    order-8 dense update; returns (GPts/s, threads, seconds)."""
+    from oracle import oracle as o
+    if threads:
+        o.set_num_threads(threads)
+    N = model_shape
+    rng = np.random.default_rng(7)
+
+    class M:  # minimal stand-in carrying what dense_steps reads
+        pass
+    m = M()
+    m.ndim, m.N, m.spacing = 3, list(N), [H] * 3
+    m.m = np.full(N, 1.0 / 3.0 ** 2)
+    m.m += 0.05 * rng.random(N[2])[None, None, :]
+    m.damp = np.zeros(N)
+    m.damp[:NBL] = 0.01
+    cur = rng.standard_normal(N) * 1e-3
+    old = cur.copy()
+    t0 = time.time()
+    o.dense_steps(m, ORDER, vmax_dt, steps, cur, old)
+    sec = time.time() - t0
+    return float(np.prod(N)) * steps / sec / 1e9, o.num_threads(), sec
+
+
+def reference_arm(args):
+    """`--impl reference`: the CPU implementation of the path on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    N = [N_PHYS + 2 * NBL] * 3
+    from paper_1808_01995_b200 import capi
+    dt = capi.critical_dt([H] * 3, 4.5, ORDER)
+    kind = "port"
+    # a bounded sample: each "step" below is one dense time step of the full 592^3 grid
+    gpts, cores, sec = cpu_run(N, dt, 1)            # warm-up + calibration
+    k = max(1, min(args.steps, int(25.0 / max(sec, 1e-3))))
+    w = min(args.warmup, 1)
+    if w:
+        cpu_run(N, dt, w)
+    gpts, cores, sec = cpu_run(N, dt, k)
+    line = {
+        "impl": "reference", "metric": "acoustic_forward_gpts_per_s", "value": gpts,
+        "unit": "GPts/s", "n_gpus": args.gpus, "steps": k, "warmup": w,
+        "ms_per_step": sec / k * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.gpus),
+        "cpu_baseline": {"value": gpts, "unit": "GPts/s", "cores": cores, "kind": kind,
+                         "sample": f"{k} dense time steps of the full 592^3 order-8 grid "
+                                   f"(f64 oracle port, OpenMP, {cores} threads)"},
+        "e2e": {"value": gpts, "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n_gpus):
+    return {"workload": "BASELINE.json configs[1]: acoustic forward, 512^3 physical + 40-node "
+                        "absorbing layer (592^3 computed), space order 8, fp32, 1 Ricker source, "
+                        "512x512 receivers, seeded smoothed-noise velocity in [1.5,4.5] km/s",
+            "grid": [N_PHYS + 2 * NBL] * 3, "space_order": ORDER,
+            "decomposition": f"{n_gpus} slab(s) along the slowest axis",
+            "l2": "every field (0.83 GB) is larger than the 126 MB L2: no flush needed"}
+
+
+# ---- our arm -----------------------------------------------------------------------------
+
+def ours(args):
+    import torch
+    from paper_1808_01995_b200 import capi
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available() or capi.device_count() < 1:
+        raise SystemExit("bench.py needs a CUDA device: there is no CPU fallback")
+    K, W = args.steps, max(args.warmup, 3)
+    if world > 1:
+        from paper_1808_01995_b200 import slabs
+        return slabs.bench_distributed(args, K, W, build_workload, workload_config,
+                                       BYTES_PER_POINT, peaks)
+    torch.cuda.set_device(local)
+    cfg, model, geom = build_workload(W + K)
+    N = model.grid.shape
+    pts = float(np.prod(N))
+    t0 = time.time()
+    plan = make_plan(model, geom, local)
+    tile = plan.get_tile()
+    log(f"[bench] plan + uploads in {time.time() - t0:.1f}s, tile {tile}")
+    src = geom.src.traces
+    plan.upload_traces(capi.CLOUD_SRC, src)
+
+    # --- value: K steps after W warm-up steps, inputs resident, device-timed ------------
+    F = capi.OP_FORWARD
+    plan.step_begin(F)
+    plan.run_steps(F, 1, 1 + W)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        rep = plan.run_steps(F, 1 + W, 1 + W + K)
+        torch.cuda.synchronize()
+        # --- roofline: the dense-update kernel alone over the same K steps ----------------
+        plan.step_begin(F)
+        plan.run_steps(F, 1, 1 + W)
+        st = plan.time_stencil(F, 1 + W, 1 + W + K)
+    clocks = clk.summary()
+    plan.step_end(F)
+    value = pts * K / rep.seconds / 1e9
+    kern_s = st.seconds / st.steps
+    peak, peak_kind = peaks()
+    achieved = BYTES_PER_POINT * pts / kern_s / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # --- e2e: the C-ABI call with host buffers, K steps ---------------------------------
+    plan.close()
+    from paper_1808_01995_b200 import _sfb_host as Hst
+    from paper_1808_01995_b200 import synthetic as syn
+    dt, tn = syn.time_axis(model.critical_dt(ORDER), K)
+    geom2 = Hst.AcquisitionGeometry(model, np.asarray(cfg["src"]).ravel(), cfg["rec"].ravel(),
+                                    0.0, tn, dt, cfg["f0"])
+    plan2 = make_plan(model, geom2, local)
+    src2 = np.ascontiguousarray(geom2.src.traces)
+    plan2.forward(src2[:])  # warm-up pass (allocations, first-touch of the staging buffers)
+    t0 = time.perf_counter()
+    rec, rep2 = plan2.forward(src2)
+    e2e_s = time.perf_counter() - t0
+    e2e = pts * K / e2e_s / 1e9
+    assert np.isfinite(rec).all() and float(np.abs(rec).max()) > 0.0
+    plan2.close()
+
+    # --- CPU baseline on this box's host cores (bounded sample) -------------------------
+    cpu = None
+    if not args.no_cpu:
+        g1, cores, s1 = cpu_run(N, geom.dt, 1)
+        n = max(2, min(40, int(15.0 / max(s1, 1e-3))))
+        g, cores, s = cpu_run(N, geom.dt, n)
+        cpu = {"value": g, "unit": "GPts/s", "cores": cores, "kind": "port",
+               "sample": f"{n} dense time steps of the same 592^3 order-8 grid, f64 oracle "
+                         f"(oracle/sf_oracle.c, gcc -O3 -fopenmp), {s:.1f} s"}
+
+    line = {
+        "metric": "acoustic_forward_gpts_per_s", "value": value, "unit": "GPts/s", "n_gpus": 1,
+        "steps": K, "warmup": W, "ms_per_step": rep.seconds / K * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(1),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "acoustic_step_kernel", "kernel_ms": kern_s * 1e3,
+                     "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts,
+                     "tile": tile},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": "GPts/s", "h2d_bytes_per_step": int(geom2.n_src * 8),
+                "d2h_bytes_per_step": int(geom2.n_rec * 8), "seconds": e2e_s,
+                "device_seconds": rep2.seconds},
+        "gpu_launches": int(rep.kernel_launches),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours(args)
+
+
+if __name__ == "__main__":
+    main()

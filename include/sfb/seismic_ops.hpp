@@ -1,0 +1,118 @@
+// seismic_ops.hpp -- the operator entry points of the wave-propagator path, GPU build.
+//
+// Same names, argument meaning and error behaviour as the reference's
+// proj/include/sf/seismic_ops.hpp:13-97; each function cites the lines it replaces.  The
+// engine behind them is libsfb200.so (include/sfb200.h): hand-written sm_100a kernels,
+// no backend dispatch and no CPU fallback -- Backend / nthreads / tiles are accepted for
+// source compatibility and ignored.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "sfb/geometry.hpp"
+#include "sfb/model.hpp"
+
+namespace sfb {
+
+enum class Backend { Interpreter, Emitted, Auto };  // proj/include/sf/execute.hpp:22 (ignored)
+
+// proj/include/sf/execute.hpp:40-46
+struct ExecutionReport {
+    double seconds = 0.0;  // stepping loop only, device time
+    long long flops = 0;
+    double gflops = 0.0;
+    long steps = 0;
+    std::vector<long> tiles;
+    double gpts_per_s = 0.0;
+    long kernel_launches = 0;
+};
+
+class Engine;  // owns one sfb_plan
+
+// proj/include/sf/seismic_ops.hpp:17-23.  `inj` traces are caller input, `smp` traces are
+// produced by the run; rows 0, 1 and nt-1 of the sampled traces are structural zeros.
+struct WaveOp {
+    std::shared_ptr<Engine> engine;
+    std::shared_ptr<TimeFunction> wavefield;
+    std::shared_ptr<SparseFunction> inj, smp;
+    double dt = 0;
+    long nt = 0;
+    int space_order = 0;
+    bool adjoint = false;
+    // save=true keeps the forward history in HBM (every save_every-th level; 1 = the
+    // reference's full history).  host_history additionally mirrors every saved level
+    // into `wavefield` as the reference does (proj/src/seismic_ops.cpp:66-68).
+    long save_every = 0;
+    bool host_history = true;
+};
+
+// proj/include/sf/seismic_ops.hpp:28-30, proj/src/seismic_ops.cpp:58-82
+WaveOp forward_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
+                        int space_order, bool save = false, std::vector<long> tiles = {});
+// proj/include/sf/seismic_ops.hpp:35-36, proj/src/seismic_ops.cpp:84-107
+WaveOp adjoint_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
+                        int space_order);
+
+// proj/include/sf/seismic_ops.hpp:40-47
+struct GradientOp {
+    std::shared_ptr<Engine> engine;
+    std::shared_ptr<TimeFunction> v;
+    std::shared_ptr<Function> grad;
+    std::shared_ptr<SparseFunction> resid;
+    double dt = 0;
+    long nt = 0;
+    int space_order = 0;
+};
+
+// proj/include/sf/seismic_ops.hpp:49-51, proj/src/seismic_ops.cpp:109-135.  saved_u must
+// be the saved (non-buffered, nt-slot) wavefield of a forward operator that has run.
+GradientOp gradient_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
+                             int space_order, std::shared_ptr<TimeFunction> saved_u);
+
+// proj/include/sf/seismic_ops.hpp:55-58, proj/src/seismic_ops.cpp:137-147
+ExecutionReport run_wave(WaveOp& w, Backend backend = Backend::Auto, int nthreads = 1);
+ExecutionReport run_gradient(GradientOp& g, Backend backend = Backend::Auto,
+                             int nthreads = 1);
+
+// proj/include/sf/seismic_ops.hpp:61, proj/src/seismic_ops.cpp:149-160
+double objective(const SparseFunction& pred, const std::vector<double>& observed);
+
+// proj/include/sf/seismic_ops.hpp:63-73
+struct GradientResult {
+    double objective = 0;
+    std::vector<double> gradient;  // per physical-domain cell, row-major
+    std::vector<double> residual;
+};
+
+// proj/src/seismic_ops.cpp:197-216.  save_every is an extension (1 = reference): image
+// against every save_every-th forward level only, which divides the HBM the history needs.
+GradientResult fwi_gradient(const SeismicModel& model, AcquisitionGeometry& geom,
+                            const std::vector<double>& observed, int space_order,
+                            Backend backend = Backend::Auto, long save_every = 1);
+
+// proj/include/sf/seismic_ops.hpp:75-97, proj/src/seismic_ops.cpp:218-286
+struct FwiConfig {
+    int space_order = 8;
+    long n_iter = 15;
+    double step_scale = 0.05;
+    double m_min = 0, m_max = 0;
+    Backend backend = Backend::Auto;
+    int nthreads = 1;  // shots in flight at once (one engine each)
+};
+
+struct FwiResult {
+    std::vector<double> objectives;
+    std::vector<double> model_rms;
+    std::vector<double> final_m;
+};
+
+FwiResult fwi(SeismicModel& model, std::vector<AcquisitionGeometry>& shots,
+              const std::vector<std::vector<double>>& observed, const FwiConfig& cfg,
+              const std::vector<double>* true_m = nullptr);
+
+// CUDA device the operators created by this thread run on (default 0)
+void set_device(int ordinal);
+int device();
+
+}  // namespace sfb

@@ -164,6 +164,11 @@ SFB_API int sfb_run_resident(sfb_plan* plan, int op, int64_t save_every, sfb_rep
  * state first (descending for the backward operators); timed on the device */
 SFB_API int sfb_run_steps(sfb_plan* plan, int op, int64_t t_from, int64_t t_to,
                           sfb_report* report);
+/* the same window with the dense update kernel alone (no scatter / gather launches):
+ * report->seconds / report->steps is that kernel's average launch duration, which the
+ * roofline figure of bench.py is computed from */
+SFB_API int sfb_time_stencil(sfb_plan* plan, int op, int64_t t_from, int64_t t_to,
+                             sfb_report* report);
 
 /* ---- slab stepping (multi-GPU; the caller moves ghost planes between ranks) --------
  * One time step is: sfb_step_begin (zeroes state when t is the first step of the window),

@@ -44,7 +44,7 @@ SYMBOLS = [
     "sfb_plan_destroy", "sfb_fd_weights", "sfb_critical_dt", "sfb_set_model",
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
-    "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_step_begin", "sfb_step_compute",
+    "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
     "sfb_step_points", "sfb_step_end", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping",
@@ -64,6 +64,7 @@ lib.sfb_upload_traces.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
 lib.sfb_download_traces.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
 lib.sfb_run_resident.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.POINTER(Report)]
 lib.sfb_run_steps.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.POINTER(Report)]
+lib.sfb_time_stencil.argtypes = lib.sfb_run_steps.argtypes
 lib.sfb_step_begin.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_step_compute.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
 lib.sfb_step_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
@@ -215,6 +216,11 @@ class Plan:
     def run_steps(self, op, t_from, t_to):
         rep = Report()
         self._chk(lib.sfb_run_steps(self.h, op, t_from, t_to, C.byref(rep)))
+        return rep
+
+    def time_stencil(self, op, t_from, t_to):
+        rep = Report()
+        self._chk(lib.sfb_time_stencil(self.h, op, t_from, t_to, C.byref(rep)))
         return rep
 
     def set_tile(self, txv, ty, stages=0, chunk=0):

@@ -958,41 +958,45 @@ SFB_API int sfb_run_resident(sfb_plan* plan, int op, int64_t save_every, sfb_rep
     return guarded(plan, [&] { run_op(*plan, op, save_every, report); });
 }
 
+namespace {
+void run_window(Plan& P, int op, long long t_from, long long t_to, bool with_points,
+                sfb_report* report) {
+    const OpRoles ro = roles(op);
+    require(t_from >= 1 && t_to <= P.desc.nt - 1 && t_from <= t_to, SFB_ERR_PARAMETER,
+            "run_steps: window outside [1, nt-1)");
+    const long before = P.launches;
+    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+    for (long long i = 0; i < t_to - t_from; ++i) {
+        const long long t = ro.backward ? t_to - 1 - i : t_from + i;
+        step_compute(P, op, t, SFB_PART_ALL);
+        if (with_points) step_points(P, op, t, SFB_PART_ALL);
+    }
+    SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    float ms = 0.f;
+    SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+    if (report) {
+        const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
+        const long long fpp = 3LL * P.K * P.ndim + 3LL * P.ndim + 11 + (ro.imaging ? 7 : 0);
+        report->seconds = ms * 1e-3;
+        report->steps = long(t_to - t_from);
+        report->flops = (long long)(double(fpp) * own * double(report->steps));
+        report->gflops = ms > 0 ? double(report->flops) / (ms * 1e-3) / 1e9 : 0.0;
+        report->gpts_per_s = ms > 0 ? own * double(report->steps) / (ms * 1e-3) / 1e9 : 0.0;
+        report->kernel_launches = P.launches - before;
+    }
+}
+}  // namespace
+
 SFB_API int sfb_run_steps(sfb_plan* plan, int op, int64_t t_from, int64_t t_to, sfb_report* report) {
     if (!plan) return SFB_ERR_PARAMETER;
-    return guarded(plan, [&] {
-        Plan& P = *plan;
-        const OpRoles ro = roles(op);
-        require(t_from >= 1 && t_to <= P.desc.nt - 1 && t_from <= t_to, SFB_ERR_PARAMETER,
-                "run_steps: window outside [1, nt-1)");
-        const long before = P.launches;
-        SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
-        if (!ro.backward) {
-            for (long long t = t_from; t < t_to; ++t) {
-                step_compute(P, op, t, SFB_PART_ALL);
-                step_points(P, op, t, SFB_PART_ALL);
-            }
-        } else {
-            for (long long t = t_to - 1; t >= t_from; --t) {
-                step_compute(P, op, t, SFB_PART_ALL);
-                step_points(P, op, t, SFB_PART_ALL);
-            }
-        }
-        SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
-        SFB_CUDA(cudaStreamSynchronize(P.s_main));
-        float ms = 0.f;
-        SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
-        if (report) {
-            const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
-            const long long fpp = 3LL * P.K * P.ndim + 3LL * P.ndim + 11 + (ro.imaging ? 7 : 0);
-            report->seconds = ms * 1e-3;
-            report->steps = long(t_to - t_from);
-            report->flops = (long long)(double(fpp) * own * double(report->steps));
-            report->gflops = ms > 0 ? double(report->flops) / (ms * 1e-3) / 1e9 : 0.0;
-            report->gpts_per_s = ms > 0 ? own * double(report->steps) / (ms * 1e-3) / 1e9 : 0.0;
-            report->kernel_launches = P.launches - before;
-        }
-    });
+    return guarded(plan, [&] { run_window(*plan, op, t_from, t_to, true, report); });
+}
+
+SFB_API int sfb_time_stencil(sfb_plan* plan, int op, int64_t t_from, int64_t t_to,
+                             sfb_report* report) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] { run_window(*plan, op, t_from, t_to, false, report); });
 }
 
 SFB_API int sfb_forward(sfb_plan* plan, const double* src, double* rec, int64_t save_every,

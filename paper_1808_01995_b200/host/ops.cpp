@@ -1,0 +1,353 @@
+// ops.cpp -- forward / adjoint / gradient operators of the host layer on top of the C-ABI
+// engine (include/sfb200.h).  Structure follows the reference's entry points
+// (proj/src/seismic_ops.cpp:58-286); what the reference hands to its compiler and its
+// run_window (proj/src/seismic_ops.cpp:44-54) is handed to sfb_forward / sfb_adjoint /
+// sfb_gradient here.
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <thread>
+
+#include "sfb/seismic_ops.hpp"
+#include "sfb200.h"
+
+namespace sfb {
+
+namespace {
+thread_local int g_device = 0;
+}
+
+void set_device(int ordinal) { g_device = ordinal; }
+int device() { return g_device; }
+
+// One sfb_plan plus what is bound to it.
+class Engine {
+public:
+    Engine(const SeismicModel& model, const AcquisitionGeometry& geom, int space_order) {
+        const Grid& g = *model.grid();
+        sfb_plan_desc d{};
+        d.ndim = g.ndim();
+        for (int a = 0; a < d.ndim; ++a) {
+            d.shape[a] = g.shape()[std::size_t(a)];
+            d.spacing[a] = g.spacing()[std::size_t(a)];
+        }
+        d.space_order = space_order;
+        d.dt = geom.dt();
+        d.nt = geom.nt();
+        d.device = g_device;
+        int rc = sfb_plan_create(&d, &plan_);
+        if (rc != SFB_OK) raise_status(rc, sfb_last_error(nullptr));
+        try {
+            sfb_field_view mv = view(*model.m()), dv = view(*model.damp());
+            check(sfb_set_model(plan_, &mv, &dv, model.v_max()));
+            bind_cloud(SFB_CLOUD_SRC, *geom.src());
+            bind_cloud(SFB_CLOUD_REC, *geom.rec());
+        } catch (...) {
+            sfb_plan_destroy(plan_);
+            throw;
+        }
+    }
+    ~Engine() { sfb_plan_destroy(plan_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    sfb_plan* plan() const { return plan_; }
+    void check(int rc) const {
+        if (rc != SFB_OK) raise_status(rc, sfb_last_error(plan_));
+    }
+
+    static sfb_field_view view(const FieldBase& f) {
+        sfb_field_view v{};
+        const std::size_t nd = f.extents().size();
+        const int first = f.has_time() ? 1 : 0;
+        std::vector<long> zero(nd, 0);
+        v.ptr = f.values() + f.flat_index(zero);
+        for (std::size_t a = std::size_t(first); a < nd; ++a) v.stride[a - first] = f.stride(int(a));
+        return v;
+    }
+    // mutable view of time slot `slot` of a TimeFunction, or of a Function
+    static sfb_field_mview mview(const FieldBase& f, long slot = 0) {
+        sfb_field_view v = view(f);
+        sfb_field_mview m{};
+        m.ptr = const_cast<double*>(v.ptr) + (f.has_time() ? slot * f.stride(0) : 0);
+        for (int a = 0; a < 3; ++a) m.stride[a] = v.stride[a];
+        return m;
+    }
+
+private:
+    void bind_cloud(int which, SparseFunction& s) {
+        s.locate();
+        std::vector<int64_t> base(s.base_table().begin(), s.base_table().end());
+        check(sfb_set_points(plan_, which, s.npoints(), base.data(), s.weight_table().data()));
+    }
+
+    sfb_plan* plan_ = nullptr;
+};
+
+namespace {
+
+// proj/src/seismic_ops.cpp:15-22
+void check_cfl(const SeismicModel& model, const AcquisitionGeometry& geom, int space_order) {
+    const double crit = model.critical_dt(space_order);
+    if (geom.dt() > crit * (1.0 + 1e-12))
+        throw StabilityError("dt " + std::to_string(geom.dt()) + " exceeds the stable limit " +
+                             std::to_string(crit) + " at order " + std::to_string(space_order));
+}
+
+ExecutionReport to_report(const sfb_report& r) {
+    ExecutionReport e;
+    e.seconds = r.seconds;
+    e.flops = r.flops;
+    e.gflops = r.gflops;
+    e.steps = r.steps;
+    e.gpts_per_s = r.gpts_per_s;
+    e.kernel_launches = r.kernel_launches;
+    return e;
+}
+
+std::vector<double> cloud_coords(const SparseFunction& s) { return s.coords(); }
+
+}  // namespace
+
+// proj/src/seismic_ops.cpp:58-82
+WaveOp forward_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
+                        int space_order, bool save, std::vector<long> /*tiles*/) {
+    check_space_order(space_order);
+    check_cfl(model, geom, space_order);
+    WaveOp w;
+    w.dt = geom.dt();
+    w.nt = geom.nt();
+    w.space_order = space_order;
+    w.inj = geom.src();
+    w.smp = geom.rec();
+    w.save_every = save ? 1 : 0;
+    w.wavefield = save ? TimeFunction::create("u", model.grid(), space_order, 2, geom.nt())
+                       : TimeFunction::create("u", model.grid(), space_order, 2);
+    w.engine = std::make_shared<Engine>(model, geom, space_order);
+    return w;
+}
+
+// proj/src/seismic_ops.cpp:84-107: receiver traces are injected, the field is sampled at
+// the source coordinates into a fresh cloud "srca".
+WaveOp adjoint_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
+                        int space_order) {
+    check_space_order(space_order);
+    check_cfl(model, geom, space_order);
+    WaveOp w;
+    w.dt = geom.dt();
+    w.nt = geom.nt();
+    w.space_order = space_order;
+    w.adjoint = true;
+    w.inj = geom.rec();
+    w.smp = SparseFunction::create("srca", model.grid(), cloud_coords(*geom.src()), geom.nt());
+    w.smp->locate();
+    w.wavefield = TimeFunction::create("v", model.grid(), space_order, 2);
+    w.engine = std::make_shared<Engine>(model, geom, space_order);
+    return w;
+}
+
+// proj/src/seismic_ops.cpp:109-135
+GradientOp gradient_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
+                             int space_order, std::shared_ptr<TimeFunction> saved_u) {
+    check_space_order(space_order);
+    check_cfl(model, geom, space_order);
+    if (!saved_u || saved_u->time_buffered() || saved_u->time_slots() != geom.nt())
+        throw ParameterError("gradient_operator: saved forward history required");
+    if (!saved_u->device_history)
+        throw ParameterError("gradient_operator: saved forward history required "
+                             "(run the saving forward operator first: the history lives in HBM)");
+    GradientOp g;
+    g.dt = geom.dt();
+    g.nt = geom.nt();
+    g.space_order = space_order;
+    g.resid = SparseFunction::create("resid", model.grid(), cloud_coords(*geom.rec()), geom.nt());
+    g.resid->locate();
+    g.v = TimeFunction::create("v", model.grid(), space_order, 2);
+    g.grad = Function::create("grad", model.grid(), space_order);
+    // the forward operator's engine holds the history, the model and both clouds
+    g.engine = std::static_pointer_cast<Engine>(saved_u->device_history);
+    return g;
+}
+
+// proj/src/seismic_ops.cpp:137-141 (+ run_window :44-54)
+ExecutionReport run_wave(WaveOp& w, Backend, int) {
+    if (!w.engine) throw BindingError("run_wave: operator was not built");
+    Engine& e = *w.engine;
+    sfb_report rep{};
+    w.wavefield->zero();
+    if (!w.adjoint) {
+        e.check(sfb_forward(e.plan(), w.inj->traces().data(), w.smp->traces().data(),
+                            w.save_every, &rep));
+    } else {
+        e.check(sfb_adjoint(e.plan(), w.inj->traces().data(), w.smp->traces().data(), &rep));
+    }
+    // mirror the live time levels into the host TimeFunction (slot rules of
+    // proj/src/execute.cpp:187-199)
+    TimeFunction& u = *w.wavefield;
+    if (w.save_every > 0) {
+        u.device_history = w.engine;
+        u.device_save_every = w.save_every;
+        if (w.host_history && !u.time_buffered())
+            for (long t = 2; t < w.nt; t += 1) {
+                if (t % w.save_every != 0) continue;
+                sfb_field_mview mv = Engine::mview(u, t);
+                e.check(sfb_get_wavefield(e.plan(), 0, t, &mv));
+            }
+    } else if (w.nt >= 3) {
+        const long a = w.adjoint ? 0 : w.nt - 1, b = w.adjoint ? 1 : w.nt - 2;
+        for (long lvl : {a, b}) {
+            sfb_field_mview mv = Engine::mview(u, u.time_buffered() ? lvl % u.time_slots() : lvl);
+            e.check(sfb_get_wavefield(e.plan(), 0, lvl, &mv));
+        }
+    }
+    return to_report(rep);
+}
+
+// proj/src/seismic_ops.cpp:143-147
+ExecutionReport run_gradient(GradientOp& g, Backend, int) {
+    if (!g.engine) throw BindingError("run_gradient: operator was not built");
+    Engine& e = *g.engine;
+    sfb_report rep{};
+    g.v->zero();
+    g.grad->zero();
+    sfb_field_mview gv = Engine::mview(*g.grad);
+    e.check(sfb_gradient(e.plan(), g.resid->traces().data(), &gv, &rep));
+    return to_report(rep);
+}
+
+// proj/src/seismic_ops.cpp:149-160
+double objective(const SparseFunction& pred, const std::vector<double>& observed) {
+    const std::size_t n = std::size_t(pred.nt()) * std::size_t(pred.npoints());
+    if (observed.size() != n) throw ParameterError("objective: observed trace shape mismatch");
+    double phi = 0;
+    const std::vector<double>& p = pred.traces();
+    for (std::size_t i = 0; i < n; ++i) {
+        const double r = p[i] - observed[i];
+        phi += 0.5 * r * r;
+    }
+    return phi;
+}
+
+namespace {
+
+// adjoint of the edge-clamped extension, proj/src/seismic_ops.cpp:166-193: every padded
+// cell is summed onto the physical cell it copies, padded cells visited in row-major order
+std::vector<double> fold_gradient(const SeismicModel& model, const Function& grad) {
+    const std::vector<long>& ps = model.physical_shape();
+    const std::vector<long>& shape = model.grid()->shape();
+    const int nd = int(shape.size()), off = 3 - nd;
+    long N[3] = {1, 1, 1}, pn[3] = {1, 1, 1}, pad[3] = {0, 0, 0}, st[3] = {0, 0, 0};
+    for (int a = 0; a < nd; ++a) {
+        N[off + a] = shape[std::size_t(a)];
+        pn[off + a] = ps[std::size_t(a)];
+        pad[off + a] = model.nbl();
+        st[off + a] = grad.stride(a);
+    }
+    std::vector<long> zero(std::size_t(nd), 0);
+    const double* origin = grad.values() + grad.flat_index(zero);
+    std::vector<double> out(std::size_t(pn[0]) * pn[1] * pn[2], 0.0);
+    for (long i = 0; i < N[0]; ++i) {
+        const long pi = std::clamp(i - pad[0], 0L, pn[0] - 1);
+        for (long j = 0; j < N[1]; ++j) {
+            const long pj = std::clamp(j - pad[1], 0L, pn[1] - 1);
+            const double* row = origin + i * st[0] + j * st[1];
+            double* orow = out.data() + (std::size_t(pi) * pn[1] + pj) * pn[2];
+            for (long l = 0; l < N[2]; ++l) orow[std::clamp(l - pad[2], 0L, pn[2] - 1)] += row[l];
+        }
+    }
+    return out;
+}
+
+}  // namespace
+
+// proj/src/seismic_ops.cpp:197-216
+GradientResult fwi_gradient(const SeismicModel& model, AcquisitionGeometry& geom,
+                            const std::vector<double>& observed, int space_order, Backend backend,
+                            long save_every) {
+    if (save_every < 1) throw ParameterError("fwi_gradient: save_every must be >= 1");
+    WaveOp fwd = forward_operator(model, geom, space_order, true);
+    fwd.save_every = save_every;
+    fwd.host_history = false;  // the history stays in HBM
+    run_wave(fwd, backend);
+    GradientResult res;
+    res.objective = objective(*geom.rec(), observed);
+    GradientOp g = gradient_operator(model, geom, space_order, fwd.wavefield);
+    const std::size_t n = std::size_t(geom.nt()) * std::size_t(geom.n_rec());
+    res.residual.resize(n);
+    const std::vector<double>& pred = geom.rec()->traces();
+    for (std::size_t i = 0; i < n; ++i) res.residual[i] = pred[i] - observed[i];
+    g.resid->traces() = res.residual;
+    run_gradient(g, backend);
+    res.gradient = fold_gradient(model, *g.grad);
+    return res;
+}
+
+// proj/src/seismic_ops.cpp:218-286: fixed-step projected gradient descent; shot gradients
+// computed cfg.nthreads at a time (one engine per shot) and reduced in shot order.
+FwiResult fwi(SeismicModel& model, std::vector<AcquisitionGeometry>& shots,
+              const std::vector<std::vector<double>>& observed, const FwiConfig& cfg,
+              const std::vector<double>* true_m) {
+    if (shots.empty() || shots.size() != observed.size())
+        throw ParameterError("fwi: one observed record per shot required");
+    if (!(cfg.m_min > 0.0) || !(cfg.m_max > cfg.m_min)) throw ParameterError("fwi: bad model box");
+    FwiResult out;
+    std::vector<double> m = model.physical_m();
+    double alpha = 0;
+    auto rms_error = [&](const std::vector<double>& cur) {
+        if (!true_m) return 0.0;
+        double s = 0;
+        for (std::size_t i = 0; i < cur.size(); ++i) s += (cur[i] - (*true_m)[i]) * (cur[i] - (*true_m)[i]);
+        return std::sqrt(s / double(cur.size()));
+    };
+    const int dev = device();
+    for (long it = 0; it < cfg.n_iter; ++it) {
+        std::vector<GradientResult> parts(shots.size());
+        std::vector<std::string> failures(shots.size());
+        const std::size_t width = cfg.nthreads > 1 ? std::size_t(cfg.nthreads) : 1;
+        for (std::size_t lo = 0; lo < shots.size(); lo += width) {
+            const std::size_t hi = std::min(shots.size(), lo + width);
+            std::vector<std::thread> pool;
+            for (std::size_t s = lo; s < hi; ++s)
+                pool.emplace_back([&, s] {
+                    set_device(dev);
+                    try {
+                        parts[s] = fwi_gradient(model, shots[s], observed[s], cfg.space_order,
+                                                cfg.backend);
+                    } catch (const Error& e) {
+                        failures[s] = e.what();
+                    }
+                });
+            for (auto& th : pool) th.join();
+        }
+        for (const auto& f : failures)
+            if (!f.empty()) throw StabilityError("fwi: shot failed: " + f);
+        double phi = 0;
+        std::vector<double> g(m.size(), 0.0);
+        for (const auto& p : parts) {
+            phi += p.objective;
+            for (std::size_t i = 0; i < g.size(); ++i) g[i] += p.gradient[i];
+        }
+        if (!std::isfinite(phi))
+            throw StabilityError("fwi: non-finite objective at iteration " + std::to_string(it));
+        out.objectives.push_back(phi);
+        out.model_rms.push_back(rms_error(m));
+        if (it == 0) {
+            double gmax = 0, mmax = 0;
+            for (double v : g) gmax = std::max(gmax, std::abs(v));
+            for (double v : m) mmax = std::max(mmax, std::abs(v));
+            if (gmax == 0.0) {
+                out.final_m = m;
+                return out;
+            }
+            alpha = cfg.step_scale * mmax / gmax;
+        }
+        for (std::size_t i = 0; i < m.size(); ++i)
+            m[i] = std::clamp(m[i] - alpha * g[i], cfg.m_min, cfg.m_max);
+        model.set_physical_m(m);
+    }
+    out.model_rms.push_back(rms_error(m));
+    out.final_m = m;
+    return out;
+}
+
+}  // namespace sfb

@@ -1,0 +1,77 @@
+"""Seeded synthetic inputs of BASELINE.json's configurations.
+
+The reference uses no public dataset and BASELINE.json names none: every benchmark and
+full-size test runs on the generators below (numpy default_rng(seed) + a separable
+Gaussian blur), which stand in for no external data.  Host-side input generation only --
+nothing here is on the propagator path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED = 18080199  # base seed; +i per field
+
+
+def smooth_field(shape, seed, sigma, lo, hi, dtype=np.float32):
+    """Gaussian blur (sigma in cells, periodic so the statistics are uniform) of N(0,1)
+    noise, mapped linearly to [lo, hi]."""
+    from scipy.ndimage import gaussian_filter1d
+    g = np.random.default_rng(seed).standard_normal(shape, dtype=dtype)
+    for ax in range(len(shape)):
+        g = gaussian_filter1d(g, float(sigma), axis=ax, mode="wrap", truncate=3.0)
+    gmin, gmax = float(g.min()), float(g.max())
+    return (lo + (hi - lo) * (g.astype(np.float64) - gmin) / (gmax - gmin))
+
+
+def two_layer(shape, split, v_top=1.5, v_bottom=2.5):
+    """Two layers split on the depth (last, contiguous) axis (proj/src/verify.cpp:210-213)."""
+    v = np.empty(shape, dtype=np.float64)
+    v[..., :split] = v_top
+    v[..., split:] = v_bottom
+    return v
+
+
+def receiver_grid(n0, n1, h, depth):
+    """n0 x n1 receivers on the lattice at fixed depth: (h*i, h*j, depth)."""
+    ii, jj = np.meshgrid(np.arange(n0) * h, np.arange(n1) * h, indexing="ij")
+    return np.stack([ii.ravel(), jj.ravel(), np.full(ii.size, float(depth))], axis=1)
+
+
+def config(number: int, n: int | None = None, nsteps: int | None = None):
+    """Parameters of BASELINE.json config `number` (1-based), optionally shrunk to n^3
+    physical nodes / nsteps time steps for parity tests.  Returns a dict; velocity is
+    generated lazily by the caller via the 'velocity' callable."""
+    if number == 1:
+        n = n or 101
+        return dict(name="cfg1_acoustic_so4_101", shape=[n, n, n], h=10.0, nbl=40, order=4,
+                    f0=0.010, velocity=lambda: two_layer([n, n, n], n // 2 if n != 101 else 50),
+                    src=[[(n - 1) * 5.0, (n - 1) * 5.0, 20.0]],
+                    rec=np.array([[10.0 * i, (n - 1) * 5.0, 20.0] for i in range(n)]),
+                    tn=1000.0, nsteps=nsteps)
+    if number in (2, 3):
+        n = n or 512
+        h = 12.5
+        c = h * (n - 1) / 2.0 + h / 4.0  # off-node, centre of the grid (3193.75 at n=512)
+        vel = (lambda: smooth_field([n, n, n], SEED, 8.0, 1.5, 4.5)) if number == 2 else \
+              (lambda: two_layer([n, n, n], n // 2))
+        return dict(name=f"cfg{number}_acoustic_so8_{n}", shape=[n, n, n], h=h, nbl=40, order=8,
+                    f0=0.015, velocity=vel, src=[[c, c, 18.75]],
+                    rec=receiver_grid(n, n, h, 25.0), tn=None, nsteps=nsteps or 500)
+    if number == 5:
+        n = n or 1024
+        h = 12.5
+        rng = np.random.default_rng(SEED + 7)
+        src = rng.uniform(0.0, h * (n - 1), size=(8, 3))
+        return dict(name=f"cfg5_acoustic_so16_{n}", shape=[n, n, n], h=h, nbl=40, order=16,
+                    f0=0.015, velocity=lambda: smooth_field([n, n, n], SEED + 6, 8.0, 1.5, 4.5),
+                    src=src, rec=receiver_grid(n, n, h, 25.0), tn=None, nsteps=nsteps or 1000)
+    raise ValueError(f"no acoustic config {number}")
+
+
+def time_axis(critical_dt, nsteps=None, tn=None):
+    """dt = the CFL critical dt; tn chosen so that floor(tn/dt)+1 = nsteps+2 robustly
+    (SURVEY.md section 8d), unless the config fixes tn."""
+    dt = critical_dt
+    if tn is None or nsteps is not None:
+        tn = (nsteps + 1.5) * dt
+    return dt, tn

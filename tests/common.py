@@ -9,7 +9,7 @@ SEED = 18080199
 def smooth_field(shape, seed, sigma, lo, hi):
     """Seeded Gaussian-smoothed noise mapped linearly to [lo, hi] (config 2 recipe)."""
     from scipy.ndimage import gaussian_filter
-    g = gaussian_filter(np.random.default_rng(seed).standard_normal(shape), sigma, mode="nearest")
+    g = gaussian_filter(np.random.default_rng(seed).standard_normal(shape), sigma, mode="wrap")
     return lo + (hi - lo) * (g - g.min()) / (g.max() - g.min())
 
 
