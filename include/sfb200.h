@@ -204,6 +204,8 @@ SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_
 SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk);
 SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* stages, int* chunk,
                          int* separable_damping);
+/* kernels launched by this plan since the last sfb_step_begin */
+SFB_API int sfb_launch_count(sfb_plan* plan, int64_t* count);
 /* on != 0: always stream the dense damp array, even when it is a sum of 1-D profiles
  * (build_damping, proj/src/model.cpp:35-56) that the kernel could rebuild on the fly.
  * Call before sfb_set_model. */

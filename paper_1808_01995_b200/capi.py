@@ -47,7 +47,7 @@ SYMBOLS = [
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
     "sfb_step_points", "sfb_step_end", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
-    "sfb_set_dense_damping",
+    "sfb_set_dense_damping", "sfb_launch_count",
 ]
 
 lib.sfb_last_error.restype = C.c_char_p
@@ -77,6 +77,7 @@ lib.sfb_copy_halo.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
 lib.sfb_set_tile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
 lib.sfb_get_tile.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 5
 lib.sfb_set_dense_damping.argtypes = [C.c_void_p, C.c_int]
+lib.sfb_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
 lib.sfb_fd_weights.argtypes = [C.c_int, C.c_int, C.c_void_p]
 lib.sfb_critical_dt.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double)]
 lib.sfb_locate.argtypes = [C.POINTER(PlanDesc), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -230,6 +231,11 @@ class Plan:
         v = [C.c_int() for _ in range(5)]
         self._chk(lib.sfb_get_tile(self.h, *[C.byref(x) for x in v]))
         return dict(zip(["txv", "ty", "stages", "chunk", "sep"], [x.value for x in v]))
+
+    def launch_count(self):
+        n = C.c_int64()
+        self._chk(lib.sfb_launch_count(self.h, C.byref(n)))
+        return n.value
 
     def set_dense_damping(self, on=True):
         self._chk(lib.sfb_set_dense_damping(self.h, int(on)))

@@ -9,8 +9,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <numeric>
+#include <thread>
 
 #include "fdweights.hpp"
 #include "plan.hpp"
@@ -382,29 +384,93 @@ void build_cloud(Plan& P, Cloud& c) {
     c.set = true;
 }
 
-void upload_traces(Plan& P, Cloud& c, const double* host) {
-    const long long n = P.desc.nt * c.np;
-    DevBuf tmp;
-    tmp.alloc(size_t(n) * 8, false);
-    SFB_CUDA(cudaMemcpyAsync(tmp.p, host, size_t(n) * 8, cudaMemcpyHostToDevice, P.s_main));
-    const int nb = int(std::min<long long>((n + 255) / 256, 148 * 16));
-    convert_f64_f32_flat<<<std::max(nb, 1), 256, 0, P.s_main>>>(tmp.as<double>(),
-                                                               c.tr_in.as<float>(), n);
-    SFB_CUDA(cudaGetLastError());
+// ---- trace traffic: fp32 on the wire, repacked to/from the caller's f64 on host threads ----
+
+constexpr size_t kStageBytes = 32u << 20;  // per half
+
+template <typename Fn>
+void parallel_chunks(long long n, Fn&& fn) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nthr = unsigned(std::max<long long>(1, std::min<long long>(hw, n / 65536)));
+    if (nthr <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const long long per = (n + nthr - 1) / nthr;
+    for (unsigned i = 0; i < nthr; ++i) {
+        const long long b = i * per, e = std::min(n, b + per);
+        if (b < e) pool.emplace_back([=, &fn] { fn(b, e); });
+    }
+    for (auto& t : pool) t.join();
+}
+
+void widen(const float* src, double* dst, long long n) {
+    parallel_chunks(n, [=](long long b, long long e) {
+        for (long long i = b; i < e; ++i) dst[i] = double(src[i]);
+    });
+}
+
+void narrow(const double* src, float* dst, long long n) {
+    parallel_chunks(n, [=](long long b, long long e) {
+        for (long long i = b; i < e; ++i) dst[i] = float(src[i]);
+    });
+}
+
+// host f64 [n] -> device fp32 [n], chunked through the pinned halves
+void upload_f32(Plan& P, const double* host, float* dev, long long n) {
+    PinnedStage& st = P.stage;
+    const long long cap = (long long)std::min<size_t>(kStageBytes / 4, size_t(std::max<long long>(n, 1)));
+    st.ensure(size_t(cap));
+    int b = 0;
+    bool used[2] = {false, false};
+    for (long long off = 0; off < n; off += cap, b ^= 1) {
+        const long long len = std::min(cap, n - off);
+        if (used[b]) SFB_CUDA(cudaEventSynchronize(st.moved[b]));
+        narrow(host + off, st.p[b], len);
+        SFB_CUDA(cudaMemcpyAsync(dev + off, st.p[b], size_t(len) * 4, cudaMemcpyHostToDevice,
+                                 P.s_main));
+        SFB_CUDA(cudaEventRecord(st.moved[b], P.s_main));
+        used[b] = true;
+    }
     SFB_CUDA(cudaStreamSynchronize(P.s_main));
+}
+
+// device fp32 [n] -> host f64 [n]; the device data must be complete on s_main
+void download_f32(Plan& P, const float* dev, double* host, long long n) {
+    PinnedStage& st = P.stage;
+    const long long cap = (long long)std::min<size_t>(kStageBytes / 4, size_t(std::max<long long>(n, 1)));
+    st.ensure(size_t(cap));
+    long long pend_off[2] = {0, 0}, pend_len[2] = {0, 0};
+    int b = 0;
+    for (long long off = 0; off < n; off += cap, b ^= 1) {
+        const long long len = std::min(cap, n - off);
+        SFB_CUDA(cudaMemcpyAsync(st.p[b], dev + off, size_t(len) * 4, cudaMemcpyDeviceToHost,
+                                 P.s_main));
+        SFB_CUDA(cudaEventRecord(st.moved[b], P.s_main));
+        pend_off[b] = off;
+        pend_len[b] = len;
+        if (pend_len[b ^ 1]) {  // repack the previous chunk while this one is in flight
+            SFB_CUDA(cudaEventSynchronize(st.moved[b ^ 1]));
+            widen(st.p[b ^ 1], host + pend_off[b ^ 1], pend_len[b ^ 1]);
+            pend_len[b ^ 1] = 0;
+        }
+    }
+    for (int i = 0; i < 2; ++i)
+        if (pend_len[i]) {
+            SFB_CUDA(cudaEventSynchronize(st.moved[i]));
+            widen(st.p[i], host + pend_off[i], pend_len[i]);
+        }
+}
+
+void upload_traces(Plan& P, Cloud& c, const double* host) {
+    upload_f32(P, host, c.tr_in.as<float>(), P.desc.nt * c.np);
     c.has_in = true;
 }
 
 void download_traces(Plan& P, Cloud& c, double* host) {
-    const long long n = P.desc.nt * c.np;
-    DevBuf tmp;
-    tmp.alloc(size_t(n) * 8, false);
-    const int nb = int(std::min<long long>((n + 255) / 256, 148 * 16));
-    convert_f32_f64_flat<<<std::max(nb, 1), 256, 0, P.s_main>>>(c.tr_out.as<float>(),
-                                                               tmp.as<double>(), n);
-    SFB_CUDA(cudaGetLastError());
-    SFB_CUDA(cudaMemcpyAsync(host, tmp.p, size_t(n) * 8, cudaMemcpyDeviceToHost, P.s_main));
     SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    download_f32(P, c.tr_out.as<float>(), host, P.desc.nt * c.np);
 }
 
 // ---- stepping ------------------------------------------------------------------------------
@@ -630,21 +696,69 @@ void finite_guard(Plan& P, const char* what) {
     if (bad) throw Failure(SFB_ERR_STABILITY, std::string(what) + ": wavefield went non-finite");
 }
 
-void run_op(Plan& P, int op, long long save_every, sfb_report* rep) {
+// Streams the sampled trace rows to the caller's f64 table while the time loop runs: every
+// `rows` completed rows are copied (fp32, copy stream, pinned half) and the previous chunk
+// is widened on host threads in the shadow of the GPU.
+struct RowStreamer {
+    Plan& P;
+    Cloud& c;
+    double* host;
+    long long rows;            // rows per chunk
+    long long lo = -1, hi = -1;  // rows gathered since the last flush
+    int b = 0;
+    long long pend_row[2] = {0, 0}, pend_rows[2] = {0, 0};
+
+    RowStreamer(Plan& p, Cloud& cl, double* h) : P(p), c(cl), host(h) {
+        rows = std::max<long long>(1, (long long)(kStageBytes / 4) / std::max<long long>(c.np, 1));
+        P.stage.ensure(size_t(rows * c.np));
+    }
+    void drain(int i) {
+        if (!pend_rows[i]) return;
+        SFB_CUDA(cudaEventSynchronize(P.stage.moved[i]));
+        widen(P.stage.p[i], host + pend_row[i] * c.np, pend_rows[i] * c.np);
+        pend_rows[i] = 0;
+    }
+    void flush() {
+        if (lo < 0) return;
+        PinnedStage& st = P.stage;
+        SFB_CUDA(cudaEventRecord(st.ready[b], P.s_main));
+        SFB_CUDA(cudaStreamWaitEvent(st.copy, st.ready[b], 0));
+        SFB_CUDA(cudaMemcpyAsync(st.p[b], c.tr_out.as<float>() + lo * c.np,
+                                 size_t((hi - lo + 1) * c.np) * 4, cudaMemcpyDeviceToHost, st.copy));
+        SFB_CUDA(cudaEventRecord(st.moved[b], st.copy));
+        pend_row[b] = lo;
+        pend_rows[b] = hi - lo + 1;
+        lo = hi = -1;
+        b ^= 1;
+        drain(b);  // the half we are about to reuse: its copy was queued a chunk ago
+    }
+    void row_done(long long t) {
+        lo = lo < 0 ? t : std::min(lo, t);
+        hi = hi < 0 ? t : std::max(hi, t);
+        if (hi - lo + 1 >= rows) flush();
+    }
+    void finish() {
+        flush();
+        drain(0);
+        drain(1);
+        // rows 0 and nt-1 are never sampled (structural zeros, seismic_ops.hpp:13-16)
+        std::fill(host, host + c.np, 0.0);
+        if (P.desc.nt > 1) std::fill(host + (P.desc.nt - 1) * c.np, host + P.desc.nt * c.np, 0.0);
+    }
+};
+
+void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stream_out = nullptr) {
     const OpRoles ro = roles(op);
     step_begin(P, op, save_every);
     const long long nt = P.desc.nt;
+    std::unique_ptr<RowStreamer> rs;
+    if (stream_out && ro.smp >= 0) rs.reset(new RowStreamer(P, P.cloud[ro.smp], stream_out));
     SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
-    if (!ro.backward) {
-        for (long long t = 1; t < nt - 1; ++t) {
-            step_compute(P, op, t, SFB_PART_ALL);
-            step_points(P, op, t, SFB_PART_ALL);
-        }
-    } else {
-        for (long long t = nt - 2; t >= 1; --t) {
-            step_compute(P, op, t, SFB_PART_ALL);
-            step_points(P, op, t, SFB_PART_ALL);
-        }
+    for (long long i = 0; i < nt - 2; ++i) {
+        const long long t = ro.backward ? nt - 2 - i : 1 + i;
+        step_compute(P, op, t, SFB_PART_ALL);
+        step_points(P, op, t, SFB_PART_ALL);
+        if (rs) rs->row_done(t);
     }
     SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
     SFB_CUDA(cudaStreamSynchronize(P.s_main));
@@ -652,6 +766,7 @@ void run_op(Plan& P, int op, long long save_every, sfb_report* rep) {
     SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
     finite_guard(P, op == SFB_OP_FORWARD ? "forward" : (op == SFB_OP_ADJOINT ? "adjoint" : "gradient"));
     if (op == SFB_OP_FORWARD && save_every > 0) P.history_valid = true;
+    if (rs) rs->finish();
     if (rep) {
         const long steps = long(std::max<long long>(0, nt - 2));
         int D = P.ndim;
@@ -1007,8 +1122,7 @@ SFB_API int sfb_forward(sfb_plan* plan, const double* src, double* rec, int64_t 
         require(src && rec, SFB_ERR_PARAMETER, "forward: null trace table");
         require(P.cloud[0].set && P.cloud[1].set, SFB_ERR_BINDING, "point clouds are not bound");
         upload_traces(P, P.cloud[SFB_CLOUD_SRC], src);
-        run_op(P, SFB_OP_FORWARD, save_every, report);
-        download_traces(P, P.cloud[SFB_CLOUD_REC], rec);
+        run_op(P, SFB_OP_FORWARD, save_every, report, rec);
     });
 }
 
@@ -1019,8 +1133,7 @@ SFB_API int sfb_adjoint(sfb_plan* plan, const double* rec, double* srca, sfb_rep
         require(rec && srca, SFB_ERR_PARAMETER, "adjoint: null trace table");
         require(P.cloud[0].set && P.cloud[1].set, SFB_ERR_BINDING, "point clouds are not bound");
         upload_traces(P, P.cloud[SFB_CLOUD_REC], rec);
-        run_op(P, SFB_OP_ADJOINT, 0, report);
-        download_traces(P, P.cloud[SFB_CLOUD_SRC], srca);
+        run_op(P, SFB_OP_ADJOINT, 0, report, srca);
     });
 }
 
@@ -1147,6 +1260,12 @@ SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_
         SFB_CUDA(cudaMemcpyAsync(dst, src, size_t(count) * 4, cudaMemcpyDeviceToDevice,
                                  dst_plan->s_main));
     });
+}
+
+SFB_API int sfb_launch_count(sfb_plan* plan, int64_t* count) {
+    if (!plan || !count) return SFB_ERR_PARAMETER;
+    *count = plan->launches;
+    return SFB_OK;
 }
 
 SFB_API int sfb_set_dense_damping(sfb_plan* plan, int on) {

@@ -60,6 +60,43 @@ struct DevBuf {
     }
 };
 
+// Pinned host staging for trace traffic: two halves so a transfer overlaps the host-side
+// f32<->f64 repacking of the previous chunk.
+struct PinnedStage {
+    float* p[2] = {nullptr, nullptr};
+    size_t floats = 0;  // per half
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr}, moved[2] = {nullptr, nullptr};
+    PinnedStage() = default;
+    PinnedStage(const PinnedStage&) = delete;
+    PinnedStage& operator=(const PinnedStage&) = delete;
+    ~PinnedStage() {
+        for (int i = 0; i < 2; ++i) {
+            if (p[i]) cudaFreeHost(p[i]);
+            if (ready[i]) cudaEventDestroy(ready[i]);
+            if (moved[i]) cudaEventDestroy(moved[i]);
+        }
+        if (copy) cudaStreamDestroy(copy);
+    }
+    void ensure(size_t n) {
+        if (!copy) {
+            SFB_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                SFB_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+                SFB_CUDA(cudaEventCreateWithFlags(&moved[i], cudaEventDisableTiming));
+            }
+        }
+        if (n <= floats) return;
+        for (int i = 0; i < 2; ++i) {
+            if (p[i]) cudaFreeHost(p[i]);
+            p[i] = nullptr;
+            SFB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p[i]), n * sizeof(float),
+                                   cudaHostAllocDefault));
+        }
+        floats = n;
+    }
+};
+
 // One sparse point cloud (sources or receivers) in both of its roles.
 struct Cloud {
     long long np = 0;
@@ -108,6 +145,7 @@ struct Plan {
     double v_max = 0;
 
     Cloud cloud[2];
+    PinnedStage stage;
 
     const StepVariant* variant = nullptr;       // chosen tile shape
     int chunk = 0;                              // output planes per block

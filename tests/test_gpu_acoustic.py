@@ -224,3 +224,46 @@ def test_slab_decomposition_matches_single_domain_bitwise():
     n0 = model.N[0]
     rec3, u3 = _run_slabs(model, geom, 8, [0, 20, 41, n0])
     assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
+
+
+def test_step_loop_engine_on_one_rank_matches_forward():
+    """slabs.step_loop + PlanEngine (the multi-GPU driver) with a single slab and no
+    neighbours must reproduce sfb_forward exactly."""
+    import torch
+    from paper_1808_01995_b200 import capi, slabs
+    model, geom = make_problem([40, 30, 34], 10.0, 8, 8, 50)
+    plan = make_plan(model, geom, 8)
+    rec1, _ = plan.forward(geom.src)
+    u1 = plan.wavefield(geom.nt - 1)
+    plan.close()
+
+    plan = make_plan(model, geom, 8)
+    plan.upload_traces(capi.CLOUD_SRC, geom.src)
+    eng = slabs.PlanEngine(plan, capi.OP_FORWARD, 0)
+    plan.step_begin(capi.OP_FORWARD)
+    slabs.step_loop(eng, slabs.HaloExchanger(0, 1), 1, geom.nt - 1)
+    torch.cuda.synchronize()
+    plan.step_end(capi.OP_FORWARD)
+    assert np.array_equal(plan.download_traces(capi.CLOUD_REC), rec1)
+    assert np.array_equal(plan.wavefield(geom.nt - 1), u1)
+    plan.close()
+
+
+def test_streamed_traces_with_many_receivers():
+    # enough receivers that the trace table leaves in several pinned chunks
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([24, 24, 24], 10.0, 6, 4, 30)
+    n = 36
+    L = model.spacing[0] * (model.shape[0] - 1)
+    xs = np.linspace(0.0, L, n)
+    rec = np.array([[x, y, 25.0] for x in xs for y in xs] * 260)  # 336960 points
+    geom2 = o.Geometry(model, geom.src_coords.ravel(), rec.ravel(), 0.0, geom.tn, geom.dt, geom.f0)
+    ref = o.forward(model, geom2, 4)
+    plan = make_plan(model, geom2, 4)
+    got, _ = plan.forward(geom2.src)
+    assert rel_l2(got, ref["smp"]) <= 1e-5
+    assert (got[[0, geom2.nt - 1]] == 0.0).all()
+    plan.upload_traces(capi.CLOUD_SRC, geom2.src)
+    plan.run_resident(capi.OP_FORWARD)
+    assert np.array_equal(plan.download_traces(capi.CLOUD_REC), got)
+    plan.close()
