@@ -341,6 +341,49 @@ def dense_steps(model, space_order, dt, steps, cur, old):
         raise MemoryError("oracle allocation failed")
 
 
+class _Tti(C.Structure):
+    _fields_ = [("eps", C.POINTER(C.c_double)), ("delta", C.POINTER(C.c_double)),
+                ("theta", C.POINTER(C.c_double)), ("phi", C.POINTER(C.c_double)),
+                ("w1", C.POINTER(C.c_double))]
+
+
+def tti_critical_dt(model: Model, space_order, eps_max):
+    """The builder's TTI time-step bound: the acoustic CFL rule
+    (src/model.cpp:103-111) evaluated with v_max*sqrt(1 + 2 eps_max), times 0.9 because the
+    rotated operator applies first-derivative stencils twice."""
+    return 0.9 * model.critical_dt(space_order) / np.sqrt(1.0 + 2.0 * eps_max)
+
+
+def tti_forward(model: Model, geom, space_order, eps, delta, theta, phi, src=None,
+                want_final=False, want_energy=False):
+    """Builder-defined TTI forward operator (no reference counterpart: parity unpinned)."""
+    w2 = second_derivative_weights(space_order)
+    w1 = first_derivative_weights(space_order)
+    g = _grid(model, space_order, geom.dt, geom.nt, w2)
+    fields = [np.ascontiguousarray(np.broadcast_to(np.asarray(f, dtype=np.float64), model.N))
+              for f in (eps, delta, theta, phi)]
+    t = _Tti(*[_p(f) for f in fields], _p(w1))
+    src = np.ascontiguousarray(geom.src if src is None else src, dtype=np.float64)
+    rec = np.zeros((geom.nt, geom.n_rec))
+    fp = np.empty(model.N) if want_final else None
+    fr = np.empty(model.N) if want_final else None
+    en = np.zeros(geom.nt) if want_energy else None
+    rc = lib().sfo_tti_forward(C.byref(g), C.byref(t), _p(model.m), _p(model.damp),
+                               C.c_long(geom.n_src), _p(geom.src_base, C.c_long), _p(geom.src_w),
+                               _p(src), C.c_long(geom.n_rec), _p(geom.rec_base, C.c_long),
+                               _p(geom.rec_w), _p(rec), _p(fp), _p(fr), _p(en))
+    if rc == 2:
+        raise ArithmeticError("field went non-finite")
+    if rc:
+        raise MemoryError("oracle allocation failed")
+    out = {"smp": rec}
+    if want_final:
+        out["p"], out["r"] = fp, fr
+    if want_energy:
+        out["energy"] = en
+    return out
+
+
 def num_threads():
     return int(lib().sfo_num_threads())
 

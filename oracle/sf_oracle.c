@@ -545,3 +545,172 @@ int sfo_dense_steps(const sfo_grid *g, const double *m, const double *damp, long
     free(inv0);
     return 0;
 }
+
+/* ====================================================================================
+ * TTI forward (pseudo-acoustic, rotated Laplacian).  NO REFERENCE COUNTERPART: the
+ * reference has no anisotropic operator, so this restates the builder's
+ * own formulation and its parity is UNPINNED by the reference.
+ *
+ *   m p_tt + damp p_t = (1+2 eps) H0(p) + sqrt(1+2 delta) Hz(r)
+ *   m r_tt + damp r_t = sqrt(1+2 delta) H0(p) + Hz(r)
+ *   g(f)  = a D0 f + b D1 f + c D2 f,      (a,b,c) = (sin th cos ph, sin th sin ph, cos th)
+ *   Hz(f) = D0(a g) + D1(b g) + D2(c g)    ( = -Dbar^T Dbar f: negative semi-definite )
+ *   H0(f) = L(f) - Hz(f),                   L = the acoustic order-k Laplacian
+ * D_i = centred order-k first derivative on axis i (weights w1_1..w1_K, antisymmetric),
+ * every field restricted to the grid with zero outside (the reference's halo convention).
+ * Time discretisation, damping, injection (into p and r, weight dt^2/m) and sampling (of
+ * p) are the acoustic operator's (Appendix B).  With eps = delta = theta = phi = 0 the
+ * two equations coincide and p = r follows the acoustic update exactly.
+ * ==================================================================================== */
+
+typedef struct {
+    const double *eps, *delta, *theta, *phi; /* compact [N0][N1][N2] */
+    const double *w1;                        /* first-derivative weights w1_1..w1_K */
+} sfo_tti;
+
+static void tti_g(const emb3 *e, const double *w1, const double *f, const double *a,
+                  const double *b, const double *c, double *g /* haloed */) {
+    const int K = e->K;
+    const long st[3] = {e->s0, e->s1, 1};
+    const double ih[3] = {sqrt(e->ih2[0]), sqrt(e->ih2[1]), sqrt(e->ih2[2])};
+#pragma omp parallel for collapse(2) schedule(static)
+    for (long i = 0; i < e->N[0]; ++i)
+        for (long j = 0; j < e->N[1]; ++j) {
+            size_t row = hidx(e, i, j, 0), crow = ((size_t)i * e->N[1] + j) * e->N[2];
+            for (long l = 0; l < e->N[2]; ++l) {
+                size_t q = row + l;
+                double d[3] = {0, 0, 0};
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (!e->act[ax]) continue;
+                    double s = 0.0;
+                    for (int jj = 1; jj <= K; ++jj)
+                        s += w1[jj - 1] * (f[q + jj * st[ax]] - f[q - jj * st[ax]]);
+                    d[ax] = s * ih[ax];
+                }
+                g[q] = a[crow + l] * d[0] + b[crow + l] * d[1] + c[crow + l] * d[2];
+            }
+        }
+}
+
+/* hz = D0(a g) + D1(b g) + D2(c g); abc are haloed copies so neighbours outside read 0 */
+static void tti_hz(const emb3 *e, const double *w1, const double *g, const double *ah,
+                   const double *bh, const double *ch, double *hz /* compact */) {
+    const int K = e->K;
+    const long st[3] = {e->s0, e->s1, 1};
+    const double ih[3] = {sqrt(e->ih2[0]), sqrt(e->ih2[1]), sqrt(e->ih2[2])};
+    const double *n[3] = {ah, bh, ch};
+#pragma omp parallel for collapse(2) schedule(static)
+    for (long i = 0; i < e->N[0]; ++i)
+        for (long j = 0; j < e->N[1]; ++j) {
+            size_t row = hidx(e, i, j, 0), crow = ((size_t)i * e->N[1] + j) * e->N[2];
+            for (long l = 0; l < e->N[2]; ++l) {
+                size_t q = row + l;
+                double acc = 0.0;
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (!e->act[ax]) continue;
+                    double s = 0.0;
+                    for (int jj = 1; jj <= K; ++jj) {
+                        size_t qp = q + jj * st[ax], qm = q - jj * st[ax];
+                        s += w1[jj - 1] * (n[ax][qp] * g[qp] - n[ax][qm] * g[qm]);
+                    }
+                    acc += s * ih[ax];
+                }
+                hz[crow + l] = acc;
+            }
+        }
+}
+
+static void to_haloed(const emb3 *e, const double *compact, double *haloed) {
+    memset(haloed, 0, e->total * sizeof(double));
+    for (long i = 0; i < e->N[0]; ++i)
+        for (long j = 0; j < e->N[1]; ++j)
+            memcpy(haloed + hidx(e, i, j, 0), compact + ((size_t)i * e->N[1] + j) * e->N[2],
+                   (size_t)e->N[2] * sizeof(double));
+}
+
+/* TTI forward sweep over [1, nt-1).  src [nt][nsrc] injected into p and r, rec [nt][nrec]
+ * samples p.  Optional outputs: final_p / final_r = level nt-1 (compact); energy [nt] =
+ * sum p^2 + r^2 per level written (growth / dissipation checks).  Returns 0 / 2 / 3. */
+int sfo_tti_forward(const sfo_grid *g, const sfo_tti *t, const double *m, const double *damp,
+                    long nsrc, const long *src_base, const double *src_w, const double *src_tr,
+                    long nrec, const long *rec_base, const double *rec_w, double *rec_tr,
+                    double *final_p, double *final_r, double *energy) {
+    emb3 e;
+    embed(g, &e);
+    const int K = e.K;
+    const long nt = g->nt;
+    size_t cnt = (size_t)e.N[0] * e.N[1] * e.N[2];
+    double *P[3], *R[3];
+    for (int s = 0; s < 3; ++s) {
+        P[s] = (double *)calloc(e.total, sizeof(double));
+        R[s] = (double *)calloc(e.total, sizeof(double));
+        if (!P[s] || !R[s]) return 3;
+    }
+    double *gp = (double *)calloc(e.total, sizeof(double)), *gr = (double *)calloc(e.total, sizeof(double));
+    double *ah = (double *)malloc(e.total * sizeof(double)), *bh = (double *)malloc(e.total * sizeof(double));
+    double *ch = (double *)malloc(e.total * sizeof(double));
+    double *a = (double *)malloc(cnt * sizeof(double)), *b = (double *)malloc(cnt * sizeof(double));
+    double *c = (double *)malloc(cnt * sizeof(double));
+    double *hzp = (double *)malloc(cnt * sizeof(double)), *hzr = (double *)malloc(cnt * sizeof(double));
+    double *inv0 = make_inv0(&e, g->dt, m, damp);
+    if (!gp || !gr || !ah || !bh || !ch || !a || !b || !c || !hzp || !hzr || !inv0) return 3;
+    for (size_t i = 0; i < cnt; ++i) {
+        a[i] = sin(t->theta[i]) * cos(t->phi[i]);
+        b[i] = sin(t->theta[i]) * sin(t->phi[i]);
+        c[i] = cos(t->theta[i]);
+    }
+    to_haloed(&e, a, ah);
+    to_haloed(&e, b, bh);
+    to_haloed(&e, c, ch);
+    memset(rec_tr, 0, (size_t)nt * (size_t)nrec * sizeof(double));
+    if (energy) memset(energy, 0, (size_t)nt * sizeof(double));
+    const double s0 = 1.0 / g->dt, s1 = 1.0 / (g->dt * g->dt);
+    const long st[3] = {e.s0, e.s1, 1};
+    for (long tt = 1; tt < nt - 1; ++tt) {
+        double *pc = P[tt % 3], *po = P[(tt - 1) % 3], *pn = P[(tt + 1) % 3];
+        double *rc = R[tt % 3], *ro = R[(tt - 1) % 3], *rn = R[(tt + 1) % 3];
+        tti_g(&e, t->w1, pc, a, b, c, gp);
+        tti_g(&e, t->w1, rc, a, b, c, gr);
+        tti_hz(&e, t->w1, gp, ah, bh, ch, hzp);
+        tti_hz(&e, t->w1, gr, ah, bh, ch, hzr);
+        double en = 0.0;
+#pragma omp parallel for collapse(2) schedule(static) reduction(+ : en)
+        for (long i = 0; i < e.N[0]; ++i)
+            for (long j = 0; j < e.N[1]; ++j) {
+                size_t row = hidx(&e, i, j, 0), crow = ((size_t)i * e.N[1] + j) * e.N[2];
+                for (long l = 0; l < e.N[2]; ++l) {
+                    size_t q = row + l, k = crow + l;
+                    double lap = 0.0;
+                    for (int d = 0; d < 3; ++d) {
+                        if (!e.act[d]) continue;
+                        double acc = g->w2[0] * pc[q];
+                        for (int jj = K; jj >= 1; --jj)
+                            acc += g->w2[jj] * (pc[q - jj * st[d]] + pc[q + jj * st[d]]);
+                        lap += acc * e.ih2[d];
+                    }
+                    const double h0 = lap - hzp[k];
+                    const double e1 = 1.0 + 2.0 * t->eps[k], e2 = sqrt(1.0 + 2.0 * t->delta[k]);
+                    const double rhs_p = e1 * h0 + e2 * hzr[k];
+                    const double rhs_r = e2 * h0 + hzr[k];
+                    pn[q] = (rhs_p - m[k] * (po[q] - 2.0 * pc[q]) * s1 + 0.5 * damp[k] * po[q] * s0) * inv0[k];
+                    rn[q] = (rhs_r - m[k] * (ro[q] - 2.0 * rc[q]) * s1 + 0.5 * damp[k] * ro[q] * s0) * inv0[k];
+                    en += pn[q] * pn[q] + rn[q] * rn[q];
+                }
+            }
+        inject_points(&e, g->ndim, g->dt, nsrc, src_base, src_w, src_tr + (size_t)tt * nsrc, pn, m);
+        inject_points(&e, g->ndim, g->dt, nsrc, src_base, src_w, src_tr + (size_t)tt * nsrc, rn, m);
+        sample_points(&e, g->ndim, nrec, rec_base, rec_w, pc, rec_tr + (size_t)tt * nrec);
+        if (energy) energy[tt + 1] = en;
+    }
+    if (final_p) compact_copy(&e, P[(nt - 1) % 3], final_p);
+    if (final_r) compact_copy(&e, R[(nt - 1) % 3], final_r);
+    int ok = 1;
+    for (int s = 0; s < 3; ++s) ok = ok && all_finite(P[s], e.total) && all_finite(R[s], e.total);
+    for (int s = 0; s < 3; ++s) {
+        free(P[s]);
+        free(R[s]);
+    }
+    free(gp); free(gr); free(ah); free(bh); free(ch); free(a); free(b); free(c);
+    free(hzp); free(hzr); free(inv0);
+    return ok ? 0 : 2;
+}

@@ -55,6 +55,8 @@ lib.sfb_last_error.argtypes = [C.c_void_p]
 lib.sfb_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]
 lib.sfb_plan_destroy.argtypes = [C.c_void_p]
 lib.sfb_set_model.argtypes = [C.c_void_p, C.POINTER(FieldView), C.POINTER(FieldView), C.c_double]
+lib.sfb_set_model_tti.argtypes = [C.c_void_p] + [C.POINTER(FieldView)] * 4
+lib.sfb_tti_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Report)]
 lib.sfb_set_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
 lib.sfb_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Report)]
 lib.sfb_adjoint.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Report)]
@@ -168,6 +170,18 @@ class Plan:
         damp = np.asarray(damp, dtype=np.float64)
         self._chk(lib.sfb_set_model(self.h, C.byref(_view(m)), C.byref(_view(damp)), float(v_max)))
 
+    def set_model_tti(self, epsilon, delta, theta, phi):
+        views = [_view(np.asarray(f, dtype=np.float64)) for f in (epsilon, delta, theta, phi)]
+        self._keep = views
+        self._chk(lib.sfb_set_model_tti(self.h, *[C.byref(v) for v in views]))
+
+    def tti_forward(self, src):
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        rec = np.empty((self.nt, self.np[CLOUD_REC]))
+        rep = Report()
+        self._chk(lib.sfb_tti_forward(self.h, src.ctypes.data, rec.ctypes.data, C.byref(rep)))
+        return rec, rep
+
     def set_points(self, cloud, base, w):
         base = np.ascontiguousarray(base, dtype=np.int64)
         w = np.ascontiguousarray(w, dtype=np.float64)
@@ -195,9 +209,9 @@ class Plan:
         self._chk(lib.sfb_gradient(self.h, resid.ctypes.data, C.byref(_view(grad)), C.byref(rep)))
         return grad, rep
 
-    def wavefield(self, level, out=None):
+    def wavefield(self, level, out=None, field=0):
         out = np.zeros(self.shape) if out is None else out
-        self._chk(lib.sfb_get_wavefield(self.h, 0, level, C.byref(_view(out))))
+        self._chk(lib.sfb_get_wavefield(self.h, field, level, C.byref(_view(out))))
         return out
 
     def upload_traces(self, cloud, tr):

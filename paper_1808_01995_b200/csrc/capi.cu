@@ -17,6 +17,7 @@
 #include "fdweights.hpp"
 #include "plan.hpp"
 #include "point_kernels.cuh"
+#include "tti_kernels.cuh"
 
 namespace sfb {
 
@@ -486,6 +487,7 @@ OpRoles roles(int op) {
     case SFB_OP_FORWARD: return {false, SFB_CLOUD_SRC, SFB_CLOUD_REC, false};
     case SFB_OP_ADJOINT: return {true, SFB_CLOUD_REC, SFB_CLOUD_SRC, false};
     case SFB_OP_GRADIENT: return {true, SFB_CLOUD_REC, -1, true};
+    case SFB_OP_TTI_FORWARD: return {false, SFB_CLOUD_SRC, SFB_CLOUD_REC, false};
     default: throw Failure(SFB_ERR_PARAMETER, "unknown operator id");
     }
 }
@@ -610,7 +612,8 @@ void step_compute(Plan& P, int op, long long t, int part) {
 
 // part: SFB_PART_ALL = every node + gather; SFB_PART_LOW = nodes of both boundary plane
 // groups (boundary stream); SFB_PART_INTERIOR = remaining nodes + gather
-void step_points(Plan& P, int op, long long t, int part) {
+void step_points(Plan& P, int op, long long t, int part, float* target_override = nullptr,
+                 bool allow_gather = true) {
     const OpRoles ro = roles(op);
     const int cur = int(t & 1), oth = cur ^ 1;
     const long long tnew = ro.backward ? t - 1 : t + 1;
@@ -624,7 +627,7 @@ void step_points(Plan& P, int op, long long t, int part) {
     bool gather = false;
     if (part == SFB_PART_ALL) {
         rg[0] = {0, ci.ncell};
-        gather = ro.smp >= 0;
+        gather = ro.smp >= 0 && allow_gather;
     } else if (part == SFB_PART_LOW || part == SFB_PART_HIGH) {
         rg[0] = {0, ci.cell_lo_end};
         rg[1] = {ci.cell_hi_begin, ci.ncell};
@@ -646,7 +649,7 @@ void step_points(Plan& P, int op, long long t, int part) {
         pp.ent_point = ci.ent_point.as<int>();
         pp.ent_w = ci.ent_w.as<float>();
         pp.inj_row = ci.tr_in.as<float>() + t * ci.np;
-        pp.target = P.u[oth].as<float>();
+        pp.target = target_override ? target_override : P.u[oth].as<float>();
         pp.r = P.r.as<float>();
         pp.inv_dt2 = P.coef.inv_dt2;
         if (op == SFB_OP_FORWARD && P.save_every > 0 && tnew % P.save_every == 0)
@@ -780,6 +783,100 @@ void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stre
         rep->gpts_per_s = rep->seconds > 0 ? own * steps / rep->seconds / 1e9 : 0.0;
         rep->kernel_launches = P.launches;
         (void)pts;
+    }
+}
+
+// ---- TTI forward ---------------------------------------------------------------------------
+
+void tti_fill_params(Plan& P, TtiParams& tp) {
+    tp.K = P.K;
+    double ih[3], ih2[3], c0 = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        ih[d] = P.act[d] ? 1.0 / P.h[d] : 0.0;
+        ih2[d] = ih[d] * ih[d];
+        c0 += P.w2[0] * ih2[d];
+    }
+    tp.c0 = float(c0);
+    for (int j = 1; j <= P.K; ++j) {
+        tp.lz[j - 1] = float(P.w2[j] * ih2[0]);
+        tp.ly[j - 1] = float(P.w2[j] * ih2[1]);
+        tp.lx[j - 1] = float(P.w2[j] * ih2[2]);
+        tp.fz[j - 1] = float(P.w1[j] * ih[0]);
+        tp.fy[j - 1] = float(P.w1[j] * ih[1]);
+        tp.fx[j - 1] = float(P.w1[j] * ih[2]);
+    }
+    tp.qscale = P.coef.qscale;
+    tp.n0 = P.n0;
+    tp.N1 = int(P.N[1]);
+    tp.N2 = int(P.N[2]);
+    tp.pitch = P.pitch;
+    tp.plane = P.plane;
+    tp.a = P.t_a.as<float>();
+    tp.b = P.t_b.as<float>();
+    tp.c = P.t_c.as<float>();
+    tp.e1 = P.t_e1.as<float>();
+    tp.e2 = P.t_e2.as<float>();
+    tp.rm = P.r.as<float>();
+    tp.damp = P.sep ? nullptr : P.damp.as<float>();
+    tp.dz = P.dz.as<float>();
+    tp.dy = P.dy.as<float>();
+    tp.dx = P.dx.as<float>();
+    tp.gp = P.t_gp.as<float>();
+    tp.gr = P.t_gr.as<float>();
+}
+
+void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
+    require(P.tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
+    require(P.n0 == P.N[0], SFB_ERR_CAPABILITY, "the TTI operator is single-slab in this round");
+    const int op = SFB_OP_TTI_FORWARD;
+    step_begin(P, op, 0);
+    for (int b = 0; b < 2; ++b)
+        SFB_CUDA(cudaMemsetAsync(P.t_r[b].p, 0, size_t(P.ucount) * 4, P.s_main));
+    SFB_CUDA(cudaMemsetAsync(P.t_gp.p, 0, size_t(P.ucount) * 4, P.s_main));
+    SFB_CUDA(cudaMemsetAsync(P.t_gr.p, 0, size_t(P.ucount) * 4, P.s_main));
+    TtiParams tp{};
+    tti_fill_params(P, tp);
+    const long long nt = P.desc.nt;
+    dim3 block(kTtiBX, kTtiBY);
+    dim3 grid(unsigned((P.N[2] + kTtiBX - 1) / kTtiBX), unsigned((P.N[1] + kTtiBY - 1) / kTtiBY),
+              unsigned(P.n0));
+    std::unique_ptr<RowStreamer> rs;
+    if (stream_out) rs.reset(new RowStreamer(P, P.cloud[SFB_CLOUD_REC], stream_out));
+    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+    for (long long t = 1; t < nt - 1; ++t) {
+        const int cur = int(t & 1), oth = cur ^ 1;
+        tp.pc = P.u[cur].as<float>();
+        tp.rc = P.t_r[cur].as<float>();
+        tp.po = P.u[oth].as<float>();
+        tp.ro = P.t_r[oth].as<float>();
+        tti_gradient_kernel<<<grid, block, 0, P.s_main>>>(tp);
+        tti_update_kernel<<<grid, block, 0, P.s_main>>>(tp);
+        SFB_CUDA(cudaGetLastError());
+        P.launches += 2;
+        step_points(P, op, t, SFB_PART_ALL);                                   // p: scatter + gather
+        step_points(P, op, t, SFB_PART_ALL, P.t_r[oth].as<float>(), false);    // r: scatter
+        P.live_level[cur] = t;
+        P.live_level[oth] = t + 1;
+        if (rs) rs->row_done(t);
+    }
+    SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    float ms = 0.f;
+    SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+    finite_guard(P, "tti_forward");
+    if (rs) rs->finish();
+    if (rep) {
+        const long steps = long(std::max<long long>(0, nt - 2));
+        const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
+        // per node: 2 fields x (3 first derivatives + rotation) + 2 x divergence of 3 products
+        // + Laplacian + 2 updates, adds and multiplies counted as the reference counts them
+        const long long fpp = 2LL * (6 * P.K + 5) + 2LL * (12 * P.K) + (9LL * P.K + 3) + 24;
+        rep->seconds = ms * 1e-3;
+        rep->steps = steps;
+        rep->flops = (long long)(double(fpp) * own * steps);
+        rep->gflops = ms > 0 ? double(rep->flops) / (ms * 1e-3) / 1e9 : 0.0;
+        rep->gpts_per_s = ms > 0 ? own * steps / (ms * 1e-3) / 1e9 : 0.0;
+        rep->kernel_launches = P.launches;
     }
 }
 
@@ -1026,11 +1123,62 @@ SFB_API int sfb_set_model(sfb_plan* plan, const sfb_field_view* m, const sfb_fie
     });
 }
 
-SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view*, const sfb_field_view*,
-                      const sfb_field_view*, const sfb_field_view*) {
+SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
+                              const sfb_field_view* delta, const sfb_field_view* theta,
+                              const sfb_field_view* phi) {
     if (!plan) return SFB_ERR_PARAMETER;
-    plan->err = "TTI operator is not built in this round";
-    return SFB_ERR_CAPABILITY;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(epsilon && delta && theta && phi && epsilon->ptr && delta->ptr && theta->ptr &&
+                    phi->ptr, SFB_ERR_PARAMETER, "set_model_tti: null field");
+        require(P.model_set, SFB_ERR_BINDING, "bind m and damp first (sfb_set_model)");
+        // stability gates of the builder's formulation: eps >= delta everywhere (the
+        // pseudo-acoustic system is ill-posed otherwise) and the acoustic CFL rule with
+        // v_max sqrt(1 + 2 eps_max), times 0.9 for the twice-applied first derivatives
+        const IntView ev = embed_view(P, epsilon->ptr, epsilon->stride);
+        const IntView dv = embed_view(P, delta->ptr, delta->stride);
+        double eps_max = 0.0;
+        bool ordered = true;
+        for (long long i = 0; i < P.N[0]; ++i)
+            for (long long j = 0; j < P.N[1]; ++j)
+                for (long long l = 0; l < P.N[2]; ++l) {
+                    const double e = ev.ptr[i * ev.s[0] + j * ev.s[1] + l * ev.s[2]];
+                    const double d = dv.ptr[i * dv.s[0] + j * dv.s[1] + l * dv.s[2]];
+                    eps_max = std::max(eps_max, e);
+                    ordered = ordered && e >= d && (1.0 + 2.0 * d) > 0.0;
+                }
+        if (!ordered)
+            throw Failure(SFB_ERR_STABILITY, "TTI medium needs epsilon >= delta > -1/2 everywhere");
+        if (P.v_max > 0.0) {
+            double crit = 0;
+            sfb_critical_dt(P.ndim, P.desc.spacing, P.v_max, P.desc.space_order, &crit);
+            crit *= 0.9 / std::sqrt(1.0 + 2.0 * eps_max);
+            if (P.desc.dt > crit * (1.0 + 1e-12))
+                throw Failure(SFB_ERR_STABILITY, "dt " + std::to_string(P.desc.dt) +
+                                                     " exceeds the TTI stable limit " +
+                                                     std::to_string(crit));
+        }
+        std::vector<Frac> w;
+        centred_weights(1, P.desc.space_order, w);
+        for (int j = 0; j <= P.K; ++j) P.w1[j] = to_double(w[j]);
+        DevBuf te, td, tt, tph;
+        upload_f64(P, ev, te);
+        upload_f64(P, dv, td);
+        upload_f64(P, embed_view(P, theta->ptr, theta->stride), tt);
+        upload_f64(P, embed_view(P, phi->ptr, phi->stride), tph);
+        for (int b = 0; b < 2; ++b) P.t_r[b].alloc(size_t(P.ucount) * 4);
+        for (DevBuf* d : {&P.t_gp, &P.t_gr, &P.t_a, &P.t_b, &P.t_c}) d->alloc(size_t(P.ucount) * 4);
+        P.t_e1.alloc(size_t(P.ccount) * 4);
+        P.t_e2.alloc(size_t(P.ccount) * 4);
+        const long long rows = (long long)P.n0 * P.N[1];
+        tti_setup_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(
+            te.as<double>(), td.as<double>(), tt.as<double>(), tph.as<double>(), P.t_a.as<float>(),
+            P.t_b.as<float>(), P.t_c.as<float>(), P.t_e1.as<float>(), P.t_e2.as<float>(), rows,
+            int(P.N[2]), P.pitch, (long long)P.K * P.plane);
+        SFB_CUDA(cudaGetLastError());
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        P.tti_set = true;
+    });
 }
 
 SFB_API int sfb_set_points(sfb_plan* plan, int cloud, int64_t np, const int64_t* base,
@@ -1070,7 +1218,12 @@ SFB_API int sfb_download_traces(sfb_plan* plan, int cloud, double* traces) {
 
 SFB_API int sfb_run_resident(sfb_plan* plan, int op, int64_t save_every, sfb_report* report) {
     if (!plan) return SFB_ERR_PARAMETER;
-    return guarded(plan, [&] { run_op(*plan, op, save_every, report); });
+    return guarded(plan, [&] {
+        if (op == SFB_OP_TTI_FORWARD)
+            run_tti(*plan, report, nullptr);
+        else
+            run_op(*plan, op, save_every, report);
+    });
 }
 
 namespace {
@@ -1152,20 +1305,27 @@ SFB_API int sfb_gradient(sfb_plan* plan, const double* resid, const sfb_field_mv
     });
 }
 
-SFB_API int sfb_tti_forward(sfb_plan* plan, const double*, double*, sfb_report*) {
+SFB_API int sfb_tti_forward(sfb_plan* plan, const double* src, double* rec, sfb_report* report) {
     if (!plan) return SFB_ERR_PARAMETER;
-    plan->err = "TTI operator is not built in this round";
-    return SFB_ERR_CAPABILITY;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(src && rec, SFB_ERR_PARAMETER, "tti_forward: null trace table");
+        require(P.cloud[0].set && P.cloud[1].set, SFB_ERR_BINDING, "point clouds are not bound");
+        upload_traces(P, P.cloud[SFB_CLOUD_SRC], src);
+        run_tti(P, report, rec);
+    });
 }
 
 SFB_API int sfb_get_wavefield(sfb_plan* plan, int field, int64_t level, const sfb_field_mview* out) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
         Plan& P = *plan;
-        require(out && out->ptr && field == 0, SFB_ERR_PARAMETER, "get_wavefield: bad argument");
+        require(out && out->ptr && (field == 0 || (field == 1 && P.tti_set)), SFB_ERR_PARAMETER,
+                "get_wavefield: bad argument");
         for (int b = 0; b < 2; ++b)
             if (P.live_level[b] == level) {
-                download_field(P, P.u[b].as<float>() + (long long)P.K * P.plane, out);
+                const DevBuf& buf = field == 1 ? P.t_r[b] : P.u[b];
+                download_field(P, buf.as<float>() + (long long)P.K * P.plane, out);
                 return;
             }
         if (P.history_valid && P.save_every > 0 && level >= 0 && level % P.save_every == 0 &&

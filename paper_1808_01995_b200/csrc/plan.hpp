@@ -147,6 +147,11 @@ struct Plan {
     Cloud cloud[2];
     PinnedStage stage;
 
+    // TTI operator state (builder-defined formulation, csrc/tti_kernels.cuh)
+    bool tti_set = false;
+    DevBuf t_r[2], t_gp, t_gr, t_a, t_b, t_c, t_e1, t_e2;  // p lives in u[2]
+    double w1[kMaxK + 1] = {0};                             // first-derivative weights
+
     const StepVariant* variant = nullptr;       // chosen tile shape
     int chunk = 0;                              // output planes per block
 

@@ -1,0 +1,92 @@
+"""TTI forward operator on the GPU against the builder's own f64 oracle restatement.
+The reference has no TTI operator: parity here is UNPINNED by the
+reference; the pins are the self-checks the survey lists -- the isotropic limit reproduces
+the acoustic operator, the wavefield does not grow over 500 steps, the layer dissipates."""
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+from tests.common import make_plan, make_problem, rel_l2, smooth_field
+
+pytestmark = pytest.mark.gpu
+
+
+def tti_fields(N, seed=1):
+    eps = smooth_field(N, seed + 1, 3.0, 0.0, 0.3)
+    delta = np.minimum(smooth_field(N, seed + 2, 3.0, 0.0, 0.2), eps)  # eps >= delta
+    theta = smooth_field(N, seed + 3, 3.0, 0.0, np.pi / 4)
+    phi = smooth_field(N, seed + 4, 3.0, 0.0, np.pi / 4)
+    return eps, delta, theta, phi
+
+
+def tti_problem(shape, order, nsteps, nbl=8, h=10.0):
+    model, geom0 = make_problem(shape, h, nbl, order, nsteps, dt_frac=0.5)
+    dt = o.tti_critical_dt(model, order, 0.3)
+    geom = o.Geometry(model, geom0.src_coords.ravel(), geom0.rec_coords.ravel(), 0.0,
+                      (nsteps + 1.5) * dt, dt, 0.015)
+    assert geom.nt == nsteps + 2
+    return model, geom
+
+
+@pytest.mark.parametrize("order", [4, 8, 12])
+def test_tti_parity_with_oracle(order):
+    model, geom = tti_problem([30, 26, 34], order, 100)
+    eps, delta, theta, phi = tti_fields(model.N)
+    ref = o.tti_forward(model, geom, order, eps, delta, theta, phi, want_final=True)
+    plan = make_plan(model, geom, order)
+    plan.set_model_tti(eps, delta, theta, phi)
+    rec, rep = plan.tti_forward(geom.src)
+    assert rep.steps == 100 and np.abs(ref["smp"]).max() > 0
+    assert rel_l2(rec, ref["smp"]) <= 1e-5
+    assert rel_l2(plan.wavefield(geom.nt - 1, field=0), ref["p"]) <= 1e-5
+    assert rel_l2(plan.wavefield(geom.nt - 1, field=1), ref["r"]) <= 1e-5
+    plan.close()
+
+
+def test_tti_isotropic_limit_is_the_acoustic_operator():
+    model, geom = make_problem([28, 24, 30], 10.0, 8, 8, 80, dt_frac=0.8)
+    z = np.zeros(model.N)
+    plan = make_plan(model, geom, 8)
+    plan.set_model_tti(z, z, z, z)
+    rec_t, _ = plan.tti_forward(geom.src)
+    p = plan.wavefield(geom.nt - 1, field=0)
+    r = plan.wavefield(geom.nt - 1, field=1)
+    rec_a, _ = plan.forward(geom.src)
+    u = plan.wavefield(geom.nt - 1)
+    assert rel_l2(rec_t, rec_a) <= 2e-6 and rel_l2(p, u) <= 2e-6 and np.array_equal(p, r)
+    plan.close()
+
+
+def test_tti_no_growth_over_500_steps():
+    model, geom = tti_problem([24, 22, 26], 8, 500, nbl=6)
+    eps, delta, theta, phi = tti_fields(model.N, seed=7)
+    plan = make_plan(model, geom, 8)
+    plan.set_model_tti(eps, delta, theta, phi)
+    rec, _ = plan.tti_forward(geom.src)
+    ref = o.tti_forward(model, geom, 8, eps, delta, theta, phi, want_final=True)
+    assert np.isfinite(rec).all()
+    # late-time amplitude stays below the peak: no exponential growth
+    assert np.abs(rec[400:]).max() <= np.abs(rec).max()
+    assert rel_l2(rec, ref["smp"]) <= 1e-4                    # full run tolerance
+    assert rel_l2(plan.wavefield(geom.nt - 1, field=0), ref["p"]) <= 1e-4
+    plan.close()
+
+
+def test_tti_rejects_ill_posed_medium_and_large_dt():
+    from paper_1808_01995_b200 import capi
+    model, geom = tti_problem([20, 20, 20], 8, 10, nbl=6)
+    eps, delta, theta, phi = tti_fields(model.N)
+    plan = make_plan(model, geom, 8)
+    with pytest.raises(capi.SfbError) as e:
+        plan.set_model_tti(delta * 0.5, delta + 0.01, theta, phi)   # eps < delta
+    assert e.value.code == capi.ERR_STABILITY
+    with pytest.raises(capi.SfbError) as e:
+        plan.tti_forward(geom.src)                                   # fields never bound
+    assert e.value.code == capi.ERR_BINDING
+    plan.close()
+    model2, geom2 = make_problem([20, 20, 20], 10.0, 6, 8, 10)       # acoustic critical dt
+    plan = make_plan(model2, geom2, 8)
+    with pytest.raises(capi.SfbError) as e:
+        plan.set_model_tti(eps, delta, theta, phi)
+    assert e.value.code == capi.ERR_STABILITY
+    plan.close()
