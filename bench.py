@@ -250,7 +250,7 @@ def ours(args):
     pts = float(np.prod(N))
     t0 = time.time()
     plan = make_plan(model, geom, local)
-    tile = plan.get_tile()
+    tile = plan.autotune()   # as in the paper, timing starts after the tile-shape autotuning
     log(f"[bench] plan + uploads in {time.time() - t0:.1f}s, tile {tile}")
     src = geom.src.traces
     plan.upload_traces(capi.CLOUD_SRC, src)

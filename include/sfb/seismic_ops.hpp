@@ -45,6 +45,9 @@ struct WaveOp {
     // into `wavefield` as the reference does (proj/src/seismic_ops.cpp:66-68).
     long save_every = 0;
     bool host_history = true;
+    // TTI operator only: the auxiliary field r of the coupled pair (wavefield holds p)
+    bool tti = false;
+    std::shared_ptr<TimeFunction> wavefield_r;
 };
 
 // proj/include/sf/seismic_ops.hpp:28-30, proj/src/seismic_ops.cpp:58-82
@@ -53,6 +56,28 @@ WaveOp forward_operator(const SeismicModel& model, const AcquisitionGeometry& ge
 // proj/include/sf/seismic_ops.hpp:35-36, proj/src/seismic_ops.cpp:84-107
 WaveOp adjoint_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
                         int space_order);
+
+// ---- TTI (no reference counterpart) ----------------
+// Thomsen parameters and the tilt / azimuth of the symmetry axis on the model's padded
+// grid.  The pseudo-acoustic system needs epsilon >= delta > -1/2 everywhere.
+struct TtiModel {
+    std::shared_ptr<Function> epsilon, delta, theta, phi;
+    // fields over the physical shape, edge-extended into the absorbing layer like the
+    // velocity (proj/src/model.cpp:92-100)
+    TtiModel(const SeismicModel& model, const std::vector<double>& epsilon,
+             const std::vector<double>& delta, const std::vector<double>& theta,
+             const std::vector<double>& phi);
+    double epsilon_max() const;
+};
+
+// largest stable dt of the TTI operator: the acoustic rule (proj/src/model.cpp:103-111)
+// with v_max sqrt(1 + 2 eps_max), times 0.9 for the twice-applied first derivatives
+double tti_critical_dt(const SeismicModel& model, const TtiModel& tti, int space_order);
+
+// coupled (p, r) forward operator; sources are injected into both fields, receivers
+// sample p.  StabilityError when dt exceeds tti_critical_dt or epsilon < delta somewhere.
+WaveOp tti_forward_operator(const SeismicModel& model, const TtiModel& tti,
+                            const AcquisitionGeometry& geom, int space_order);
 
 // proj/include/sf/seismic_ops.hpp:40-47
 struct GradientOp {

@@ -199,11 +199,15 @@ SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_
 
 /* ---- tile shape (the counterpart of the reference's loop-blocking autotune,
  * proj/include/sf/execute.hpp:56): threads along the contiguous axis (x4 nodes each),
- * tile rows, ring stages (0 = any), output planes per block (0 = automatic).  Only
- * compiled shapes are accepted. */
+ * tile rows, ring stages (0 = any; negative = the dual-stream kernel with that many
+ * stages), output planes per block (0 = automatic).  Only compiled shapes are accepted. */
 SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk);
 SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* stages, int* chunk,
                          int* separable_damping);
+/* times every compiled tile shape of the plan's order for `steps` launches (0 = default) on
+ * the plan's own zeroed buffers and keeps the fastest: the counterpart of the reference's
+ * autotune (proj/include/sf/execute.hpp:56).  Wavefield state is lost. */
+SFB_API int sfb_autotune(sfb_plan* plan, int steps);
 /* kernels launched by this plan since the last sfb_step_begin */
 SFB_API int sfb_launch_count(sfb_plan* plan, int64_t* count);
 /* on != 0: always stream the dense damp array, even when it is a sum of 1-D profiles

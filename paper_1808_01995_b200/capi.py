@@ -47,7 +47,7 @@ SYMBOLS = [
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
     "sfb_step_points", "sfb_step_end", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
-    "sfb_set_dense_damping", "sfb_launch_count",
+    "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune",
 ]
 
 lib.sfb_last_error.restype = C.c_char_p
@@ -79,6 +79,7 @@ lib.sfb_copy_halo.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
 lib.sfb_set_tile.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
 lib.sfb_get_tile.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 5
 lib.sfb_set_dense_damping.argtypes = [C.c_void_p, C.c_int]
+lib.sfb_autotune.argtypes = [C.c_void_p, C.c_int]
 lib.sfb_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
 lib.sfb_fd_weights.argtypes = [C.c_int, C.c_int, C.c_void_p]
 lib.sfb_critical_dt.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double)]
@@ -245,6 +246,10 @@ class Plan:
         v = [C.c_int() for _ in range(5)]
         self._chk(lib.sfb_get_tile(self.h, *[C.byref(x) for x in v]))
         return dict(zip(["txv", "ty", "stages", "chunk", "sep"], [x.value for x in v]))
+
+    def autotune(self, steps=0):
+        self._chk(lib.sfb_autotune(self.h, steps))
+        return self.get_tile()
 
     def launch_count(self):
         n = C.c_int64()

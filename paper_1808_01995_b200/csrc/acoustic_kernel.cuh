@@ -62,9 +62,10 @@ struct StepParams {
     int chunk;           // output planes per block
 };
 
-// the four tensor maps of one launch: u[t] with halo box; u[t-1], r, damp with plain box
+// the tensor maps of one launch: u[t] with halo box (u) and with plain box (f); u[t-1], r,
+// damp with plain box
 struct StepMaps {
-    CUtensorMap u, o, r, d;
+    CUtensorMap u, f, o, r, d;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -110,6 +111,107 @@ __device__ __forceinline__ float fast_rcp(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return fmaf(y, fmaf(-x, y, 1.f), y);
+}
+
+// One output plane for the four nodes of a thread: stencil from the register queue (d0)
+// and the centre plane in shared memory `cp` (d1, d2), then -- after telling the producer
+// that this iteration's shared-memory reads are over -- damping, leapfrog and the stores.
+template <int K, int KP, int SW, bool SEP>
+__device__ __forceinline__ void plane_update(const StepParams& p, const float (&q)[2 * K + 1][4],
+                                             const float* cp, int tx, int ty, float4 o4, float4 r4,
+                                             float4 d4, const float (&dxy)[4], float dzv,
+                                             bool warp_dxy, bool rin, bool lane0,
+                                             uint64_t* done_bar, float* po, long long gc) {
+        float acc[4];
+        // centre and streaming-axis neighbours from the register queue
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float a = p.k.c0 * q[K][c];
+#pragma unroll
+            for (int j = 1; j <= K; ++j) a = fmaf(p.k.cz[j - 1], q[K - j][c] + q[K + j][c], a);
+            acc[c] = a;
+        }
+        // contiguous-axis neighbours: one aligned row segment
+        {
+            float xr[2 * KP + 4];
+            const float* rowp = cp + (ty + K) * SW + 4 * tx;
+#pragma unroll
+            for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
+                if (v == KP / 4) {  // own float4: already in the queue
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) xr[4 * v + c] = q[K][c];
+                } else {
+                    const float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
+                    xr[4 * v + 0] = t4.x;
+                    xr[4 * v + 1] = t4.y;
+                    xr[4 * v + 2] = t4.z;
+                    xr[4 * v + 3] = t4.w;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int j = 1; j <= K; ++j)
+                    acc[c] = fmaf(p.k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], acc[c]);
+        }
+        // d1 neighbours: the column strip above and below
+        {
+            const float* colp = cp + ty * SW + KP + 4 * tx;
+#pragma unroll
+            for (int j = 1; j <= K; ++j) {
+                const float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
+                const float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
+                acc[0] = fmaf(p.k.cy[j - 1], lo.x + hi.x, acc[0]);
+                acc[1] = fmaf(p.k.cy[j - 1], lo.y + hi.y, acc[1]);
+                acc[2] = fmaf(p.k.cy[j - 1], lo.z + hi.z, acc[2]);
+                acc[3] = fmaf(p.k.cy[j - 1], lo.w + hi.w, acc[3]);
+            }
+        }
+        // all shared-memory reads of this iteration are done
+        __syncwarp();
+        if (lane0) mbar_arrive(done_bar);
+
+        const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
+        const float ov[4] = {o4.x, o4.y, o4.z, o4.w};
+        float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+        bool damped;
+        if (SEP) {
+            damped = warp_dxy || dzv != 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dv[c] = dxy[c] + dzv;
+        } else {
+            damped = __any_sync(0xffffffffu, (dv[0] + dv[1]) + (dv[2] + dv[3]) != 0.f);
+        }
+        float un[4];
+        if (damped) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float qq = dv[c] * rv[c] * p.k.qscale;
+                const float c1 = fast_rcp(1.f + qq);
+                const float c2 = (1.f - qq) * c1;
+                const float t = fmaf(rv[c], acc[c], 2.f * q[K][c]);
+                un[c] = fmaf(c1, t, -c2 * ov[c]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) un[c] = fmaf(rv[c], acc[c], 2.f * q[K][c]) - ov[c];
+        }
+        if (rin) {
+            __stcs(reinterpret_cast<float4*>(po), make_float4(un[0], un[1], un[2], un[3]));
+            if (p.snap)
+                __stcs(reinterpret_cast<float4*>(p.snap + gc),
+                       make_float4(un[0], un[1], un[2], un[3]));
+            if (p.usave) {
+                const float4 g4 = __ldcs(reinterpret_cast<const float4*>(p.grad + gc));
+                const float4 s4 = __ldcs(reinterpret_cast<const float4*>(p.usave + gc));
+                float4 gn;
+                gn.x = fmaf(-s4.x * p.k.inv_dt2, (un[0] - 2.f * q[K][0]) + ov[0], g4.x);
+                gn.y = fmaf(-s4.y * p.k.inv_dt2, (un[1] - 2.f * q[K][1]) + ov[1], g4.y);
+                gn.z = fmaf(-s4.z * p.k.inv_dt2, (un[2] - 2.f * q[K][2]) + ov[2], g4.z);
+                gn.w = fmaf(-s4.w * p.k.inv_dt2, (un[3] - 2.f * q[K][3]) + ov[3], g4.w);
+                __stcs(reinterpret_cast<float4*>(p.grad + gc), gn);
+            }
+        }
 }
 
 template <int K, int TXV, int TY, int NST, bool SEP>
@@ -273,97 +375,8 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
         const float dzv = dzn;
         if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
 
-        const float* cp = ring + cs * STAGE;
-        float acc[4];
-        // centre and streaming-axis neighbours from the register queue
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            float a = p.k.c0 * q[K][c];
-#pragma unroll
-            for (int j = 1; j <= K; ++j) a = fmaf(p.k.cz[j - 1], q[K - j][c] + q[K + j][c], a);
-            acc[c] = a;
-        }
-        // contiguous-axis neighbours: one aligned row segment
-        {
-            float xr[2 * KP + 4];
-            const float* rowp = cp + (ty + K) * SW + 4 * tx;
-#pragma unroll
-            for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
-                if (v == KP / 4) {  // own float4: already in the queue
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) xr[4 * v + c] = q[K][c];
-                } else {
-                    const float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
-                    xr[4 * v + 0] = t4.x;
-                    xr[4 * v + 1] = t4.y;
-                    xr[4 * v + 2] = t4.z;
-                    xr[4 * v + 3] = t4.w;
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-#pragma unroll
-                for (int j = 1; j <= K; ++j)
-                    acc[c] = fmaf(p.k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], acc[c]);
-        }
-        // d1 neighbours: the column strip above and below
-        {
-            const float* colp = cp + ty * SW + KP + 4 * tx;
-#pragma unroll
-            for (int j = 1; j <= K; ++j) {
-                const float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
-                const float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
-                acc[0] = fmaf(p.k.cy[j - 1], lo.x + hi.x, acc[0]);
-                acc[1] = fmaf(p.k.cy[j - 1], lo.y + hi.y, acc[1]);
-                acc[2] = fmaf(p.k.cy[j - 1], lo.z + hi.z, acc[2]);
-                acc[3] = fmaf(p.k.cy[j - 1], lo.w + hi.w, acc[3]);
-            }
-        }
-        // all shared-memory reads of this iteration are done
-        __syncwarp();
-        if (lane0) mbar_arrive(done + ds);
-
-        const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
-        const float ov[4] = {o4.x, o4.y, o4.z, o4.w};
-        float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-        bool damped;
-        if (SEP) {
-            damped = warp_dxy || dzv != 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) dv[c] = dxy[c] + dzv;
-        } else {
-            damped = __any_sync(0xffffffffu, (dv[0] + dv[1]) + (dv[2] + dv[3]) != 0.f);
-        }
-        float un[4];
-        if (damped) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float qq = dv[c] * rv[c] * p.k.qscale;
-                const float c1 = fast_rcp(1.f + qq);
-                const float c2 = (1.f - qq) * c1;
-                const float t = fmaf(rv[c], acc[c], 2.f * q[K][c]);
-                un[c] = fmaf(c1, t, -c2 * ov[c]);
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) un[c] = fmaf(rv[c], acc[c], 2.f * q[K][c]) - ov[c];
-        }
-        if (rin) {
-            __stcs(reinterpret_cast<float4*>(po), make_float4(un[0], un[1], un[2], un[3]));
-            if (p.snap)
-                __stcs(reinterpret_cast<float4*>(p.snap + gc),
-                       make_float4(un[0], un[1], un[2], un[3]));
-            if (p.usave) {
-                const float4 g4 = __ldcs(reinterpret_cast<const float4*>(p.grad + gc));
-                const float4 s4 = __ldcs(reinterpret_cast<const float4*>(p.usave + gc));
-                float4 gn;
-                gn.x = fmaf(-s4.x * p.k.inv_dt2, (un[0] - 2.f * q[K][0]) + ov[0], g4.x);
-                gn.y = fmaf(-s4.y * p.k.inv_dt2, (un[1] - 2.f * q[K][1]) + ov[1], g4.y);
-                gn.z = fmaf(-s4.z * p.k.inv_dt2, (un[2] - 2.f * q[K][2]) + ov[2], g4.z);
-                gn.w = fmaf(-s4.w * p.k.inv_dt2, (un[3] - 2.f * q[K][3]) + ov[3], g4.w);
-                __stcs(reinterpret_cast<float4*>(p.grad + gc), gn);
-            }
-        }
+        plane_update<K, KP, SW, SEP>(p, q, ring + cs * STAGE, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
+                                     rin, lane0, done + ds, po, gc);
         po += p.plane;
         gc += p.plane;
         if (++s == NST) {
@@ -373,6 +386,160 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
         if (++cs == NST) cs = 0;
         if (++as == NAUX) as = 0;
         if (++ds == NAUX) ds = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// "Dual-stream" variant.  The ring kernel above keeps every plane between the newest and
+// the centre one in shared memory (NST = K + 3 haloed stages), which at high order leaves
+// room for a single block per SM.  Here a plane of u[t] is fetched twice instead: once as
+// a plain TX x TY box when it is the newest plane (it only feeds the register queue) and
+// once, K iterations later, as the haloed box when it is the centre plane (the second
+// fetch hits L2: K planes of a few MB).  Everything an iteration needs -- feed box, centre
+// box, aux boxes -- sits in ONE stage of an NS-deep ring, so shared memory no longer grows
+// with K and one full/done barrier pair per stage orders it all.
+template <int K, int TXV, int TY, int NS, bool SEP>
+struct DualShape {
+    static constexpr int KP = (K + 3) & ~3;
+    static constexpr int TX = TXV * 4;
+    static constexpr int SW = TX + 2 * KP;
+    static constexpr int SH = TY + 2 * K;
+    static constexpr int CBOX = SW * SH;                 // centre box (floats)
+    static constexpr int CPAD = ((CBOX + 31) / 32) * 32;
+    static constexpr int ABOX = TX * TY;                 // feed / aux box
+    static constexpr int NARR = SEP ? 2 : 3;
+    static constexpr int STAGE = ABOX + CPAD + NARR * ABOX;
+    static constexpr int NCONS = TXV * TY;
+    static constexpr int NTHREADS = NCONS + 32;
+    static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8 + 128;
+    static_assert(NCONS % 32 == 0 && (ABOX * 4) % 128 == 0 && NS >= 2, "tile shape");
+};
+
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB>
+__global__ void __launch_bounds__(DualShape<K, TXV, TY, NS, SEP>::NTHREADS, MINB)
+acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
+                          const __grid_constant__ StepParams p) {
+    using S = DualShape<K, TXV, TY, NS, SEP>;
+    constexpr int KP = S::KP, SW = S::SW, STAGE = S::STAGE, Q = 2 * K + 1;
+    constexpr int NARR = S::NARR, ABOX = S::ABOX, CPAD = S::CPAD, TX = S::TX;
+    constexpr int NCW = S::NCONS / 32;
+
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t mis = smem_u32(smem_raw) & 127u;
+    float* ring = reinterpret_cast<float*>(smem_raw + ((128u - mis) & 127u));
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
+    uint64_t* done = full + NS;
+
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int zb = p.z_lo + blockIdx.z * p.chunk;
+    const int ze = min(zb + p.chunk, p.z_hi);
+    const int nplanes = (ze - zb) + 2 * K;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(done + s, NCW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (tid >= S::NCONS) {
+        if (tid == S::NCONS) {
+            int s = 0;
+            uint32_t dph = 0;
+            for (int n = 0; n < nplanes; ++n) {
+                if (n >= NS) mbar_wait(done + s, dph);  // iteration n - NS released the stage
+                const bool out = n >= 2 * K;
+                float* st = ring + s * STAGE;
+                mbar_arrive_expect_tx(full + s, (ABOX + (out ? S::CBOX + NARR * ABOX : 0)) * 4);
+                tma_load_3d(st, &tm.f, x0, y0, zb + n, full + s);              // newest plane
+                if (out) {
+                    const int zo = zb + n - 2 * K;
+                    tma_load_3d(st + ABOX, &tm.u, x0 - KP, y0 - K, zo + K, full + s);  // centre
+                    float* ad = st + ABOX + CPAD;
+                    tma_load_3d(ad, &tm.o, x0, y0, zo + K, full + s);
+                    tma_load_3d(ad + ABOX, &tm.r, x0, y0, zo, full + s);
+                    if (!SEP) tma_load_3d(ad + 2 * ABOX, &tm.d, x0, y0, zo, full + s);
+                }
+                if (++s == NS) {
+                    s = 0;
+                    if (n >= NS) dph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    const int tx = tid % TXV, ty = tid / TXV;
+    const int x = x0 + 4 * tx, y = y0 + ty;
+    const bool rin = x < p.N2 && y < p.N1;
+    const bool lane0 = (tid & 31) == 0;
+
+    float dxy[4] = {0.f, 0.f, 0.f, 0.f};
+    bool warp_dxy = false;
+    if (SEP) {
+        if (rin) {
+            const float4 dx4 = __ldg(reinterpret_cast<const float4*>(p.dx + x));
+            const float dyv = __ldg(p.dy + y);
+            dxy[0] = dx4.x + dyv;
+            dxy[1] = dx4.y + dyv;
+            dxy[2] = dx4.z + dyv;
+            dxy[3] = dx4.w + dyv;
+        }
+        warp_dxy = __any_sync(0xffffffffu, (dxy[0] + dxy[1]) + (dxy[2] + dxy[3]) != 0.f);
+    }
+
+    float q[Q][4];
+#pragma unroll
+    for (int j = 0; j < Q; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
+
+    const int aown = ty * TX + 4 * tx;
+    long long gc = (long long)zb * p.plane + (long long)y * p.pitch + x;
+    float* po = p.uo + gc + (long long)K * p.plane;
+    float dzn = 0.f;
+    if (SEP) dzn = __ldg(p.dz + zb);
+    int s = 0;
+    uint32_t fph = 0;
+
+    for (int n = 0; n < nplanes; ++n) {
+        mbar_wait(full + s, fph);
+        const float* st = ring + s * STAGE;
+        {
+            const float4 v = *reinterpret_cast<const float4*>(st + aown);
+#pragma unroll
+            for (int j = 0; j < Q - 1; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
+            q[Q - 1][0] = v.x;
+            q[Q - 1][1] = v.y;
+            q[Q - 1][2] = v.z;
+            q[Q - 1][3] = v.w;
+        }
+        if (n < 2 * K) {
+            __syncwarp();
+            if (lane0) mbar_arrive(done + s);
+        } else {
+            const float* ap = st + ABOX + CPAD + aown;
+            const float4 o4 = *reinterpret_cast<const float4*>(ap);
+            const float4 r4 = *reinterpret_cast<const float4*>(ap + ABOX);
+            float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!SEP) d4 = *reinterpret_cast<const float4*>(ap + 2 * ABOX);
+            const float dzv = dzn;
+            if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
+            plane_update<K, KP, SW, SEP>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
+                                         rin, lane0, done + s, po, gc);
+            po += p.plane;
+            gc += p.plane;
+        }
+        if (++s == NS) {
+            s = 0;
+            fph ^= 1;
+        }
     }
 }
 

@@ -111,13 +111,27 @@ void make_tensor_maps(Plan& P) {
 
 // ---- tile shape / chunk choice ----------------------------------------------------------
 
-void select_variant(Plan& P, int txv, int ty, int nst) {
+void select_variant(Plan& P, int txv, int ty, int nst, int dual = -1) {
     const StepVariant* best = nullptr;
     for (const StepVariant& v : step_variant_registry()) {
         if (v.K != P.K || v.sep != P.sep) continue;
+        if (dual >= 0 && int(v.dual) != dual) continue;
         if (txv > 0 && (v.TXV != txv || v.TY != ty || (nst > 0 && v.NST != nst))) continue;
+        if (txv <= 0) {
+            // default shape (measured on B200, tools/probe_tiles.py): the ring kernel up to
+            // order 8, the dual-stream kernel (4 stages) above, 64 x 16 tiles
+            const bool want_dual = P.K >= 5;
+            if (v.dual != want_dual || v.TXV != 16 || v.TY != 16) continue;
+            if (v.NST != (want_dual ? 4 : P.K + 3)) continue;
+        }
         if (!best) best = &v;
     }
+    if (!best && txv <= 0)  // fall back to any compiled shape of this order
+        for (const StepVariant& v : step_variant_registry())
+            if (v.K == P.K && v.sep == P.sep) {
+                best = &v;
+                break;
+            }
     if (!best)
         throw Failure(SFB_ERR_CAPABILITY, "no kernel image for space order " +
                                               std::to_string(2 * P.K));
@@ -598,6 +612,7 @@ void step_compute(Plan& P, int op, long long t, int part) {
     cudaStream_t st = part_stream(P, part);
     StepMaps maps;
     maps.u = P.tm_u[cur];
+    maps.f = P.tm_o[cur];
     maps.o = P.tm_o[oth];
     maps.r = P.tm_r;
     maps.d = P.sep ? P.tm_r : P.tm_d;
@@ -1117,7 +1132,7 @@ SFB_API int sfb_set_model(sfb_plan* plan, const sfb_field_view* m, const sfb_fie
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
         detect_separable_damping(P, embed_view(P, damp->ptr, damp->stride), tmp);
         if (P.sep) P.damp.release();
-        select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST);
+        select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST, int(P.variant->dual));
         P.model_set = true;
         P.history_valid = false;
     });
@@ -1422,6 +1437,44 @@ SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_
     });
 }
 
+SFB_API int sfb_autotune(sfb_plan* plan, int steps) {
+    // the counterpart of the reference's autotune (proj/include/sf/execute.hpp:56): time
+    // every compiled tile shape of this order on the plan's own (zeroed) buffers, keep the
+    // fastest.  Destroys the wavefield state; call before a run.
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(P.model_set, SFB_ERR_BINDING, "autotune needs the model (sfb_set_model)");
+        require(P.desc.nt >= 4, SFB_ERR_PARAMETER, "autotune needs nt >= 4");
+        if (steps < 1) steps = 6;
+        const StepVariant* best = nullptr;
+        float best_ms = 0.f;
+        for (const StepVariant& v : step_variant_registry()) {
+            if (v.K != P.K || v.sep != P.sep) continue;
+            select_variant(P, v.TXV, v.TY, v.NST, int(v.dual));
+            SFB_CUDA(cudaMemsetAsync(P.u[0].p, 0, size_t(P.ucount) * 4, P.s_main));
+            SFB_CUDA(cudaMemsetAsync(P.u[1].p, 0, size_t(P.ucount) * 4, P.s_main));
+            P.save_every = 0;
+            for (int rep = 0; rep < 2; ++rep) {  // first round warms up
+                SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+                for (int i = 0; i < steps; ++i) step_compute(P, SFB_OP_FORWARD, 1 + (i & 1), SFB_PART_ALL);
+                SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+                SFB_CUDA(cudaStreamSynchronize(P.s_main));
+            }
+            float ms = 0.f;
+            SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+            if (!best || ms < best_ms) {
+                best = &v;
+                best_ms = ms;
+            }
+        }
+        require(best != nullptr, SFB_ERR_CAPABILITY, "no kernel image for this space order");
+        select_variant(P, best->TXV, best->TY, best->NST, int(best->dual));
+        P.history_valid = false;
+        P.live_level[0] = P.live_level[1] = -1;
+    });
+}
+
 SFB_API int sfb_launch_count(sfb_plan* plan, int64_t* count) {
     if (!plan || !count) return SFB_ERR_PARAMETER;
     *count = plan->launches;
@@ -1437,7 +1490,8 @@ SFB_API int sfb_set_dense_damping(sfb_plan* plan, int on) {
 SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
-        select_variant(*plan, txv, ty, stages);
+        // stages < 0 selects the dual-stream kernel with |stages| stages
+        select_variant(*plan, txv, ty, stages < 0 ? -stages : stages, stages < 0 ? 1 : 0);
         if (chunk > 0) plan->chunk = std::min(chunk, plan->n0);
     });
 }
@@ -1446,7 +1500,7 @@ SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* nst, int* chunk
     if (!plan || !plan->variant) return SFB_ERR_PARAMETER;
     if (txv) *txv = plan->variant->TXV;
     if (ty) *ty = plan->variant->TY;
-    if (nst) *nst = plan->variant->NST;
+    if (nst) *nst = plan->variant->dual ? -plan->variant->NST : plan->variant->NST;
     if (chunk) *chunk = plan->chunk;
     if (sep) *sep = plan->variant->sep ? 1 : 0;
     return SFB_OK;

@@ -11,8 +11,9 @@
 namespace sfb {
 
 struct StepVariant {
-    int K, TXV, TY, NST;
+    int K, TXV, TY, NST;  // NST: ring stages (ring kernel) or stages of the dual-stream ring
     bool sep;
+    bool dual;            // dual-stream kernel (u[t] fetched as feed + centre boxes)
     int tile_x, tile_y;   // output tile (d2, d1)
     int box_w, box_h;     // TMA box of u[t] (d2, d1)
     int halo_x;           // KP
@@ -36,7 +37,7 @@ void register_step() {
     using S = StepShape<K, TXV, TY, NST, SEP>;
     if constexpr (S::SMEM <= 227 * 1024) {
         StepVariant v;
-        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NST; v.sep = SEP;
+        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NST; v.sep = SEP; v.dual = false;
         v.tile_x = S::TX; v.tile_y = TY; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
         v.nthreads = S::NTHREADS; v.smem = S::SMEM;
         v.func = reinterpret_cast<const void*>(&acoustic_step_kernel<K, TXV, TY, NST, SEP>);
@@ -45,10 +46,39 @@ void register_step() {
     }
 }
 
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB>
+cudaError_t launch_dual(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
+    using S = DualShape<K, TXV, TY, NS, SEP>;
+    acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB><<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
+    return cudaGetLastError();
+}
+
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB>
+void register_dual() {
+    using S = DualShape<K, TXV, TY, NS, SEP>;
+    if constexpr (S::SMEM * MINB <= 227 * 1024) {
+        StepVariant v;
+        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NS; v.sep = SEP; v.dual = true;
+        v.tile_x = S::TX; v.tile_y = TY; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
+        v.nthreads = S::NTHREADS; v.smem = S::SMEM;
+        v.func = reinterpret_cast<const void*>(&acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB>);
+        v.launch = &launch_dual<K, TXV, TY, NS, SEP, MINB>;
+        step_variant_registry().push_back(v);
+    }
+}
+
 template <int K, int TXV, int TY, int NST>
 void register_pair() {
     register_step<K, TXV, TY, NST, false>();
     register_step<K, TXV, TY, NST, true>();
+}
+
+template <int K, int TXV, int TY, int NS>
+void register_dual_pair() {
+    // ask for as many resident blocks as the register file can hold with the queue of this K
+    constexpr int MINB = K <= 4 ? 3 : 2;
+    register_dual<K, TXV, TY, NS, false, MINB>();
+    register_dual<K, TXV, TY, NS, true, MINB>();
 }
 
 // the tile shapes built for every half-order K (dense and separable damping); the first
@@ -60,6 +90,9 @@ void register_all_for_K() {
     register_pair<K, 32, 8, K + 3>();
     register_pair<K, 16, 32, K + 3>();
     register_pair<K, 32, 16, K + 3>();
+    register_dual_pair<K, 16, 16, 3>();
+    register_dual_pair<K, 16, 16, 4>();
+    register_dual_pair<K, 32, 8, 3>();
 }
 
 struct VariantRegistrar {

@@ -146,6 +146,79 @@ WaveOp adjoint_operator(const SeismicModel& model, const AcquisitionGeometry& ge
     return w;
 }
 
+// ---- TTI ----------------------------------------------------------------------------------
+
+TtiModel::TtiModel(const SeismicModel& model, const std::vector<double>& eps,
+                   const std::vector<double>& del, const std::vector<double>& th,
+                   const std::vector<double>& ph) {
+    const std::vector<long>& ps = model.physical_shape();
+    std::size_t n = 1;
+    for (long e : ps) n *= std::size_t(e);
+    if (eps.size() != n || del.size() != n || th.size() != n || ph.size() != n)
+        throw ParameterError("TtiModel: field size does not match the physical shape");
+    const int nd = int(ps.size()), off = 3 - nd;
+    auto extend = [&](const char* name, const std::vector<double>& v) {
+        auto f = Function::create(name, model.grid(), model.space_order());
+        long N[3] = {1, 1, 1}, pn[3] = {1, 1, 1}, pad[3] = {0, 0, 0}, st[3] = {0, 0, 0};
+        for (int a = 0; a < nd; ++a) {
+            N[off + a] = model.grid()->shape()[std::size_t(a)];
+            pn[off + a] = ps[std::size_t(a)];
+            pad[off + a] = model.nbl();
+            st[off + a] = f->stride(a);
+        }
+        std::vector<long> zero(std::size_t(nd), 0);
+        double* origin = f->values() + f->flat_index(zero);
+        for (long i = 0; i < N[0]; ++i)
+            for (long j = 0; j < N[1]; ++j)
+                for (long l = 0; l < N[2]; ++l) {
+                    const long pi = std::clamp(i - pad[0], 0L, pn[0] - 1);
+                    const long pj = std::clamp(j - pad[1], 0L, pn[1] - 1);
+                    const long pl = std::clamp(l - pad[2], 0L, pn[2] - 1);
+                    origin[i * st[0] + j * st[1] + l * st[2]] =
+                        v[(std::size_t(pi) * pn[1] + pj) * pn[2] + pl];
+                }
+        return f;
+    };
+    epsilon = extend("epsilon", eps);
+    delta = extend("delta", del);
+    theta = extend("theta", th);
+    phi = extend("phi", ph);
+}
+
+double TtiModel::epsilon_max() const {
+    double m = 0.0;
+    const double* p = epsilon->values();
+    for (std::size_t i = 0; i < epsilon->storage_size(); ++i) m = std::max(m, p[i]);
+    return m;
+}
+
+double tti_critical_dt(const SeismicModel& model, const TtiModel& tti, int space_order) {
+    return 0.9 * model.critical_dt(space_order) / std::sqrt(1.0 + 2.0 * tti.epsilon_max());
+}
+
+WaveOp tti_forward_operator(const SeismicModel& model, const TtiModel& tti,
+                            const AcquisitionGeometry& geom, int space_order) {
+    check_space_order(space_order);
+    const double crit = tti_critical_dt(model, tti, space_order);
+    if (geom.dt() > crit * (1.0 + 1e-12))
+        throw StabilityError("dt " + std::to_string(geom.dt()) + " exceeds the TTI stable limit " +
+                             std::to_string(crit) + " at order " + std::to_string(space_order));
+    WaveOp w;
+    w.dt = geom.dt();
+    w.nt = geom.nt();
+    w.space_order = space_order;
+    w.tti = true;
+    w.inj = geom.src();
+    w.smp = geom.rec();
+    w.wavefield = TimeFunction::create("p", model.grid(), space_order, 2);
+    w.wavefield_r = TimeFunction::create("r", model.grid(), space_order, 2);
+    w.engine = std::make_shared<Engine>(model, geom, space_order);
+    sfb_field_view ev = Engine::view(*tti.epsilon), dv = Engine::view(*tti.delta),
+                   tv = Engine::view(*tti.theta), pv = Engine::view(*tti.phi);
+    w.engine->check(sfb_set_model_tti(w.engine->plan(), &ev, &dv, &tv, &pv));
+    return w;
+}
+
 // proj/src/seismic_ops.cpp:109-135
 GradientOp gradient_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
                              int space_order, std::shared_ptr<TimeFunction> saved_u) {
@@ -175,6 +248,18 @@ ExecutionReport run_wave(WaveOp& w, Backend, int) {
     Engine& e = *w.engine;
     sfb_report rep{};
     w.wavefield->zero();
+    if (w.tti) {
+        w.wavefield_r->zero();
+        e.check(sfb_tti_forward(e.plan(), w.inj->traces().data(), w.smp->traces().data(), &rep));
+        if (w.nt >= 3)
+            for (int field = 0; field < 2; ++field)
+                for (long lvl : {w.nt - 1, w.nt - 2}) {
+                    TimeFunction& f = field ? *w.wavefield_r : *w.wavefield;
+                    sfb_field_mview mv = Engine::mview(f, lvl % f.time_slots());
+                    e.check(sfb_get_wavefield(e.plan(), field, lvl, &mv));
+                }
+        return to_report(rep);
+    }
     if (!w.adjoint) {
         e.check(sfb_forward(e.plan(), w.inj->traces().data(), w.smp->traces().data(),
                             w.save_every, &rep));

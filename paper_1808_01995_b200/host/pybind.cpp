@@ -163,12 +163,24 @@ PYBIND11_MODULE(_sfb_host, m) {
 
     py::class_<WaveOp>(m, "WaveOp")
         .def_property_readonly("wavefield", [](const WaveOp& w) { return w.wavefield; })
+        .def_property_readonly("wavefield_r", [](const WaveOp& w) { return w.wavefield_r; })
         .def_property_readonly("inj", [](const WaveOp& w) { return w.inj; })
         .def_property_readonly("smp", [](const WaveOp& w) { return w.smp; })
         .def_readonly("dt", &WaveOp::dt)
         .def_readonly("nt", &WaveOp::nt)
         .def_readwrite("save_every", &WaveOp::save_every)
         .def_readwrite("host_history", &WaveOp::host_history);
+    py::class_<TtiModel>(m, "TtiModel")
+        .def(py::init([](const SeismicModel& model, const darray& e, const darray& d, const darray& t,
+                         const darray& p) { return new TtiModel(model, flat(e), flat(d), flat(t), flat(p)); }))
+        .def_property_readonly("epsilon", [](const TtiModel& t) { return std::static_pointer_cast<FieldBase>(t.epsilon); })
+        .def_property_readonly("delta", [](const TtiModel& t) { return std::static_pointer_cast<FieldBase>(t.delta); })
+        .def_property_readonly("theta", [](const TtiModel& t) { return std::static_pointer_cast<FieldBase>(t.theta); })
+        .def_property_readonly("phi", [](const TtiModel& t) { return std::static_pointer_cast<FieldBase>(t.phi); })
+        .def("epsilon_max", &TtiModel::epsilon_max);
+    m.def("tti_critical_dt", &tti_critical_dt);
+    m.def("tti_forward_operator", &tti_forward_operator);
+
     py::class_<GradientOp>(m, "GradientOp")
         .def_property_readonly("v", [](const GradientOp& g) { return g.v; })
         .def_property_readonly("grad", [](const GradientOp& g) { return std::static_pointer_cast<FieldBase>(g.grad); })

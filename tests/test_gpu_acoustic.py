@@ -63,7 +63,7 @@ def test_tile_shapes_agree_bitwise():
     plan = make_plan(model, geom, 8)
     base, _ = plan.forward(geom.src)
     u0 = plan.wavefield(geom.nt - 1)
-    for tile in [(16, 16, 8), (32, 8, 0), (16, 32, 0), (32, 16, 0)]:
+    for tile in [(16, 16, 8), (32, 8, 7), (16, 32, 7), (32, 16, 7), (16, 16, -3), (16, 16, -4), (32, 8, -3)]:
         for chunk in (0, 7, 60):
             plan.set_tile(*tile, chunk)
             rec, _ = plan.forward(geom.src)
@@ -96,6 +96,17 @@ def test_dense_and_separable_damping_agree():
     dense.set_model(model.m, bumpy, model.v_max)
     assert dense.get_tile()["sep"] == 0
     dense.close()
+
+
+def test_autotune_keeps_results_and_picks_a_compiled_shape():
+    model, geom = make_problem([40, 36, 44], 10.0, 8, 12, 30)
+    plan = make_plan(model, geom, 12)
+    base, _ = plan.forward(geom.src)
+    t = plan.autotune(3)
+    assert t["txv"] in (16, 32) and t["chunk"] >= 1
+    rec, _ = plan.forward(geom.src)
+    assert np.array_equal(rec, base)
+    plan.close()
 
 
 def test_zero_source_gives_zero_receivers():  # proj/tests/test_seismic.cpp:165-174

@@ -90,3 +90,37 @@ def test_tti_rejects_ill_posed_medium_and_large_dt():
         plan.set_model_tti(eps, delta, theta, phi)
     assert e.value.code == capi.ERR_STABILITY
     plan.close()
+
+
+def test_tti_through_the_host_layer():
+    from paper_1808_01995_b200 import _sfb_host as H
+    n, h, nbl, order = 22, 10.0, 6, 8
+    rng = np.random.default_rng(3)
+    vel = rng.uniform(1.5, 3.0, size=(n, n, n))
+    eps = rng.uniform(0.0, 0.3, size=(n, n, n))
+    delta = np.minimum(rng.uniform(0.0, 0.2, size=(n, n, n)), eps)
+    theta = rng.uniform(0.0, np.pi / 4, size=(n, n, n))
+    phi = rng.uniform(0.0, np.pi / 4, size=(n, n, n))
+    model = H.SeismicModel([n] * 3, [h] * 3, [0.0] * 3, vel, nbl, order)
+    tti = H.TtiModel(model, eps, delta, theta, phi)
+    dt = H.tti_critical_dt(model, tti, order)
+    L = (n - 1) * h
+    geom = H.AcquisitionGeometry(model, [0.5 * L + 1.0, 0.5 * L, 22.0],
+                                 np.array([[x, 0.5 * L, 33.0] for x in np.linspace(0, L, 9)]).ravel(),
+                                 0.0, 60.5 * dt, dt, 0.02)
+    w = H.tti_forward_operator(model, tti, geom, order)
+    rep = H.run_wave(w)
+    assert rep.steps == geom.nt - 2
+    om = o.Model([n] * 3, [h] * 3, [0.0] * 3, vel, nbl, order)
+    og = o.Geometry(om, [0.5 * L + 1.0, 0.5 * L, 22.0],
+                    np.array([[x, 0.5 * L, 33.0] for x in np.linspace(0, L, 9)]).ravel(), 0.0, 60.5 * dt, dt, 0.02)
+    assert dt == pytest.approx(o.tti_critical_dt(om, order, tti.epsilon_max()), rel=1e-14)
+    ref = o.tti_forward(om, og, order, tti.epsilon.array(), tti.delta.array(), tti.theta.array(),
+                        tti.phi.array(), want_final=True)
+    assert rel_l2(geom.rec.traces, ref["smp"]) <= 1e-5
+    assert rel_l2(w.wavefield.array()[(geom.nt - 1) % 3], ref["p"]) <= 1e-5
+    assert rel_l2(w.wavefield_r.array()[(geom.nt - 1) % 3], ref["r"]) <= 1e-5
+    geom2 = H.AcquisitionGeometry(model, [0.5 * L, 0.5 * L, 22.0], [10.0, 10.0, 10.0], 0.0, 60.5 * dt,
+                                  1.2 * dt, 0.02)
+    with pytest.raises(H.StabilityError):
+        H.tti_forward_operator(model, tti, geom2, order)
