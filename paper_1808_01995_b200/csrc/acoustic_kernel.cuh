@@ -113,22 +113,17 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return fmaf(y, fmaf(-x, y, 1.f), y);
 }
 
-// One output plane for the four nodes of a thread: stencil from the register queue (d0)
-// and the centre plane in shared memory `cp` (d1, d2), then -- after telling the producer
-// that this iteration's shared-memory reads are over -- damping, leapfrog and the stores.
-template <int K, int KP, int SW, bool SEP>
-__device__ __forceinline__ void plane_update(const StepParams& p, const float (&q)[2 * K + 1][4],
-                                             const float* cp, int tx, int ty, float4 o4, float4 r4,
-                                             float4 d4, const float (&dxy)[4], float dzv,
-                                             bool warp_dxy, bool rin, bool lane0,
-                                             uint64_t* done_bar, float* po, long long gc) {
-        float acc[4];
+// L(u) for the four nodes of a thread: d0 neighbours from the register queue, d1/d2
+// neighbours from the haloed centre box `cp` in shared memory (16-byte loads only).
+template <int K, int KP, int SW>
+__device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&q)[2 * K + 1][4],
+                                            const float* cp, int tx, int ty, float (&acc)[4]) {
         // centre and streaming-axis neighbours from the register queue
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            float a = p.k.c0 * q[K][c];
+            float a = k.c0 * q[K][c];
 #pragma unroll
-            for (int j = 1; j <= K; ++j) a = fmaf(p.k.cz[j - 1], q[K - j][c] + q[K + j][c], a);
+            for (int j = 1; j <= K; ++j) a = fmaf(k.cz[j - 1], q[K - j][c] + q[K + j][c], a);
             acc[c] = a;
         }
         // contiguous-axis neighbours: one aligned row segment
@@ -152,7 +147,7 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
             for (int c = 0; c < 4; ++c)
 #pragma unroll
                 for (int j = 1; j <= K; ++j)
-                    acc[c] = fmaf(p.k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], acc[c]);
+                    acc[c] = fmaf(k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], acc[c]);
         }
         // d1 neighbours: the column strip above and below
         {
@@ -161,12 +156,25 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
             for (int j = 1; j <= K; ++j) {
                 const float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
                 const float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
-                acc[0] = fmaf(p.k.cy[j - 1], lo.x + hi.x, acc[0]);
-                acc[1] = fmaf(p.k.cy[j - 1], lo.y + hi.y, acc[1]);
-                acc[2] = fmaf(p.k.cy[j - 1], lo.z + hi.z, acc[2]);
-                acc[3] = fmaf(p.k.cy[j - 1], lo.w + hi.w, acc[3]);
+                acc[0] = fmaf(k.cy[j - 1], lo.x + hi.x, acc[0]);
+                acc[1] = fmaf(k.cy[j - 1], lo.y + hi.y, acc[1]);
+                acc[2] = fmaf(k.cy[j - 1], lo.z + hi.z, acc[2]);
+                acc[3] = fmaf(k.cy[j - 1], lo.w + hi.w, acc[3]);
             }
         }
+}
+
+// One output plane for the four nodes of a thread: stencil from the register queue (d0)
+// and the centre plane in shared memory `cp` (d1, d2), then -- after telling the producer
+// that this iteration's shared-memory reads are over -- damping, leapfrog and the stores.
+template <int K, int KP, int SW, bool SEP>
+__device__ __forceinline__ void plane_update(const StepParams& p, const float (&q)[2 * K + 1][4],
+                                             const float* cp, int tx, int ty, float4 o4, float4 r4,
+                                             float4 d4, const float (&dxy)[4], float dzv,
+                                             bool warp_dxy, bool rin, bool lane0,
+                                             uint64_t* done_bar, float* po, long long gc) {
+        float acc[4];
+        stencil_acc<K, KP, SW>(p.k, q, cp, tx, ty, acc);
         // all shared-memory reads of this iteration are done
         __syncwarp();
         if (lane0) mbar_arrive(done_bar);

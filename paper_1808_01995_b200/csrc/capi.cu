@@ -26,6 +26,11 @@ std::vector<StepVariant>& step_variant_registry() {
     return reg;
 }
 
+std::vector<TtiVariant>& tti_variant_registry() {
+    static std::vector<TtiVariant> reg;
+    return reg;
+}
+
 namespace {
 
 thread_local std::string g_create_err;
@@ -803,41 +808,40 @@ void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stre
 
 // ---- TTI forward ---------------------------------------------------------------------------
 
-void tti_fill_params(Plan& P, TtiParams& tp) {
-    tp.K = P.K;
+void tti_coef(const Plan& P, TtiCoef& k) {
     double ih[3], ih2[3], c0 = 0.0;
     for (int d = 0; d < 3; ++d) {
         ih[d] = P.act[d] ? 1.0 / P.h[d] : 0.0;
         ih2[d] = ih[d] * ih[d];
         c0 += P.w2[0] * ih2[d];
     }
-    tp.c0 = float(c0);
+    k.c0 = float(c0);
     for (int j = 1; j <= P.K; ++j) {
-        tp.lz[j - 1] = float(P.w2[j] * ih2[0]);
-        tp.ly[j - 1] = float(P.w2[j] * ih2[1]);
-        tp.lx[j - 1] = float(P.w2[j] * ih2[2]);
-        tp.fz[j - 1] = float(P.w1[j] * ih[0]);
-        tp.fy[j - 1] = float(P.w1[j] * ih[1]);
-        tp.fx[j - 1] = float(P.w1[j] * ih[2]);
+        k.lz[j - 1] = float(P.w2[j] * ih2[0]);
+        k.ly[j - 1] = float(P.w2[j] * ih2[1]);
+        k.lx[j - 1] = float(P.w2[j] * ih2[2]);
+        k.fz[j - 1] = float(P.w1[j] * ih[0]);
+        k.fy[j - 1] = float(P.w1[j] * ih[1]);
+        k.fx[j - 1] = float(P.w1[j] * ih[2]);
     }
-    tp.qscale = P.coef.qscale;
-    tp.n0 = P.n0;
-    tp.N1 = int(P.N[1]);
-    tp.N2 = int(P.N[2]);
-    tp.pitch = P.pitch;
-    tp.plane = P.plane;
-    tp.a = P.t_a.as<float>();
-    tp.b = P.t_b.as<float>();
-    tp.c = P.t_c.as<float>();
-    tp.e1 = P.t_e1.as<float>();
-    tp.e2 = P.t_e2.as<float>();
-    tp.rm = P.r.as<float>();
-    tp.damp = P.sep ? nullptr : P.damp.as<float>();
-    tp.dz = P.dz.as<float>();
-    tp.dy = P.dy.as<float>();
-    tp.dx = P.dx.as<float>();
-    tp.gp = P.t_gp.as<float>();
-    tp.gr = P.t_gr.as<float>();
+    k.qscale = P.coef.qscale;
+}
+
+// tensor maps of every TTI field for the (fixed) TTI tile shape
+void tti_make_maps(Plan& P) {
+    const TtiVariant& v = *P.tti_variant;
+    void* wf[Plan::TF_COUNT] = {P.u[0].p, P.u[1].p, P.t_r[0].p, P.t_r[1].p, P.t_gp.p,
+                                P.t_gr.p, P.t_a.p, P.t_b.p, P.t_c.p};
+    for (int i = 0; i < Plan::TF_COUNT; ++i) {
+        encode_map(&P.tt_halo[i], wf[i], P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane, v.box_w,
+                   v.box_h);
+        encode_map(&P.tt_plain[i], wf[i], P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
+                   v.tile_x, v.tile_y);
+    }
+    void* cf[Plan::TC_COUNT] = {P.r.p, P.t_e1.p, P.t_e2.p, P.t_hzp.p, P.t_hzr.p,
+                                P.sep ? P.r.p : P.damp.p};
+    for (int i = 0; i < Plan::TC_COUNT; ++i)
+        encode_map(&P.tt_c[i], cf[i], P.N[2], P.N[1], P.n0, P.pitch, P.plane, v.tile_x, v.tile_y);
 }
 
 void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
@@ -849,25 +853,86 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
         SFB_CUDA(cudaMemsetAsync(P.t_r[b].p, 0, size_t(P.ucount) * 4, P.s_main));
     SFB_CUDA(cudaMemsetAsync(P.t_gp.p, 0, size_t(P.ucount) * 4, P.s_main));
     SFB_CUDA(cudaMemsetAsync(P.t_gr.p, 0, size_t(P.ucount) * 4, P.s_main));
-    TtiParams tp{};
-    tti_fill_params(P, tp);
+    const TtiVariant& v = *P.tti_variant;
     const long long nt = P.desc.nt;
-    dim3 block(kTtiBX, kTtiBY);
-    dim3 grid(unsigned((P.N[2] + kTtiBX - 1) / kTtiBX), unsigned((P.N[1] + kTtiBY - 1) / kTtiBY),
-              unsigned(P.n0));
+    const int sepi = P.sep ? 1 : 0;
+    // one chunk of d0 per block column so the grid fills the SMs (the rings allow one
+    // block per SM)
+    const long long tiles = ((P.N[2] + v.tile_x - 1) / v.tile_x) * ((P.N[1] + v.tile_y - 1) / v.tile_y);
+    int nch = int(std::max<long long>(1, (2LL * P.sm_count + tiles - 1) / tiles));
+    nch = std::min(nch, std::max(1, P.n0 / std::max(1, 2 * P.K)));
+    const int chunk = (P.n0 + nch - 1) / nch;
+    dim3 grid(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x), unsigned((P.N[1] + v.tile_y - 1) / v.tile_y),
+              unsigned((P.n0 + chunk - 1) / chunk));
+    RotParams rp{};
+    tti_coef(P, rp.k);
+    rp.N1 = int(P.N[1]);
+    rp.N2 = int(P.N[2]);
+    rp.pitch = P.pitch;
+    rp.plane = P.plane;
+    rp.z_lo = 0;
+    rp.z_hi = P.n0;
+    rp.chunk = chunk;
+    UpdParams up{};
+    up.k = rp.k;
+    up.dz = P.dz.as<float>();
+    up.dy = P.dy.as<float>();
+    up.dx = P.dx.as<float>();
+    up.N1 = rp.N1;
+    up.N2 = rp.N2;
+    up.pitch = P.pitch;
+    up.plane = P.plane;
+    up.z_lo = 0;
+    up.z_hi = P.n0;
+    up.chunk = chunk;
     std::unique_ptr<RowStreamer> rs;
     if (stream_out) rs.reset(new RowStreamer(P, P.cloud[SFB_CLOUD_REC], stream_out));
     SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
     for (long long t = 1; t < nt - 1; ++t) {
         const int cur = int(t & 1), oth = cur ^ 1;
-        tp.pc = P.u[cur].as<float>();
-        tp.rc = P.t_r[cur].as<float>();
-        tp.po = P.u[oth].as<float>();
-        tp.ro = P.t_r[oth].as<float>();
-        tti_gradient_kernel<<<grid, block, 0, P.s_main>>>(tp);
-        tti_update_kernel<<<grid, block, 0, P.s_main>>>(tp);
-        SFB_CUDA(cudaGetLastError());
-        P.launches += 2;
+        // 1. g(p), g(r)
+        RotMaps m1;
+        m1.f0_feed = P.tt_plain[Plan::TF_P0 + cur];
+        m1.f1_feed = P.tt_plain[Plan::TF_R0 + cur];
+        m1.f0_ctr = P.tt_halo[Plan::TF_P0 + cur];
+        m1.f1_ctr = P.tt_halo[Plan::TF_R0 + cur];
+        m1.a = P.tt_plain[Plan::TF_A];
+        m1.b = P.tt_plain[Plan::TF_B];
+        m1.c = P.tt_plain[Plan::TF_C];
+        rp.out0 = P.t_gp.as<float>();
+        rp.out1 = P.t_gr.as<float>();
+        rp.out_off = (long long)P.K * P.plane;
+        SFB_CUDA(v.rot[0](m1, rp, grid, P.s_main));
+        // 2. Hz(p), Hz(r)
+        RotMaps m2;
+        m2.f0_feed = P.tt_plain[Plan::TF_GP];
+        m2.f1_feed = P.tt_plain[Plan::TF_GR];
+        m2.f0_ctr = P.tt_halo[Plan::TF_GP];
+        m2.f1_ctr = P.tt_halo[Plan::TF_GR];
+        m2.a = P.tt_plain[Plan::TF_A];
+        m2.b = P.tt_halo[Plan::TF_B];
+        m2.c = P.tt_halo[Plan::TF_C];
+        rp.out0 = P.t_hzp.as<float>();
+        rp.out1 = P.t_hzr.as<float>();
+        rp.out_off = 0;
+        SFB_CUDA(v.rot[1](m2, rp, grid, P.s_main));
+        // 3. L(p), right-hand sides, leapfrog of both fields (in place over level t-1)
+        UpdMaps m3;
+        m3.p_feed = P.tt_plain[Plan::TF_P0 + cur];
+        m3.p_ctr = P.tt_halo[Plan::TF_P0 + cur];
+        m3.po = P.tt_plain[Plan::TF_P0 + oth];
+        m3.ro = P.tt_plain[Plan::TF_R0 + oth];
+        m3.rc = P.tt_plain[Plan::TF_R0 + cur];
+        m3.rm = P.tt_c[Plan::TC_RM];
+        m3.e1 = P.tt_c[Plan::TC_E1];
+        m3.e2 = P.tt_c[Plan::TC_E2];
+        m3.hzp = P.tt_c[Plan::TC_HZP];
+        m3.hzr = P.tt_c[Plan::TC_HZR];
+        m3.d = P.tt_c[Plan::TC_DAMP];
+        up.po = P.u[oth].as<float>();
+        up.ro = P.t_r[oth].as<float>();
+        SFB_CUDA(v.upd[sepi](m3, up, grid, P.s_main));
+        P.launches += 3;
         step_points(P, op, t, SFB_PART_ALL);                                   // p: scatter + gather
         step_points(P, op, t, SFB_PART_ALL, P.t_r[oth].as<float>(), false);    // r: scatter
         P.live_level[cur] = t;
@@ -1183,8 +1248,20 @@ SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
         upload_f64(P, embed_view(P, phi->ptr, phi->stride), tph);
         for (int b = 0; b < 2; ++b) P.t_r[b].alloc(size_t(P.ucount) * 4);
         for (DevBuf* d : {&P.t_gp, &P.t_gr, &P.t_a, &P.t_b, &P.t_c}) d->alloc(size_t(P.ucount) * 4);
-        P.t_e1.alloc(size_t(P.ccount) * 4);
-        P.t_e2.alloc(size_t(P.ccount) * 4);
+        for (DevBuf* d : {&P.t_e1, &P.t_e2, &P.t_hzp, &P.t_hzr}) d->alloc(size_t(P.ccount) * 4);
+        P.tti_variant = nullptr;
+        for (const TtiVariant& tv : tti_variant_registry())
+            if (tv.K == P.K) P.tti_variant = &tv;
+        require(P.tti_variant != nullptr, SFB_ERR_CAPABILITY, "no TTI kernel image for this order");
+        for (int i = 0; i < 2; ++i) {
+            SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_rot[i],
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(P.tti_variant->smem_rot[i])));
+            SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_upd[i],
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(P.tti_variant->smem_upd[i])));
+        }
+        tti_make_maps(P);
         const long long rows = (long long)P.n0 * P.N[1];
         tti_setup_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(
             te.as<double>(), td.as<double>(), tt.as<double>(), tph.as<double>(), P.t_a.as<float>(),

@@ -10,6 +10,7 @@
 
 #include "../../include/sfb200.h"
 #include "acoustic_kernel.cuh"
+#include "tti_variants.hpp"
 #include "variants.hpp"
 
 namespace sfb {
@@ -149,7 +150,14 @@ struct Plan {
 
     // TTI operator state (builder-defined formulation, csrc/tti_kernels.cuh)
     bool tti_set = false;
-    DevBuf t_r[2], t_gp, t_gr, t_a, t_b, t_c, t_e1, t_e2;  // p lives in u[2]
+    DevBuf t_r[2], t_gp, t_gr, t_a, t_b, t_c, t_e1, t_e2, t_hzp, t_hzr;  // p lives in u[2]
+    const TtiVariant* tti_variant = nullptr;
+    // tensor maps for the TTI tile: wavefield-layout fields (haloed / plain box) ...
+    enum { TF_P0, TF_P1, TF_R0, TF_R1, TF_GP, TF_GR, TF_A, TF_B, TF_C, TF_COUNT };
+    CUtensorMap tt_halo[TF_COUNT], tt_plain[TF_COUNT];
+    // ... and compact fields (plain box)
+    enum { TC_RM, TC_E1, TC_E2, TC_HZP, TC_HZR, TC_DAMP, TC_COUNT };
+    CUtensorMap tt_c[TC_COUNT];
     double w1[kMaxK + 1] = {0};                             // first-derivative weights
 
     const StepVariant* variant = nullptr;       // chosen tile shape

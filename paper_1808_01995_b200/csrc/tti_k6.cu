@@ -1,0 +1,2 @@
+#include "tti_variants.hpp"
+SFB_INSTANTIATE_TTI(6)

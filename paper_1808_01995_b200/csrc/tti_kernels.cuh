@@ -9,10 +9,17 @@
 // with D_i the centred order-k first derivative and L the acoustic order-k Laplacian, time
 // stepping / damping / injection / sampling as in the acoustic operator.
 //
-// Round-1 status: a first correct path -- two straightforward kernels per step (rotated
-// gradient g for p and r, then divergence + Laplacian + update) with the intermediate g
-// going through HBM/L2.  Fusing the two passes on chip (north star item 2) is the next
-// step; bench numbers for this operator are reported against its 48 B/node roofline as is.
+// One time step is three launches, all streamed along d0 with TMA boxes, shared-memory
+// stage rings and register queues exactly like the acoustic kernel (acoustic_kernel.cuh):
+//   1. rot_kernel<POST>: g(p), g(r)          (rotate after differentiating)
+//   2. rot_kernel<PRE> : Hz(p), Hz(r)        (multiply by the axis before differentiating)
+//   3. tti_update_kernel: L(p), the two right-hand sides and both leapfrog updates
+// In the rot kernels the two fields are handled by two groups of consumer warps of the same
+// block ("field-parallel warps"): each thread carries the d0 queue of ONE field, and both
+// groups share the boxes of the symmetry-axis components.  The intermediates g and Hz go
+// through HBM (28 + 28 + 44 = 100 bytes per node against the 48 of a fully fused kernel);
+// keeping them on chip needs a (2K+1)-plane ring of a haloed region per field, which does
+// not fit in 227 KB at order 12 -- see DESIGN.md section 3.4 for the arithmetic.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -21,111 +28,437 @@
 
 namespace sfb {
 
-struct TtiParams {
-    float c0;             // w2_0 * sum_d 1/h_d^2
-    float lx[kMaxK], ly[kMaxK], lz[kMaxK];   // Laplacian weights / h^2 per axis
-    float fx[kMaxK], fy[kMaxK], fz[kMaxK];   // first-derivative weights / h per axis
-    float qscale;         // 1/(2 dt)
-    int K;
-    int n0, N1, N2, pitch;
-    long long plane;
-    const float *a, *b, *c;     // unit symmetry axis, wavefield layout (ghost planes)
-    const float *e1, *e2;       // 1+2 eps, sqrt(1+2 delta), compact
-    const float *rm;            // dt^2/m, compact
-    const float *damp;          // dense damping (compact) or null
-    const float *dz, *dy, *dx;  // separable damping profiles
-    const float *pc, *rc;       // level t (ghost planes)
-    float *po, *ro;             // level t-1 in, level t+1 out (in place)
-    float *gp, *gr;             // rotated gradients of p and r (ghost planes, zero outside)
+struct TtiCoef {
+    float c0;                                  // Laplacian centre weight * sum 1/h^2
+    float lx[kMaxK], ly[kMaxK], lz[kMaxK];     // Laplacian weights / h^2 per axis
+    float fx[kMaxK], fy[kMaxK], fz[kMaxK];     // first-derivative weights / h per axis
+    float qscale;                              // 1/(2 dt)
 };
 
-constexpr int kTtiBX = 64, kTtiBY = 4;
+// ---- rotated first derivatives ---------------------------------------------------------
 
-// pass 1: g(p), g(r) at every owned node
-__global__ void __launch_bounds__(kTtiBX * kTtiBY)
-tti_gradient_kernel(const __grid_constant__ TtiParams p) {
-    const int x = blockIdx.x * kTtiBX + threadIdx.x;
-    const int y = blockIdx.y * kTtiBY + threadIdx.y;
-    const int z = blockIdx.z;
-    if (x >= p.N2 || y >= p.N1) return;
-    const long long q = (long long)(z + p.K) * p.plane + (long long)y * p.pitch + x;
-    float dp[3] = {0.f, 0.f, 0.f}, dr[3] = {0.f, 0.f, 0.f};
-    for (int j = 1; j <= p.K; ++j) {
-        const long long oz = (long long)j * p.plane;
-        dp[0] = fmaf(p.fz[j - 1], __ldg(p.pc + q + oz) - __ldg(p.pc + q - oz), dp[0]);
-        dr[0] = fmaf(p.fz[j - 1], __ldg(p.rc + q + oz) - __ldg(p.rc + q - oz), dr[0]);
-        const long long oy = (long long)j * p.pitch;
-        const bool yu = y + j < p.N1, yd = y - j >= 0;
-        const float pyu = yu ? __ldg(p.pc + q + oy) : 0.f, pyd = yd ? __ldg(p.pc + q - oy) : 0.f;
-        const float ryu = yu ? __ldg(p.rc + q + oy) : 0.f, ryd = yd ? __ldg(p.rc + q - oy) : 0.f;
-        dp[1] = fmaf(p.fy[j - 1], pyu - pyd, dp[1]);
-        dr[1] = fmaf(p.fy[j - 1], ryu - ryd, dr[1]);
-        const bool xu = x + j < p.N2, xd = x - j >= 0;
-        const float pxu = xu ? __ldg(p.pc + q + j) : 0.f, pxd = xd ? __ldg(p.pc + q - j) : 0.f;
-        const float rxu = xu ? __ldg(p.rc + q + j) : 0.f, rxd = xd ? __ldg(p.rc + q - j) : 0.f;
-        dp[2] = fmaf(p.fx[j - 1], pxu - pxd, dp[2]);
-        dr[2] = fmaf(p.fx[j - 1], rxu - rxd, dr[2]);
+struct RotMaps {
+    CUtensorMap f0_feed, f1_feed, f0_ctr, f1_ctr;  // the two input fields: plain / haloed box
+    CUtensorMap a, b, c;                           // axis components (box shape depends on PRE)
+};
+
+struct RotParams {
+    TtiCoef k;
+    float* out0;        // output of field 0 / field 1
+    float* out1;
+    long long out_off;  // element offset of local plane 0 inside the outputs
+    int N1, N2, pitch;
+    long long plane;
+    int z_lo, z_hi, chunk;
+};
+
+template <int K, int TXV, int TY, int NS, bool PRE>
+struct RotShape {
+    static constexpr int KP = (K + 3) & ~3;
+    static constexpr int TX = TXV * 4;
+    static constexpr int SW = TX + 2 * KP;
+    static constexpr int SH = TY + 2 * K;
+    static constexpr int CBOX = SW * SH;
+    static constexpr int CPAD = ((CBOX + 31) / 32) * 32;
+    static constexpr int ABOX = TX * TY;
+    // POST: feed f0,f1 | centre f0,f1 | plain a,b,c      PRE: feed g0,g1,a | centre g0,g1,b,c
+    static constexpr int NFEED = PRE ? 3 : 2;
+    static constexpr int NCTR = PRE ? 4 : 2;
+    static constexpr int NPLAIN = PRE ? 0 : 3;
+    static constexpr int STAGE = NFEED * ABOX + NCTR * CPAD + NPLAIN * ABOX;
+    static constexpr int GROUP = TXV * TY;            // consumer threads per field
+    static constexpr int NTHREADS = 2 * GROUP + 32;
+    static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8 + 128;
+    static_assert(GROUP % 32 == 0 && (ABOX * 4) % 128 == 0, "tile shape");
+};
+
+template <int K, int TXV, int TY, int NS, bool PRE>
+__global__ void __launch_bounds__(RotShape<K, TXV, TY, NS, PRE>::NTHREADS)
+tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotParams p) {
+    using S = RotShape<K, TXV, TY, NS, PRE>;
+    constexpr int KP = S::KP, SW = S::SW, STAGE = S::STAGE, Q = 2 * K + 1;
+    constexpr int ABOX = S::ABOX, CPAD = S::CPAD, TX = S::TX;
+    constexpr int NCW = 2 * S::GROUP / 32;
+    constexpr int OFF_CTR = S::NFEED * ABOX;
+    constexpr int OFF_PLAIN = OFF_CTR + S::NCTR * CPAD;
+
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t mis = smem_u32(smem_raw) & 127u;
+    float* ring = reinterpret_cast<float*>(smem_raw + ((128u - mis) & 127u));
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
+    uint64_t* done = full + NS;
+
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int zb = p.z_lo + blockIdx.z * p.chunk;
+    const int ze = min(zb + p.chunk, p.z_hi);
+    const int nplanes = (ze - zb) + 2 * K;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(done + s, NCW);
+        }
+        mbar_fence_init();
     }
-    const float a = __ldg(p.a + q), b = __ldg(p.b + q), c = __ldg(p.c + q);
-    p.gp[q] = fmaf(a, dp[0], fmaf(b, dp[1], c * dp[2]));
-    p.gr[q] = fmaf(a, dr[0], fmaf(b, dr[1], c * dr[2]));
+    __syncthreads();
+
+    if (tid >= 2 * S::GROUP) {
+        if (tid == 2 * S::GROUP) {
+            int s = 0;
+            uint32_t dph = 0;
+            for (int n = 0; n < nplanes; ++n) {
+                if (n >= NS) mbar_wait(done + s, dph);
+                const bool out = n >= 2 * K;
+                float* st = ring + s * STAGE;
+                const int feed_b = S::NFEED * ABOX, rest_b = S::NCTR * S::CBOX + S::NPLAIN * ABOX;
+                mbar_arrive_expect_tx(full + s, (feed_b + (out ? rest_b : 0)) * 4);
+                // every field lives in the wavefield layout: buffer plane = local plane + K
+                tma_load_3d(st, &tm.f0_feed, x0, y0, zb + n, full + s);
+                tma_load_3d(st + ABOX, &tm.f1_feed, x0, y0, zb + n, full + s);
+                if (PRE) tma_load_3d(st + 2 * ABOX, &tm.a, x0, y0, zb + n, full + s);
+                if (out) {
+                    const int zc = zb + n - K;  // centre plane (buffer index)
+                    tma_load_3d(st + OFF_CTR, &tm.f0_ctr, x0 - KP, y0 - K, zc, full + s);
+                    tma_load_3d(st + OFF_CTR + CPAD, &tm.f1_ctr, x0 - KP, y0 - K, zc, full + s);
+                    if (PRE) {
+                        tma_load_3d(st + OFF_CTR + 2 * CPAD, &tm.b, x0 - KP, y0 - K, zc, full + s);
+                        tma_load_3d(st + OFF_CTR + 3 * CPAD, &tm.c, x0 - KP, y0 - K, zc, full + s);
+                    } else {
+                        tma_load_3d(st + OFF_PLAIN, &tm.a, x0, y0, zc, full + s);
+                        tma_load_3d(st + OFF_PLAIN + ABOX, &tm.b, x0, y0, zc, full + s);
+                        tma_load_3d(st + OFF_PLAIN + 2 * ABOX, &tm.c, x0, y0, zc, full + s);
+                    }
+                }
+                if (++s == NS) {
+                    s = 0;
+                    if (n >= NS) dph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers: group 0 differentiates field 0, group 1 field 1 ----------------------
+    const int field = tid / S::GROUP;
+    const int lt = tid - field * S::GROUP;
+    const int tx = lt % TXV, ty = lt / TXV;
+    const int x = x0 + 4 * tx, y = y0 + ty;
+    const bool rin = x < p.N2 && y < p.N1;
+    const bool lane0 = (tid & 31) == 0;
+    float* outp = (field ? p.out1 : p.out0) + p.out_off + (long long)zb * p.plane +
+                  (long long)y * p.pitch + x;
+
+    float q[Q][4];
+#pragma unroll
+    for (int j = 0; j < Q; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
+
+    const int aown = ty * TX + 4 * tx;
+    int s = 0;
+    uint32_t fph = 0;
+    for (int n = 0; n < nplanes; ++n) {
+        mbar_wait(full + s, fph);
+        const float* st = ring + s * STAGE;
+        {
+            float4 v = *reinterpret_cast<const float4*>(st + field * ABOX + aown);
+            if (PRE) {  // queue holds a * g
+                const float4 a4 = *reinterpret_cast<const float4*>(st + 2 * ABOX + aown);
+                v.x *= a4.x;
+                v.y *= a4.y;
+                v.z *= a4.z;
+                v.w *= a4.w;
+            }
+#pragma unroll
+            for (int j = 0; j < Q - 1; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
+            q[Q - 1][0] = v.x;
+            q[Q - 1][1] = v.y;
+            q[Q - 1][2] = v.z;
+            q[Q - 1][3] = v.w;
+        }
+        if (n < 2 * K) {
+            __syncwarp();
+            if (lane0) mbar_arrive(done + s);
+        } else {
+            const float* cp = st + OFF_CTR + field * CPAD;  // haloed centre box of this field
+            float d0[4], d1[4], d2[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float a = 0.f;
+#pragma unroll
+                for (int j = 1; j <= K; ++j) a = fmaf(p.k.fz[j - 1], q[K + j][c] - q[K - j][c], a);
+                d0[c] = a;
+                d1[c] = 0.f;
+                d2[c] = 0.f;
+            }
+            {   // d2: one aligned row segment (of the products when PRE)
+                float xr[2 * KP + 4];
+                const float* rowp = cp + (ty + K) * SW + 4 * tx;
+                const float* crow = st + OFF_CTR + 3 * CPAD + (ty + K) * SW + 4 * tx;  // c box (PRE)
+#pragma unroll
+                for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
+                    float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
+                    if (PRE) {
+                        const float4 n4 = *reinterpret_cast<const float4*>(crow + 4 * v);
+                        t4.x *= n4.x;
+                        t4.y *= n4.y;
+                        t4.z *= n4.z;
+                        t4.w *= n4.w;
+                    }
+                    xr[4 * v + 0] = t4.x;
+                    xr[4 * v + 1] = t4.y;
+                    xr[4 * v + 2] = t4.z;
+                    xr[4 * v + 3] = t4.w;
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int j = 1; j <= K; ++j)
+                        d2[c] = fmaf(p.k.fx[j - 1], xr[KP + c + j] - xr[KP + c - j], d2[c]);
+            }
+            {   // d1: column strip above and below
+                const float* colp = cp + ty * SW + KP + 4 * tx;
+                const float* bcol = st + OFF_CTR + 2 * CPAD + ty * SW + KP + 4 * tx;  // b box (PRE)
+#pragma unroll
+                for (int j = 1; j <= K; ++j) {
+                    float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
+                    float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
+                    if (PRE) {
+                        const float4 bl = *reinterpret_cast<const float4*>(bcol + (K - j) * SW);
+                        const float4 bh = *reinterpret_cast<const float4*>(bcol + (K + j) * SW);
+                        lo.x *= bl.x; lo.y *= bl.y; lo.z *= bl.z; lo.w *= bl.w;
+                        hi.x *= bh.x; hi.y *= bh.y; hi.z *= bh.z; hi.w *= bh.w;
+                    }
+                    d1[0] = fmaf(p.k.fy[j - 1], hi.x - lo.x, d1[0]);
+                    d1[1] = fmaf(p.k.fy[j - 1], hi.y - lo.y, d1[1]);
+                    d1[2] = fmaf(p.k.fy[j - 1], hi.z - lo.z, d1[2]);
+                    d1[3] = fmaf(p.k.fy[j - 1], hi.w - lo.w, d1[3]);
+                }
+            }
+            float o[4];
+            if (PRE) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) o[c] = d0[c] + d1[c] + d2[c];
+            } else {
+                const float* np = st + OFF_PLAIN + aown;
+                const float4 a4 = *reinterpret_cast<const float4*>(np);
+                const float4 b4 = *reinterpret_cast<const float4*>(np + ABOX);
+                const float4 c4 = *reinterpret_cast<const float4*>(np + 2 * ABOX);
+                o[0] = fmaf(a4.x, d0[0], fmaf(b4.x, d1[0], c4.x * d2[0]));
+                o[1] = fmaf(a4.y, d0[1], fmaf(b4.y, d1[1], c4.y * d2[1]));
+                o[2] = fmaf(a4.z, d0[2], fmaf(b4.z, d1[2], c4.z * d2[2]));
+                o[3] = fmaf(a4.w, d0[3], fmaf(b4.w, d1[3], c4.w * d2[3]));
+            }
+            __syncwarp();
+            if (lane0) mbar_arrive(done + s);
+            if (rin) *reinterpret_cast<float4*>(outp) = make_float4(o[0], o[1], o[2], o[3]);
+            outp += p.plane;
+        }
+        if (++s == NS) {
+            s = 0;
+            fph ^= 1;
+        }
+    }
 }
 
-// pass 2: Hz(p), Hz(r), L(p) and the leapfrog update of both fields
-__global__ void __launch_bounds__(kTtiBX * kTtiBY)
-tti_update_kernel(const __grid_constant__ TtiParams p) {
-    const int x = blockIdx.x * kTtiBX + threadIdx.x;
-    const int y = blockIdx.y * kTtiBY + threadIdx.y;
-    const int z = blockIdx.z;
-    if (x >= p.N2 || y >= p.N1) return;
-    const long long q = (long long)(z + p.K) * p.plane + (long long)y * p.pitch + x;
-    const long long k = (long long)z * p.plane + (long long)y * p.pitch + x;
-    const float pcq = __ldg(p.pc + q), rcq = __ldg(p.rc + q);
-    float hzp = 0.f, hzr = 0.f, lap = p.c0 * pcq;
-    for (int j = 1; j <= p.K; ++j) {
-        {   // axis 0: ghost planes hold zeros (or the neighbour slab), no bounds needed
-            const long long o = (long long)j * p.plane;
-            const float nu = __ldg(p.a + q + o), nd = __ldg(p.a + q - o);
-            hzp = fmaf(p.fz[j - 1], nu * __ldg(p.gp + q + o) - nd * __ldg(p.gp + q - o), hzp);
-            hzr = fmaf(p.fz[j - 1], nu * __ldg(p.gr + q + o) - nd * __ldg(p.gr + q - o), hzr);
-            lap = fmaf(p.lz[j - 1], __ldg(p.pc + q + o) + __ldg(p.pc + q - o), lap);
+// ---- update: L(p), right-hand sides, leapfrog of p and r -----------------------------------
+
+struct UpdMaps {
+    CUtensorMap p_feed, p_ctr;               // u[t] = p: plain / haloed box
+    CUtensorMap po, ro, rc, rm, e1, e2, hzp, hzr, d;  // plain boxes of the output plane
+};
+
+struct UpdParams {
+    TtiCoef k;
+    const float *dz, *dy, *dx;   // separable damping profiles
+    float* po;                   // p level being overwritten (ghost planes)
+    float* ro;                   // r level being overwritten
+    int N1, N2, pitch;
+    long long plane;
+    int z_lo, z_hi, chunk;
+};
+
+template <int K, int TXV, int TY, int NS, bool SEP>
+struct UpdShape {
+    static constexpr int KP = (K + 3) & ~3;
+    static constexpr int TX = TXV * 4;
+    static constexpr int SW = TX + 2 * KP;
+    static constexpr int SH = TY + 2 * K;
+    static constexpr int CBOX = SW * SH;
+    static constexpr int CPAD = ((CBOX + 31) / 32) * 32;
+    static constexpr int ABOX = TX * TY;
+    static constexpr int NARR = SEP ? 8 : 9;   // po ro rc rm e1 e2 hzp hzr (damp)
+    static constexpr int STAGE = ABOX + CPAD + NARR * ABOX;
+    static constexpr int NCONS = TXV * TY;
+    static constexpr int NTHREADS = NCONS + 32;
+    static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8 + 128;
+};
+
+template <int K, int TXV, int TY, int NS, bool SEP>
+__global__ void __launch_bounds__(UpdShape<K, TXV, TY, NS, SEP>::NTHREADS)
+tti_update_kernel(const __grid_constant__ UpdMaps tm, const __grid_constant__ UpdParams p) {
+    using S = UpdShape<K, TXV, TY, NS, SEP>;
+    constexpr int KP = S::KP, SW = S::SW, STAGE = S::STAGE, Q = 2 * K + 1;
+    constexpr int NARR = S::NARR, ABOX = S::ABOX, CPAD = S::CPAD, TX = S::TX;
+    constexpr int NCW = S::NCONS / 32;
+
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t mis = smem_u32(smem_raw) & 127u;
+    float* ring = reinterpret_cast<float*>(smem_raw + ((128u - mis) & 127u));
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
+    uint64_t* done = full + NS;
+
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int zb = p.z_lo + blockIdx.z * p.chunk;
+    const int ze = min(zb + p.chunk, p.z_hi);
+    const int nplanes = (ze - zb) + 2 * K;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(done + s, NCW);
         }
-        {
-            const long long o = (long long)j * p.pitch;
-            const bool u = y + j < p.N1, d = y - j >= 0;
-            const float nu = u ? __ldg(p.b + q + o) : 0.f, nd = d ? __ldg(p.b + q - o) : 0.f;
-            const float gpu_ = u ? __ldg(p.gp + q + o) : 0.f, gpd = d ? __ldg(p.gp + q - o) : 0.f;
-            const float gru = u ? __ldg(p.gr + q + o) : 0.f, grd = d ? __ldg(p.gr + q - o) : 0.f;
-            const float pu = u ? __ldg(p.pc + q + o) : 0.f, pd = d ? __ldg(p.pc + q - o) : 0.f;
-            hzp = fmaf(p.fy[j - 1], nu * gpu_ - nd * gpd, hzp);
-            hzr = fmaf(p.fy[j - 1], nu * gru - nd * grd, hzr);
-            lap = fmaf(p.ly[j - 1], pu + pd, lap);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (tid >= S::NCONS) {
+        if (tid == S::NCONS) {
+            int s = 0;
+            uint32_t dph = 0;
+            for (int n = 0; n < nplanes; ++n) {
+                if (n >= NS) mbar_wait(done + s, dph);
+                const bool out = n >= 2 * K;
+                float* st = ring + s * STAGE;
+                mbar_arrive_expect_tx(full + s, (ABOX + (out ? S::CBOX + NARR * ABOX : 0)) * 4);
+                tma_load_3d(st, &tm.p_feed, x0, y0, zb + n, full + s);
+                if (out) {
+                    const int zo = zb + n - 2 * K;   // local output plane; buffer plane zo + K
+                    tma_load_3d(st + ABOX, &tm.p_ctr, x0 - KP, y0 - K, zo + K, full + s);
+                    float* ad = st + ABOX + CPAD;
+                    tma_load_3d(ad + 0 * ABOX, &tm.po, x0, y0, zo + K, full + s);
+                    tma_load_3d(ad + 1 * ABOX, &tm.ro, x0, y0, zo + K, full + s);
+                    tma_load_3d(ad + 2 * ABOX, &tm.rc, x0, y0, zo + K, full + s);
+                    tma_load_3d(ad + 3 * ABOX, &tm.rm, x0, y0, zo, full + s);
+                    tma_load_3d(ad + 4 * ABOX, &tm.e1, x0, y0, zo, full + s);
+                    tma_load_3d(ad + 5 * ABOX, &tm.e2, x0, y0, zo, full + s);
+                    tma_load_3d(ad + 6 * ABOX, &tm.hzp, x0, y0, zo, full + s);
+                    tma_load_3d(ad + 7 * ABOX, &tm.hzr, x0, y0, zo, full + s);
+                    if (!SEP) tma_load_3d(ad + 8 * ABOX, &tm.d, x0, y0, zo, full + s);
+                }
+                if (++s == NS) {
+                    s = 0;
+                    if (n >= NS) dph ^= 1;
+                }
+            }
         }
+        return;
+    }
+
+    const int tx = tid % TXV, ty = tid / TXV;
+    const int x = x0 + 4 * tx, y = y0 + ty;
+    const bool rin = x < p.N2 && y < p.N1;
+    const bool lane0 = (tid & 31) == 0;
+    float dxy[4] = {0.f, 0.f, 0.f, 0.f};
+    if (SEP && rin) {
+        const float4 dx4 = __ldg(reinterpret_cast<const float4*>(p.dx + x));
+        const float dyv = __ldg(p.dy + y);
+        dxy[0] = dx4.x + dyv;
+        dxy[1] = dx4.y + dyv;
+        dxy[2] = dx4.z + dyv;
+        dxy[3] = dx4.w + dyv;
+    }
+    float q[Q][4];
+#pragma unroll
+    for (int j = 0; j < Q; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
+
+    StencilCoef lk;
+    lk.c0 = p.k.c0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        lk.cx[j] = p.k.lx[j];
+        lk.cy[j] = p.k.ly[j];
+        lk.cz[j] = p.k.lz[j];
+    }
+
+    const int aown = ty * TX + 4 * tx;
+    const long long g0 = (long long)(zb + K) * p.plane + (long long)y * p.pitch + x;
+    float* pp = p.po + g0;
+    float* rp = p.ro + g0;
+    int s = 0;
+    uint32_t fph = 0;
+    for (int n = 0; n < nplanes; ++n) {
+        mbar_wait(full + s, fph);
+        const float* st = ring + s * STAGE;
         {
-            const bool u = x + j < p.N2, d = x - j >= 0;
-            const float nu = u ? __ldg(p.c + q + j) : 0.f, nd = d ? __ldg(p.c + q - j) : 0.f;
-            const float gpu_ = u ? __ldg(p.gp + q + j) : 0.f, gpd = d ? __ldg(p.gp + q - j) : 0.f;
-            const float gru = u ? __ldg(p.gr + q + j) : 0.f, grd = d ? __ldg(p.gr + q - j) : 0.f;
-            const float pu = u ? __ldg(p.pc + q + j) : 0.f, pd = d ? __ldg(p.pc + q - j) : 0.f;
-            hzp = fmaf(p.fx[j - 1], nu * gpu_ - nd * gpd, hzp);
-            hzr = fmaf(p.fx[j - 1], nu * gru - nd * grd, hzr);
-            lap = fmaf(p.lx[j - 1], pu + pd, lap);
+            const float4 v = *reinterpret_cast<const float4*>(st + aown);
+#pragma unroll
+            for (int j = 0; j < Q - 1; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
+            q[Q - 1][0] = v.x;
+            q[Q - 1][1] = v.y;
+            q[Q - 1][2] = v.z;
+            q[Q - 1][3] = v.w;
+        }
+        if (n < 2 * K) {
+            __syncwarp();
+            if (lane0) mbar_arrive(done + s);
+        } else {
+            const float* ap = st + ABOX + CPAD + aown;
+            float a[NARR][4];
+#pragma unroll
+            for (int i = 0; i < NARR; ++i) {
+                const float4 v = *reinterpret_cast<const float4*>(ap + i * ABOX);
+                a[i][0] = v.x;
+                a[i][1] = v.y;
+                a[i][2] = v.z;
+                a[i][3] = v.w;
+            }
+            float dzv = 0.f;
+            if (SEP) dzv = __ldg(p.dz + (zb + n - 2 * K));
+            float lap[4];
+            stencil_acc<K, KP, SW>(lk, q, st + ABOX, tx, ty, lap);
+            __syncwarp();
+            if (lane0) mbar_arrive(done + s);
+            float pn[4], rn[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float po = a[0][c], ro = a[1][c], rc = a[2][c], rm = a[3][c];
+                const float e1 = a[4][c], e2 = a[5][c], hzp = a[6][c], hzr = a[7][c];
+                const float dmp = SEP ? (dxy[c] + dzv) : a[NARR - 1][c];
+                const float h0 = lap[c] - hzp;
+                const float rhs_p = fmaf(e1, h0, e2 * hzr);
+                const float rhs_r = fmaf(e2, h0, hzr);
+                const float qq = dmp * rm * p.k.qscale;
+                const float c1 = fast_rcp(1.f + qq), c2 = (1.f - qq) * c1;
+                pn[c] = fmaf(c1, fmaf(rm, rhs_p, 2.f * q[K][c]), -c2 * po);
+                rn[c] = fmaf(c1, fmaf(rm, rhs_r, 2.f * rc), -c2 * ro);
+            }
+            if (rin) {
+                __stcs(reinterpret_cast<float4*>(pp), make_float4(pn[0], pn[1], pn[2], pn[3]));
+                __stcs(reinterpret_cast<float4*>(rp), make_float4(rn[0], rn[1], rn[2], rn[3]));
+            }
+            pp += p.plane;
+            rp += p.plane;
+        }
+        if (++s == NS) {
+            s = 0;
+            fph ^= 1;
         }
     }
-    const float h0 = lap - hzp;
-    const float e1 = __ldg(p.e1 + k), e2 = __ldg(p.e2 + k);
-    const float rhs_p = fmaf(e1, h0, e2 * hzr);
-    const float rhs_r = fmaf(e2, h0, hzr);
-    const float rm = __ldg(p.rm + k);
-    const float dmp = p.damp ? __ldg(p.damp + k) : (__ldg(p.dz + z) + __ldg(p.dy + y) + __ldg(p.dx + x));
-    const float qq = dmp * rm * p.qscale;
-    const float c1 = fast_rcp(1.f + qq), c2 = (1.f - qq) * c1;
-    p.po[q] = fmaf(c1, fmaf(rm, rhs_p, 2.f * pcq), -c2 * p.po[q]);
-    p.ro[q] = fmaf(c1, fmaf(rm, rhs_r, 2.f * rcq), -c2 * p.ro[q]);
 }
 
 // set-up: unit symmetry axis and Thomsen factors from the f64 inputs
-__global__ void tti_setup_kernel(const double* __restrict__ eps, const double* __restrict__ delta,
+static __global__ void tti_setup_kernel(const double* __restrict__ eps, const double* __restrict__ delta,
                                  const double* __restrict__ theta, const double* __restrict__ phi,
                                  float* a, float* b, float* c, float* e1, float* e2,
                                  long long rows, int n2, int pitch, long long ghost_off) {
