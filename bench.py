@@ -240,7 +240,7 @@ def ours(args):
     if not torch.cuda.is_available() or capi.device_count() < 1:
         raise SystemExit("bench.py needs a CUDA device: there is no CPU fallback")
     K, W = args.steps, max(args.warmup, 3)
-    if world > 1:
+    if world > 1 or os.environ.get("SFB_BENCH_FORCE_DIST"):
         from paper_1808_01995_b200 import slabs
         return slabs.bench_distributed(args, K, W, build_workload, workload_config,
                                        BYTES_PER_POINT, peaks)

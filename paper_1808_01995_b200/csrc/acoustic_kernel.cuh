@@ -33,6 +33,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace sfb {
 
 constexpr int kMaxK = 8;
@@ -115,18 +117,83 @@ __device__ __forceinline__ float fast_rcp(float x) {
 
 // L(u) for the four nodes of a thread: d0 neighbours from the register queue, d1/d2
 // neighbours from the haloed centre box `cp` in shared memory (16-byte loads only).
-template <int K, int KP, int SW>
+// Packed fp32 pairs (Blackwell FADD2 / FMUL2 / FFMA2): one issue slot for two nodes.  The
+// kernels are issue-bound at high order, not FMA-pipe-bound, so the d0 and d1 parts of the
+// stencil -- whose operands are register-aligned pairs -- run packed.  Results are the same
+// IEEE roundings as the scalar instructions.
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+    unsigned long long ra, rb, rd;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+    unsigned long long ra, rb, rd;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+    unsigned long long ra, rb, rd;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+    unsigned long long ra, rb, rc, rd;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
+}
+__device__ __forceinline__ float2 f2_splat(float v) { return make_float2(v, v); }
+
+// The register queue is addressed through a compile-time rotation ROT: logical plane i of
+// the queue lives in q[(i + ROT) % (2K+1)].  Kernels that shift the queue every iteration
+// use ROT = 0; the unrolled-rotation kernels advance ROT instead of moving registers.
+template <int K, int KP, int SW, int ROT = 0>
 __device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&q)[2 * K + 1][4],
                                             const float* cp, int tx, int ty, float (&acc)[4]) {
-        // centre and streaming-axis neighbours from the register queue
+        constexpr int Q = 2 * K + 1;
+#define SFB_Q(i) q[((i) + ROT) % Q]
+        // centre and streaming-axis neighbours from the register queue, two nodes per op
+        float2 a01 = f2_mul(f2_splat(k.c0), make_float2(SFB_Q(K)[0], SFB_Q(K)[1]));
+        float2 a23 = f2_mul(f2_splat(k.c0), make_float2(SFB_Q(K)[2], SFB_Q(K)[3]));
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            float a = k.c0 * q[K][c];
-#pragma unroll
-            for (int j = 1; j <= K; ++j) a = fmaf(k.cz[j - 1], q[K - j][c] + q[K + j][c], a);
-            acc[c] = a;
+        for (int j = 1; j <= K; ++j) {
+            const float2 w = f2_splat(k.cz[j - 1]);
+            a01 = f2_fma(w, f2_add(make_float2(SFB_Q(K - j)[0], SFB_Q(K - j)[1]),
+                                   make_float2(SFB_Q(K + j)[0], SFB_Q(K + j)[1])), a01);
+            a23 = f2_fma(w, f2_add(make_float2(SFB_Q(K - j)[2], SFB_Q(K - j)[3]),
+                                   make_float2(SFB_Q(K + j)[2], SFB_Q(K + j)[3])), a23);
         }
-        // contiguous-axis neighbours: one aligned row segment
+        // d1 neighbours: the column strip above and below (aligned pairs again)
+        {
+            const float* colp = cp + ty * SW + KP + 4 * tx;
+#pragma unroll
+            for (int j = 1; j <= K; ++j) {
+                const float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
+                const float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
+                const float2 w = f2_splat(k.cy[j - 1]);
+                a01 = f2_fma(w, f2_add(make_float2(lo.x, lo.y), make_float2(hi.x, hi.y)), a01);
+                a23 = f2_fma(w, f2_add(make_float2(lo.z, lo.w), make_float2(hi.z, hi.w)), a23);
+            }
+        }
+        // contiguous-axis neighbours: one aligned row segment; the shifted operands are not
+        // register-aligned pairs, so this part stays scalar
+        float ax[4] = {0.f, 0.f, 0.f, 0.f};
         {
             float xr[2 * KP + 4];
             const float* rowp = cp + (ty + K) * SW + 4 * tx;
@@ -134,7 +201,7 @@ __device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&
             for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
                 if (v == KP / 4) {  // own float4: already in the queue
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) xr[4 * v + c] = q[K][c];
+                    for (int c = 0; c < 4; ++c) xr[4 * v + c] = SFB_Q(K)[c];
                 } else {
                     const float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
                     xr[4 * v + 0] = t4.x;
@@ -147,34 +214,29 @@ __device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&
             for (int c = 0; c < 4; ++c)
 #pragma unroll
                 for (int j = 1; j <= K; ++j)
-                    acc[c] = fmaf(k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], acc[c]);
+                    ax[c] = fmaf(k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], ax[c]);
         }
-        // d1 neighbours: the column strip above and below
-        {
-            const float* colp = cp + ty * SW + KP + 4 * tx;
-#pragma unroll
-            for (int j = 1; j <= K; ++j) {
-                const float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
-                const float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
-                acc[0] = fmaf(k.cy[j - 1], lo.x + hi.x, acc[0]);
-                acc[1] = fmaf(k.cy[j - 1], lo.y + hi.y, acc[1]);
-                acc[2] = fmaf(k.cy[j - 1], lo.z + hi.z, acc[2]);
-                acc[3] = fmaf(k.cy[j - 1], lo.w + hi.w, acc[3]);
-            }
-        }
+        a01 = f2_add(a01, make_float2(ax[0], ax[1]));
+        a23 = f2_add(a23, make_float2(ax[2], ax[3]));
+        acc[0] = a01.x;
+        acc[1] = a01.y;
+        acc[2] = a23.x;
+        acc[3] = a23.y;
+#undef SFB_Q
 }
 
 // One output plane for the four nodes of a thread: stencil from the register queue (d0)
 // and the centre plane in shared memory `cp` (d1, d2), then -- after telling the producer
 // that this iteration's shared-memory reads are over -- damping, leapfrog and the stores.
-template <int K, int KP, int SW, bool SEP>
+template <int K, int KP, int SW, bool SEP, int ROT = 0>
 __device__ __forceinline__ void plane_update(const StepParams& p, const float (&q)[2 * K + 1][4],
                                              const float* cp, int tx, int ty, float4 o4, float4 r4,
                                              float4 d4, const float (&dxy)[4], float dzv,
                                              bool warp_dxy, bool rin, bool lane0,
                                              uint64_t* done_bar, float* po, long long gc) {
+        constexpr int QC = (K + ROT) % (2 * K + 1);  // physical slot of the centre plane
         float acc[4];
-        stencil_acc<K, KP, SW>(p.k, q, cp, tx, ty, acc);
+        stencil_acc<K, KP, SW, ROT>(p.k, q, cp, tx, ty, acc);
         // all shared-memory reads of this iteration are done
         __syncwarp();
         if (lane0) mbar_arrive(done_bar);
@@ -197,12 +259,21 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
                 const float qq = dv[c] * rv[c] * p.k.qscale;
                 const float c1 = fast_rcp(1.f + qq);
                 const float c2 = (1.f - qq) * c1;
-                const float t = fmaf(rv[c], acc[c], 2.f * q[K][c]);
+                const float t = fmaf(rv[c], acc[c], 2.f * q[QC][c]);
                 un[c] = fmaf(c1, t, -c2 * ov[c]);
             }
         } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) un[c] = fmaf(rv[c], acc[c], 2.f * q[K][c]) - ov[c];
+            const float2 u01 = make_float2(q[QC][0], q[QC][1]), u23 = make_float2(q[QC][2], q[QC][3]);
+            const float2 t01 = f2_fma(make_float2(rv[0], rv[1]), make_float2(acc[0], acc[1]),
+                                      f2_add(u01, u01));
+            const float2 t23 = f2_fma(make_float2(rv[2], rv[3]), make_float2(acc[2], acc[3]),
+                                      f2_add(u23, u23));
+            const float2 n01 = f2_add(t01, make_float2(-ov[0], -ov[1]));
+            const float2 n23 = f2_add(t23, make_float2(-ov[2], -ov[3]));
+            un[0] = n01.x;
+            un[1] = n01.y;
+            un[2] = n23.x;
+            un[3] = n23.y;
         }
         if (rin) {
             __stcs(reinterpret_cast<float4*>(po), make_float4(un[0], un[1], un[2], un[3]));
@@ -213,10 +284,10 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
                 const float4 g4 = __ldcs(reinterpret_cast<const float4*>(p.grad + gc));
                 const float4 s4 = __ldcs(reinterpret_cast<const float4*>(p.usave + gc));
                 float4 gn;
-                gn.x = fmaf(-s4.x * p.k.inv_dt2, (un[0] - 2.f * q[K][0]) + ov[0], g4.x);
-                gn.y = fmaf(-s4.y * p.k.inv_dt2, (un[1] - 2.f * q[K][1]) + ov[1], g4.y);
-                gn.z = fmaf(-s4.z * p.k.inv_dt2, (un[2] - 2.f * q[K][2]) + ov[2], g4.z);
-                gn.w = fmaf(-s4.w * p.k.inv_dt2, (un[3] - 2.f * q[K][3]) + ov[3], g4.w);
+                gn.x = fmaf(-s4.x * p.k.inv_dt2, (un[0] - 2.f * q[QC][0]) + ov[0], g4.x);
+                gn.y = fmaf(-s4.y * p.k.inv_dt2, (un[1] - 2.f * q[QC][1]) + ov[1], g4.y);
+                gn.z = fmaf(-s4.z * p.k.inv_dt2, (un[2] - 2.f * q[QC][2]) + ov[2], g4.z);
+                gn.w = fmaf(-s4.w * p.k.inv_dt2, (un[3] - 2.f * q[QC][3]) + ov[3], g4.w);
                 __stcs(reinterpret_cast<float4*>(p.grad + gc), gn);
             }
         }
@@ -423,7 +494,17 @@ struct DualShape {
     static_assert(NCONS % 32 == 0 && (ABOX * 4) % 128 == 0 && NS >= 2, "tile shape");
 };
 
-template <int K, int TXV, int TY, int NS, bool SEP, int MINB>
+template <int Q, int R, class F>
+__device__ __forceinline__ void rotate_run(F& f, int& n, int nplanes) {
+    if constexpr (R < Q) {
+        if (n >= nplanes) return;
+        f(std::integral_constant<int, R>{});
+        ++n;
+        rotate_run<Q, R + 1>(f, n, nplanes);
+    }
+}
+
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROTATE>
 __global__ void __launch_bounds__(DualShape<K, TXV, TY, NS, SEP>::NTHREADS, MINB)
 acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
                           const __grid_constant__ StepParams p) {
@@ -514,19 +595,26 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
     int s = 0;
     uint32_t fph = 0;
 
-    for (int n = 0; n < nplanes; ++n) {
+    // one plane: take the newest plane into the queue, and from iteration 2K on update one
+    // output plane.  R is the queue rotation (compile-time in the unrolled variant).
+    auto iteration = [&](auto rot, int n) {
+        constexpr int R = decltype(rot)::value;
         mbar_wait(full + s, fph);
         const float* st = ring + s * STAGE;
         {
             const float4 v = *reinterpret_cast<const float4*>(st + aown);
+            if constexpr (!ROTATE) {
 #pragma unroll
-            for (int j = 0; j < Q - 1; ++j)
+                for (int j = 0; j < Q - 1; ++j)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
-            q[Q - 1][0] = v.x;
-            q[Q - 1][1] = v.y;
-            q[Q - 1][2] = v.z;
-            q[Q - 1][3] = v.w;
+                    for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
+            }
+            // logical slot Q-1 (newest) under the rotation of this iteration
+            constexpr int NEW = (Q - 1 + R) % Q;
+            q[NEW][0] = v.x;
+            q[NEW][1] = v.y;
+            q[NEW][2] = v.z;
+            q[NEW][3] = v.w;
         }
         if (n < 2 * K) {
             __syncwarp();
@@ -539,8 +627,8 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
             if (!SEP) d4 = *reinterpret_cast<const float4*>(ap + 2 * ABOX);
             const float dzv = dzn;
             if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
-            plane_update<K, KP, SW, SEP>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
-                                         rin, lane0, done + s, po, gc);
+            plane_update<K, KP, SW, SEP, R>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
+                                            rin, lane0, done + s, po, gc);
             po += p.plane;
             gc += p.plane;
         }
@@ -548,6 +636,17 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
             s = 0;
             fph ^= 1;
         }
+    };
+    if constexpr (ROTATE) {
+        // unrolled by 2K+1: iteration i of a round sees the queue rotated by i+1 (the slot
+        // of the oldest plane is overwritten by the newest), so no register moves at all
+        int n = 0;
+        while (n < nplanes) {
+            auto step = [&](auto r) { iteration(std::integral_constant<int, (decltype(r)::value + 1) % Q>{}, n); };
+            rotate_run<Q, 0>(step, n, nplanes);
+        }
+    } else {
+        for (int n = 0; n < nplanes; ++n) iteration(std::integral_constant<int, 0>{}, n);
     }
 }
 

@@ -116,17 +116,18 @@ void make_tensor_maps(Plan& P) {
 
 // ---- tile shape / chunk choice ----------------------------------------------------------
 
+// dual: -1 any, 0 ring kernel, 1 dual-stream, 2 dual-stream with the rotated (unrolled) queue
 void select_variant(Plan& P, int txv, int ty, int nst, int dual = -1) {
     const StepVariant* best = nullptr;
     for (const StepVariant& v : step_variant_registry()) {
         if (v.K != P.K || v.sep != P.sep) continue;
-        if (dual >= 0 && int(v.dual) != dual) continue;
+        if (dual >= 0 && (int(v.dual) + int(v.rotate)) != dual) continue;
         if (txv > 0 && (v.TXV != txv || v.TY != ty || (nst > 0 && v.NST != nst))) continue;
         if (txv <= 0) {
             // default shape (measured on B200, tools/probe_tiles.py): the ring kernel up to
             // order 8, the dual-stream kernel (4 stages) above, 64 x 16 tiles
             const bool want_dual = P.K >= 5;
-            if (v.dual != want_dual || v.TXV != 16 || v.TY != 16) continue;
+            if (v.dual != want_dual || v.rotate || v.TXV != 16 || v.TY != 16) continue;
             if (v.NST != (want_dual ? 4 : P.K + 3)) continue;
         }
         if (!best) best = &v;
@@ -1197,7 +1198,8 @@ SFB_API int sfb_set_model(sfb_plan* plan, const sfb_field_view* m, const sfb_fie
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
         detect_separable_damping(P, embed_view(P, damp->ptr, damp->stride), tmp);
         if (P.sep) P.damp.release();
-        select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST, int(P.variant->dual));
+        select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST,
+                       int(P.variant->dual) + int(P.variant->rotate));
         P.model_set = true;
         P.history_valid = false;
     });
@@ -1528,7 +1530,7 @@ SFB_API int sfb_autotune(sfb_plan* plan, int steps) {
         float best_ms = 0.f;
         for (const StepVariant& v : step_variant_registry()) {
             if (v.K != P.K || v.sep != P.sep) continue;
-            select_variant(P, v.TXV, v.TY, v.NST, int(v.dual));
+            select_variant(P, v.TXV, v.TY, v.NST, int(v.dual) + int(v.rotate));
             SFB_CUDA(cudaMemsetAsync(P.u[0].p, 0, size_t(P.ucount) * 4, P.s_main));
             SFB_CUDA(cudaMemsetAsync(P.u[1].p, 0, size_t(P.ucount) * 4, P.s_main));
             P.save_every = 0;
@@ -1546,7 +1548,7 @@ SFB_API int sfb_autotune(sfb_plan* plan, int steps) {
             }
         }
         require(best != nullptr, SFB_ERR_CAPABILITY, "no kernel image for this space order");
-        select_variant(P, best->TXV, best->TY, best->NST, int(best->dual));
+        select_variant(P, best->TXV, best->TY, best->NST, int(best->dual) + int(best->rotate));
         P.history_valid = false;
         P.live_level[0] = P.live_level[1] = -1;
     });
@@ -1567,8 +1569,10 @@ SFB_API int sfb_set_dense_damping(sfb_plan* plan, int on) {
 SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
-        // stages < 0 selects the dual-stream kernel with |stages| stages
-        select_variant(*plan, txv, ty, stages < 0 ? -stages : stages, stages < 0 ? 1 : 0);
+        // stages < 0 selects the dual-stream kernel with |stages| stages; |stages| > 100 its
+        // rotated-queue variant with |stages| - 100 stages
+        const int a = stages < 0 ? -stages : stages;
+        select_variant(*plan, txv, ty, a > 100 ? a - 100 : a, stages < 0 ? (a > 100 ? 2 : 1) : 0);
         if (chunk > 0) plan->chunk = std::min(chunk, plan->n0);
     });
 }
@@ -1577,7 +1581,9 @@ SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* nst, int* chunk
     if (!plan || !plan->variant) return SFB_ERR_PARAMETER;
     if (txv) *txv = plan->variant->TXV;
     if (ty) *ty = plan->variant->TY;
-    if (nst) *nst = plan->variant->dual ? -plan->variant->NST : plan->variant->NST;
+    if (nst)
+        *nst = plan->variant->dual ? -(plan->variant->NST + (plan->variant->rotate ? 100 : 0))
+                                   : plan->variant->NST;
     if (chunk) *chunk = plan->chunk;
     if (sep) *sep = plan->variant->sep ? 1 : 0;
     return SFB_OK;

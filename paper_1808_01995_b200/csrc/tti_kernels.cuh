@@ -186,15 +186,23 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
         } else {
             const float* cp = st + OFF_CTR + field * CPAD;  // haloed centre box of this field
             float d0[4], d1[4], d2[4];
+            {   // d0 from the register queue, two nodes per instruction
+                float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float a = 0.f;
-#pragma unroll
-                for (int j = 1; j <= K; ++j) a = fmaf(p.k.fz[j - 1], q[K + j][c] - q[K - j][c], a);
-                d0[c] = a;
-                d1[c] = 0.f;
-                d2[c] = 0.f;
+                for (int j = 1; j <= K; ++j) {
+                    const float2 w = f2_splat(p.k.fz[j - 1]);
+                    a01 = f2_fma(w, f2_sub(make_float2(q[K + j][0], q[K + j][1]),
+                                           make_float2(q[K - j][0], q[K - j][1])), a01);
+                    a23 = f2_fma(w, f2_sub(make_float2(q[K + j][2], q[K + j][3]),
+                                           make_float2(q[K - j][2], q[K - j][3])), a23);
+                }
+                d0[0] = a01.x;
+                d0[1] = a01.y;
+                d0[2] = a23.x;
+                d0[3] = a23.y;
             }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) d2[c] = 0.f;
             {   // d2: one aligned row segment (of the products when PRE)
                 float xr[2 * KP + 4];
                 const float* rowp = cp + (ty + K) * SW + 4 * tx;
@@ -220,24 +228,32 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                     for (int j = 1; j <= K; ++j)
                         d2[c] = fmaf(p.k.fx[j - 1], xr[KP + c + j] - xr[KP + c - j], d2[c]);
             }
-            {   // d1: column strip above and below
+            {   // d1: column strip above and below (register-aligned pairs: packed)
                 const float* colp = cp + ty * SW + KP + 4 * tx;
                 const float* bcol = st + OFF_CTR + 2 * CPAD + ty * SW + KP + 4 * tx;  // b box (PRE)
+                float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int j = 1; j <= K; ++j) {
-                    float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
-                    float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
+                    const float4 lo = *reinterpret_cast<const float4*>(colp + (K - j) * SW);
+                    const float4 hi = *reinterpret_cast<const float4*>(colp + (K + j) * SW);
+                    float2 l01 = make_float2(lo.x, lo.y), l23 = make_float2(lo.z, lo.w);
+                    float2 h01 = make_float2(hi.x, hi.y), h23 = make_float2(hi.z, hi.w);
                     if (PRE) {
                         const float4 bl = *reinterpret_cast<const float4*>(bcol + (K - j) * SW);
                         const float4 bh = *reinterpret_cast<const float4*>(bcol + (K + j) * SW);
-                        lo.x *= bl.x; lo.y *= bl.y; lo.z *= bl.z; lo.w *= bl.w;
-                        hi.x *= bh.x; hi.y *= bh.y; hi.z *= bh.z; hi.w *= bh.w;
+                        l01 = f2_mul(l01, make_float2(bl.x, bl.y));
+                        l23 = f2_mul(l23, make_float2(bl.z, bl.w));
+                        h01 = f2_mul(h01, make_float2(bh.x, bh.y));
+                        h23 = f2_mul(h23, make_float2(bh.z, bh.w));
                     }
-                    d1[0] = fmaf(p.k.fy[j - 1], hi.x - lo.x, d1[0]);
-                    d1[1] = fmaf(p.k.fy[j - 1], hi.y - lo.y, d1[1]);
-                    d1[2] = fmaf(p.k.fy[j - 1], hi.z - lo.z, d1[2]);
-                    d1[3] = fmaf(p.k.fy[j - 1], hi.w - lo.w, d1[3]);
+                    const float2 w = f2_splat(p.k.fy[j - 1]);
+                    a01 = f2_fma(w, f2_sub(h01, l01), a01);
+                    a23 = f2_fma(w, f2_sub(h23, l23), a23);
                 }
+                d1[0] = a01.x;
+                d1[1] = a01.y;
+                d1[2] = a23.x;
+                d1[3] = a23.y;
             }
             float o[4];
             if (PRE) {

@@ -14,6 +14,7 @@ struct StepVariant {
     int K, TXV, TY, NST;  // NST: ring stages (ring kernel) or stages of the dual-stream ring
     bool sep;
     bool dual;            // dual-stream kernel (u[t] fetched as feed + centre boxes)
+    bool rotate;          // dual-stream kernel unrolled by 2K+1 (queue rotation, no moves)
     int tile_x, tile_y;   // output tile (d2, d1)
     int box_w, box_h;     // TMA box of u[t] (d2, d1)
     int halo_x;           // KP
@@ -37,7 +38,7 @@ void register_step() {
     using S = StepShape<K, TXV, TY, NST, SEP>;
     if constexpr (S::SMEM <= 227 * 1024) {
         StepVariant v;
-        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NST; v.sep = SEP; v.dual = false;
+        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NST; v.sep = SEP; v.dual = false; v.rotate = false;
         v.tile_x = S::TX; v.tile_y = TY; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
         v.nthreads = S::NTHREADS; v.smem = S::SMEM;
         v.func = reinterpret_cast<const void*>(&acoustic_step_kernel<K, TXV, TY, NST, SEP>);
@@ -46,23 +47,25 @@ void register_step() {
     }
 }
 
-template <int K, int TXV, int TY, int NS, bool SEP, int MINB>
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROT>
 cudaError_t launch_dual(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
     using S = DualShape<K, TXV, TY, NS, SEP>;
-    acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB><<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
+    acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT>
+        <<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
     return cudaGetLastError();
 }
 
-template <int K, int TXV, int TY, int NS, bool SEP, int MINB>
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROT = false>
 void register_dual() {
     using S = DualShape<K, TXV, TY, NS, SEP>;
     if constexpr (S::SMEM * MINB <= 227 * 1024) {
         StepVariant v;
-        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NS; v.sep = SEP; v.dual = true;
+        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NS; v.sep = SEP; v.dual = true; v.rotate = ROT;
         v.tile_x = S::TX; v.tile_y = TY; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
         v.nthreads = S::NTHREADS; v.smem = S::SMEM;
-        v.func = reinterpret_cast<const void*>(&acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB>);
-        v.launch = &launch_dual<K, TXV, TY, NS, SEP, MINB>;
+        v.func = reinterpret_cast<const void*>(
+            &acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT>);
+        v.launch = &launch_dual<K, TXV, TY, NS, SEP, MINB, ROT>;
         step_variant_registry().push_back(v);
     }
 }
@@ -81,6 +84,13 @@ void register_dual_pair() {
     register_dual<K, TXV, TY, NS, true, MINB>();
 }
 
+template <int K, int TXV, int TY, int NS>
+void register_rotated_pair() {
+    constexpr int MINB = K <= 4 ? 3 : 2;
+    register_dual<K, TXV, TY, NS, false, MINB, true>();
+    register_dual<K, TXV, TY, NS, true, MINB, true>();
+}
+
 // the tile shapes built for every half-order K (dense and separable damping); the first
 // entry is the default, sfb_set_tile / sfb_autotune pick among the rest
 template <int K>
@@ -93,6 +103,9 @@ void register_all_for_K() {
     register_dual_pair<K, 16, 16, 3>();
     register_dual_pair<K, 16, 16, 4>();
     register_dual_pair<K, 32, 8, 3>();
+    if constexpr (K <= 4) {  // unrolling by 2K+1 overflows the instruction cache above
+        register_rotated_pair<K, 16, 16, 3>();
+    }
 }
 
 struct VariantRegistrar {

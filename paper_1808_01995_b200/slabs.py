@@ -162,11 +162,14 @@ def bench_distributed(args, K, W, build_workload, workload_config, bytes_per_poi
     import torch
     import torch.distributed as dist
     from . import capi
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29577")
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device(f"cuda:{local}"))
     cfg, model, geom = build_workload(W + K)
     N = model.grid.shape
     order = model.space_order
@@ -186,8 +189,10 @@ def bench_distributed(args, K, W, build_workload, workload_config, bytes_per_poi
     launches0 = plan.launch_count()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.s_main.wait_stream(eng.s_bnd)
     with torch.cuda.stream(eng.s_main):
         e0.record()
+    eng.s_bnd.wait_stream(eng.s_main)
     step_loop(eng, ex, 1 + W, 1 + W + K)
     eng.s_main.wait_stream(eng.s_bnd)
     with torch.cuda.stream(eng.s_main):

@@ -63,7 +63,7 @@ def test_tile_shapes_agree_bitwise():
     plan = make_plan(model, geom, 8)
     base, _ = plan.forward(geom.src)
     u0 = plan.wavefield(geom.nt - 1)
-    for tile in [(16, 16, 8), (32, 8, 7), (16, 32, 7), (32, 16, 7), (16, 16, -3), (16, 16, -4), (32, 8, -3)]:
+    for tile in [(16, 16, 8), (32, 8, 7), (16, 32, 7), (32, 16, 7), (16, 16, -3), (16, 16, -4), (32, 8, -3), (16, 16, -103)]:
         for chunk in (0, 7, 60):
             plan.set_tile(*tile, chunk)
             rec, _ = plan.forward(geom.src)
