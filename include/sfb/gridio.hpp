@@ -1,0 +1,37 @@
+// gridio.hpp -- the wire formats on either side of the propagator path (SURVEY.md 8f,
+// rank 2): the SFGD binary grid container (proj/include/sf/gridio.hpp:8-18) and the trace
+// / coordinate CSV tables (proj/include/sf/sparse.hpp:97-104, proj/src/gridio.cpp:71-87).
+// Files written here are byte-identical to the reference's for the same data.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "sfb/sparse.hpp"
+
+namespace sfb {
+
+// magic "SFGD", u8 ndim, u8 dtype (0 = f64), u16 zero, u32 extent per dim, row-major f64
+// payload; little-endian
+void write_grid(const std::string& path, const std::vector<long>& shape,
+                const std::vector<double>& data);
+
+struct GridData {
+    std::vector<long> shape;
+    std::vector<double> data;
+};
+
+GridData read_grid(const std::string& path);
+
+// "t,p0,p1,..." header, one row per time sample, %.17g-precision values
+void write_traces_csv(const std::string& path, long nt, long npts,
+                      const std::vector<double>& traces, double t0, double dt);
+void write_traces_csv(const std::string& path, const SparseFunction& s,
+                      const std::vector<double>& times);
+void read_traces_csv(const std::string& path, SparseFunction& s,
+                     std::vector<double>* times = nullptr);
+// "x[,y[,z]]" header, one row per point
+void write_coords_csv(const std::string& path, const SparseFunction& s);
+std::vector<double> read_coords_csv(const std::string& path, std::size_t ndim);
+
+}  // namespace sfb

@@ -143,3 +143,35 @@ def dense_bench(n, order, steps, backend=EMITTED, nthreads=1):
 
 def emit_available():
     return bool(lib().sfr_emit_available())
+
+
+def write_grid(path, data):
+    data = np.ascontiguousarray(data, dtype=np.float64)
+    shape = (C.c_long * data.ndim)(*data.shape)
+    _chk(lib().sfr_write_grid(path.encode(), data.ndim, shape, data.ctypes.data_as(C.c_void_p)))
+
+
+def read_grid(path, capacity=1 << 24):
+    nd = C.c_int()
+    shape = (C.c_long * 8)()
+    buf = np.zeros(capacity)
+    _chk(lib().sfr_read_grid(path.encode(), C.byref(nd), shape, buf.ctypes.data_as(C.c_void_p),
+                             C.c_long(capacity)))
+    sh = [shape[i] for i in range(nd.value)]
+    return buf[: int(np.prod(sh))].reshape(sh).copy()
+
+
+def write_traces_table(path, traces, t0, dt):
+    tr = np.ascontiguousarray(traces, dtype=np.float64)
+    _chk(lib().sfr_write_traces_table(path.encode(), C.c_long(tr.shape[0]), C.c_long(tr.shape[1]),
+                                      tr.ctypes.data_as(C.c_void_p), C.c_double(t0), C.c_double(dt)))
+
+
+def write_cloud_csv(traces_path, coords_path, ndim, n, coords, traces, times):
+    co = np.ascontiguousarray(coords, dtype=np.float64)
+    tr = np.ascontiguousarray(traces, dtype=np.float64)
+    tm = np.ascontiguousarray(times, dtype=np.float64)
+    _chk(lib().sfr_write_cloud_csv(traces_path.encode(), coords_path.encode(), ndim, C.c_long(n),
+                                   C.c_long(tr.shape[1]), C.c_long(tr.shape[0]),
+                                   co.ctypes.data_as(C.c_void_p), tr.ctypes.data_as(C.c_void_p),
+                                   tm.ctypes.data_as(C.c_void_p)))

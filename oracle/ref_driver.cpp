@@ -16,6 +16,7 @@
 #include "sf/error.hpp"
 #include "sf/execute.hpp"
 #include "sf/geometry.hpp"
+#include "sf/gridio.hpp"
 #include "sf/lower.hpp"
 #include "sf/model.hpp"
 #include "sf/seismic_ops.hpp"
@@ -235,6 +236,49 @@ int sfr_dense_bench(long n, int order, long steps, int backend, int nthreads, do
         sf::ExecutionReport rep = (backend == 1) ? sf::run_emitted(op, args) : sf::run(op, args);
         if (seconds) *seconds = rep.seconds;
         if (flops_per_point) *flops_per_point = double(op.metrics.flops_per_point.total());
+    });
+}
+
+// the reference's own file writers / readers (proj/src/gridio.cpp, proj/src/sparse.cpp)
+int sfr_write_grid(const char* path, int ndim, const long* shape, const double* data) {
+    return guarded([&] {
+        std::vector<long> sh(shape, shape + ndim);
+        size_t n = 1;
+        for (long e : sh) n *= size_t(e);
+        sf::write_grid(path, sh, std::vector<double>(data, data + n));
+    });
+}
+
+int sfr_read_grid(const char* path, int* ndim, long* shape, double* data, long capacity) {
+    return guarded([&] {
+        sf::GridData g = sf::read_grid(path);
+        *ndim = int(g.shape.size());
+        std::copy(g.shape.begin(), g.shape.end(), shape);
+        if (long(g.data.size()) > capacity) throw sf::ParameterError("buffer too small");
+        std::copy(g.data.begin(), g.data.end(), data);
+    });
+}
+
+int sfr_write_traces_table(const char* path, long nt, long np, const double* tr, double t0,
+                           double dt) {
+    return guarded([&] {
+        sf::write_traces_csv(path, nt, np, std::vector<double>(tr, tr + nt * np), t0, dt);
+    });
+}
+
+// SparseFunction CSV pair: coords [np][ndim] + traces [nt][np] on a unit grid of `n` nodes
+int sfr_write_cloud_csv(const char* traces_path, const char* coords_path, int ndim, long n,
+                        long np, long nt, const double* coords, const double* tr,
+                        const double* times) {
+    return guarded([&] {
+        auto grid = std::make_shared<sf::Grid>(std::vector<long>(size_t(ndim), n),
+                                               std::vector<double>(size_t(ndim), 1.0),
+                                               std::vector<double>(size_t(ndim), 0.0));
+        auto s = sf::SparseFunction::create("s", grid, std::vector<double>(coords, coords + np * ndim), nt);
+        for (long t = 0; t < nt; ++t)
+            for (long p = 0; p < np; ++p) s->trace(t, p) = tr[t * np + p];
+        sf::write_traces_csv(traces_path, *s, std::vector<double>(times, times + nt));
+        sf::write_coords_csv(coords_path, *s);
     });
 }
 

@@ -7,7 +7,7 @@
 
 namespace sfb {
 
-constexpr int kTtiTXV = 16, kTtiTY = 16, kTtiNS = 3;
+constexpr int kTtiTXV = 16, kTtiTY = 16, kTtiNS = 4;
 
 struct TtiVariant {
     int K;

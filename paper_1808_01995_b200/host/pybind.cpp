@@ -4,6 +4,7 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include "sfb/gridio.hpp"
 #include "sfb/seismic_ops.hpp"
 
 namespace py = pybind11;
@@ -237,4 +238,27 @@ PYBIND11_MODULE(_sfb_host, m) {
           py::arg("true_m") = py::none());
 
     m.def("set_device", &set_device);
+
+    // wire formats (proj/include/sf/gridio.hpp, proj/include/sf/sparse.hpp:97-104)
+    m.def("write_grid", [](const std::string& path, std::vector<long> shape, const darray& data) {
+        write_grid(path, shape, flat(data));
+    });
+    m.def("read_grid", [](const std::string& path) {
+        GridData g = read_grid(path);
+        py::array_t<double> a(std::vector<py::ssize_t>(g.shape.begin(), g.shape.end()));
+        std::copy(g.data.begin(), g.data.end(), a.mutable_data());
+        return a;
+    });
+    m.def("write_traces_table", [](const std::string& path, const darray& tr, double t0, double dt) {
+        write_traces_csv(path, long(tr.shape(0)), long(tr.shape(1)), flat(tr), t0, dt);
+    });
+    m.def("write_traces_csv", [](const std::string& path, const SparseFunction& s,
+                                 std::vector<double> times) { write_traces_csv(path, s, times); });
+    m.def("read_traces_csv", [](const std::string& path, SparseFunction& s) {
+        std::vector<double> times;
+        read_traces_csv(path, s, &times);
+        return times;
+    });
+    m.def("write_coords_csv", &write_coords_csv);
+    m.def("read_coords_csv", &read_coords_csv);
 }
