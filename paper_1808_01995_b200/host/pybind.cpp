@@ -6,6 +6,7 @@
 
 #include "sfb/gridio.hpp"
 #include "sfb/seismic_ops.hpp"
+#include "sfb/verify.hpp"
 
 namespace py = pybind11;
 using namespace sfb;
@@ -238,6 +239,63 @@ PYBIND11_MODULE(_sfb_host, m) {
           py::arg("true_m") = py::none());
 
     m.def("set_device", &set_device);
+
+    // verification recipes (proj/include/sf/verify.hpp, proj/include/sf/slopefit.hpp)
+    py::class_<SlopeFit>(m, "SlopeFit")
+        .def_readonly("slope", &SlopeFit::slope)
+        .def_readonly("intercept", &SlopeFit::intercept)
+        .def_readonly("residual", &SlopeFit::residual);
+    m.def("fit_loglog", &fit_loglog);
+    py::class_<AdjointConfig>(m, "AdjointConfig")
+        .def(py::init<>())
+        .def_readwrite("ndim", &AdjointConfig::ndim)
+        .def_readwrite("n", &AdjointConfig::n)
+        .def_readwrite("space_order", &AdjointConfig::space_order)
+        .def_readwrite("h", &AdjointConfig::h)
+        .def_readwrite("nbl", &AdjointConfig::nbl)
+        .def_readwrite("tn", &AdjointConfig::tn)
+        .def_readwrite("f0", &AdjointConfig::f0);
+    py::class_<AdjointReport>(m, "AdjointReport")
+        .def_readonly("forward_dot", &AdjointReport::forward_dot)
+        .def_readonly("adjoint_dot", &AdjointReport::adjoint_dot)
+        .def_readonly("rel_err", &AdjointReport::rel_err);
+    m.def("adjoint_test", &adjoint_test, py::call_guard<py::gil_scoped_release>());
+    py::class_<GradientConfig>(m, "GradientConfig")
+        .def(py::init<>())
+        .def_readwrite("nx", &GradientConfig::nx)
+        .def_readwrite("nz", &GradientConfig::nz)
+        .def_readwrite("h", &GradientConfig::h)
+        .def_readwrite("space_order", &GradientConfig::space_order)
+        .def_readwrite("nbl", &GradientConfig::nbl)
+        .def_readwrite("tn", &GradientConfig::tn)
+        .def_readwrite("f0", &GradientConfig::f0)
+        .def_readwrite("steps", &GradientConfig::steps);
+    py::class_<GradientReport>(m, "GradientReport")
+        .def_readonly("phi0", &GradientReport::phi0)
+        .def_readonly("dphi", &GradientReport::dphi)
+        .def_readonly("steps", &GradientReport::steps)
+        .def_readonly("eps0", &GradientReport::eps0)
+        .def_readonly("eps1", &GradientReport::eps1)
+        .def_readonly("eps1_fitted", &GradientReport::eps1_fitted)
+        .def_readonly("fit0", &GradientReport::fit0)
+        .def_readonly("fit1", &GradientReport::fit1)
+        .def_readonly("fit1_valid", &GradientReport::fit1_valid);
+    m.def("gradient_test", &gradient_test, py::call_guard<py::gil_scoped_release>());
+    py::class_<BenchConfig>(m, "BenchConfig")
+        .def(py::init<>())
+        .def_readwrite("orders", &BenchConfig::orders)
+        .def_readwrite("n", &BenchConfig::n)
+        .def_readwrite("steps", &BenchConfig::steps)
+        .def_readwrite("wall_order", &BenchConfig::wall_order)
+        .def_readwrite("repeats", &BenchConfig::repeats);
+    py::class_<BenchReport>(m, "BenchReport")
+        .def_readonly("orders", &BenchReport::orders)
+        .def_readonly("oi", &BenchReport::oi)
+        .def_readonly("flops", &BenchReport::flops)
+        .def_readonly("wall_small", &BenchReport::wall_small)
+        .def_readonly("wall_big", &BenchReport::wall_big)
+        .def_readonly("wall_ratio", &BenchReport::wall_ratio);
+    m.def("bench", &bench, py::call_guard<py::gil_scoped_release>());
 
     // wire formats (proj/include/sf/gridio.hpp, proj/include/sf/sparse.hpp:97-104)
     m.def("write_grid", [](const std::string& path, std::vector<long> shape, const darray& data) {

@@ -186,3 +186,14 @@ def test_no_cpu_fallback_without_a_device():
     with pytest.raises(capi.SfbError) as e:
         capi.Plan([21, 21], [10.0, 10.0], 8, 1.0, 10)
     assert e.value.code == capi.ERR_CAPABILITY
+
+
+def test_loglog_fit():  # proj/tests/test_verify.cpp:13-28
+    x = [1.0, 2.0, 4.0, 8.0]
+    f = H.fit_loglog(x, [3.5 * v ** 2.25 for v in x])
+    assert f.slope == pytest.approx(2.25, rel=1e-12)
+    assert f.intercept == pytest.approx(np.log(3.5), rel=1e-12) and f.residual <= 1e-12
+    for bad in ([[1.0, 2.0], [1.0, 2.0]], [[1.0, 2.0, 2.0], [1.0, 2.0, 3.0]],
+                [[1.0, 2.0, 3.0], [1.0, -2.0, 3.0]], [[1.0, 3.0, 2.0], [1.0, 2.0, 3.0]]):
+        with pytest.raises(H.ParameterError):
+            H.fit_loglog(*bad)

@@ -190,3 +190,30 @@ def test_fwi_reduces_the_objective_with_parallel_shots():
     cfg.m_min, cfg.m_max = 1.0 / 2.5 ** 2, 1.0 / 1.2 ** 2
     res = H.fwi(m, shots, obs, cfg, m_true)
     assert len(res.objectives) == 4 and res.objectives[-1] < res.objectives[0]
+
+
+def test_verification_recipes():  # proj/tests/test_verify.cpp:68-93 and the gradient_test recipe
+    c = H.AdjointConfig()
+    c.ndim, c.n, c.space_order, c.tn = 3, 24, 6, 150.0
+    r = H.adjoint_test(c)
+    assert r.forward_dot > 0.0 and r.rel_err <= 1e-4
+    b = H.BenchConfig()
+    b.orders, b.n, b.steps, b.repeats = [2, 4, 8], 48, 40, 1
+    rb = H.bench(b)
+    assert len(rb.oi) == 3 and 0.0 < rb.oi[0] < rb.oi[1] < rb.oi[2] and rb.flops[0] < rb.flops[2]
+    assert rb.flops == [29.0, 38.0, 56.0]  # 3KD + 3D + 11 in 3-D
+    assert rb.wall_small > 0.0 and rb.wall_big > 0.0
+    g = H.GradientConfig()
+    g.nx, g.nz, g.nbl, g.tn = 41, 31, 16, 220.0
+    rg = H.gradient_test(g)
+    assert rg.phi0 > 0.0
+    assert rg.fit0.slope == pytest.approx(1.0, abs=0.1)        # PAPER.md:962 reports 1.06
+    assert rg.fit1_valid and rg.fit1.slope == pytest.approx(2.0, abs=0.15)  # and 2.01
+
+
+def test_verify_cli(capsys):
+    import json
+    from paper_1808_01995_b200 import verify
+    assert verify.main(["adjoint", "--ndim", "2", "--n", "48", "--order", "4", "--tn", "200"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    assert out["pass"] and out["forward_dot"] > 0
