@@ -183,6 +183,8 @@ SFB_API int sfb_step_compute(sfb_plan* plan, int op, int64_t t, int part);
  * planes are shipped; INTERIOR = the remaining nodes and the gather */
 SFB_API int sfb_step_points(sfb_plan* plan, int op, int64_t t, int part);
 SFB_API int sfb_step_end(sfb_plan* plan, int op);
+/* gradient accumulated by the last gradient sweep (owned planes only are written) */
+SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* grad);
 /* ghost / boundary plane blocks of the level written at step t of `op`:
  * send_lo/send_hi = owned boundary planes to ship, recv_lo/recv_hi = ghost planes to
  * fill; each is `*count` contiguous floats. */

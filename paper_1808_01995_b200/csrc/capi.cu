@@ -1432,6 +1432,16 @@ SFB_API int sfb_get_wavefield(sfb_plan* plan, int field, int64_t level, const sf
     });
 }
 
+SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* out) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        require(out && out->ptr, SFB_ERR_PARAMETER, "get_gradient: null view");
+        require(plan->grad.p != nullptr, SFB_ERR_BINDING, "no gradient sweep has run on this plan");
+        SFB_CUDA(cudaStreamSynchronize(plan->s_main));
+        download_field(*plan, plan->grad.as<float>(), out);
+    });
+}
+
 SFB_API int sfb_step_begin(sfb_plan* plan, int op, int64_t save_every) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {

@@ -192,38 +192,56 @@ def test_unstable_dt_and_nan_guard():
     plan2.close()
 
 
-def _run_slabs(model, geom, order, cuts, op_forward=True):
+def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_forward=False):
     """N plans on one device stepping in lockstep with device-to-device ghost copies:
-    the single-GPU emulation of the multi-GPU slab protocol."""
+    the single-GPU emulation of the multi-GPU slab protocol.  Returns the summed sampled
+    traces, the assembled last level and (gradient) the assembled grad."""
     from paper_1808_01995_b200 import capi
+    op = capi.OP_FORWARD if op is None else op
+    backward = op != capi.OP_FORWARD
     plans = [make_plan(model, geom, order, slab=(cuts[i], cuts[i + 1])) for i in range(len(cuts) - 1)]
-    op = capi.OP_FORWARD
-    for p in plans:
-        p.upload_traces(capi.CLOUD_SRC, geom.src)
-        p.step_begin(op)
-    for t in range(1, geom.nt - 1):
+
+    def sweep(o, traces_cloud, traces, se):
         for p in plans:
-            p.step_compute(op, t, capi.PART_LOW)
-            p.step_compute(op, t, capi.PART_HIGH)
-            p.step_points(op, t, capi.PART_LOW)
-            p.step_compute(op, t, capi.PART_INTERIOR)
-            p.step_points(op, t, capi.PART_INTERIOR)
+            p.upload_traces(traces_cloud, traces)
+            p.step_begin(o, se)
+        ts = range(geom.nt - 2, 0, -1) if o != capi.OP_FORWARD else range(1, geom.nt - 1)
+        for t in ts:
+            for p in plans:
+                p.step_compute(o, t, capi.PART_LOW)
+                p.step_compute(o, t, capi.PART_HIGH)
+                p.step_points(o, t, capi.PART_LOW)
+                p.step_compute(o, t, capi.PART_INTERIOR)
+                p.step_points(o, t, capi.PART_INTERIOR)
+            for p in plans:
+                p.sync()
+            for i in range(len(plans) - 1):
+                a, b = plans[i].halo_blocks(o, t), plans[i + 1].halo_blocks(o, t)
+                plans[i + 1].copy_halo(b["recv_lo"], a["send_hi"], a["count"])
+                plans[i].copy_halo(a["recv_hi"], b["send_lo"], a["count"])
+            for p in plans:
+                p.sync()
         for p in plans:
-            p.sync()
-        for i in range(len(plans) - 1):
-            a, b = plans[i].halo_blocks(op, t), plans[i + 1].halo_blocks(op, t)
-            plans[i + 1].copy_halo(b["recv_lo"], a["send_hi"], a["count"])
-            plans[i].copy_halo(a["recv_hi"], b["send_lo"], a["count"])
-        for p in plans:
-            p.sync()
-    rec = np.zeros((geom.nt, geom.n_rec))
+            p.step_end(o)
+
+    if prior_forward:  # the gradient sweep images against each slab's own saved history
+        sweep(capi.OP_FORWARD, capi.CLOUD_SRC, geom.src, save_every)
+    sweep(op, capi.CLOUD_REC if backward else capi.CLOUD_SRC, geom.src if inj is None else inj,
+          save_every)
+    smp_cloud = capi.CLOUD_SRC if backward else capi.CLOUD_REC
+    n_smp = geom.n_src if backward else geom.n_rec
+    rec = np.zeros((geom.nt, n_smp))
     u = np.zeros(model.N)
+    grad = np.zeros(model.N)
     for p in plans:
-        p.step_end(op)
-        rec += p.download_traces(capi.CLOUD_REC)
-        p.wavefield(geom.nt - 1, out=u)
+        if op != capi.OP_GRADIENT:
+            rec += p.download_traces(smp_cloud)
+        p.wavefield(0 if backward else geom.nt - 1, out=u)
+        if op == capi.OP_GRADIENT:
+            import ctypes as C
+            p._chk(capi.lib.sfb_get_gradient(p.h, C.byref(capi._view(grad))))
         p.close()
-    return rec, u
+    return rec, u, grad
 
 
 def test_slab_decomposition_matches_single_domain_bitwise():
@@ -233,8 +251,27 @@ def test_slab_decomposition_matches_single_domain_bitwise():
     u1 = plan.wavefield(geom.nt - 1)
     plan.close()
     n0 = model.N[0]
-    rec3, u3 = _run_slabs(model, geom, 8, [0, 20, 41, n0])
+    rec3, u3, _ = _run_slabs(model, geom, 8, [0, 20, 41, n0])
     assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
+
+
+def test_slab_decomposition_adjoint_and_gradient_bitwise():
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([48, 30, 34], 10.0, 8, 8, 40)
+    rng = np.random.default_rng(9)
+    data = rng.standard_normal((geom.nt, geom.n_rec)) * np.hanning(geom.nt)[:, None]
+    plan = make_plan(model, geom, 8)
+    srca1, _ = plan.adjoint(data)
+    v1 = plan.wavefield(0)
+    plan.forward(geom.src, save_every=2)
+    g1, _ = plan.gradient(data)
+    plan.close()
+    n0 = model.N[0]
+    srca3, v3, _ = _run_slabs(model, geom, 8, [0, 20, 41, n0], op=capi.OP_ADJOINT, inj=data)
+    assert np.array_equal(srca3, srca1) and np.array_equal(v3, v1)
+    _, _, g3 = _run_slabs(model, geom, 8, [0, 20, 41, n0], op=capi.OP_GRADIENT, save_every=2,
+                          inj=data, prior_forward=True)
+    assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
 
 
 def test_step_loop_engine_on_one_rank_matches_forward():
