@@ -124,6 +124,10 @@ struct FwiConfig {
     double m_min = 0, m_max = 0;
     Backend backend = Backend::Auto;
     int nthreads = 1;  // shots in flight at once (one engine each)
+    // extension: CUDA ordinals the shots are dealt to round-robin (empty = the calling
+    // thread's device).  Shot gradients are still reduced in shot order on the host, so the
+    // result does not depend on the device list.
+    std::vector<int> devices;
 };
 
 struct FwiResult {

@@ -331,7 +331,7 @@ FwiResult fwi(SeismicModel& model, std::vector<AcquisitionGeometry>& shots,
             std::vector<std::thread> pool;
             for (std::size_t s = lo; s < hi; ++s)
                 pool.emplace_back([&, s] {
-                    set_device(dev);
+                    set_device(cfg.devices.empty() ? dev : cfg.devices[s % cfg.devices.size()]);
                     try {
                         parts[s] = fwi_gradient(model, shots[s], observed[s], cfg.space_order,
                                                 cfg.backend);

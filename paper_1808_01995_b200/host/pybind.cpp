@@ -217,7 +217,8 @@ PYBIND11_MODULE(_sfb_host, m) {
         .def_readwrite("step_scale", &FwiConfig::step_scale)
         .def_readwrite("m_min", &FwiConfig::m_min)
         .def_readwrite("m_max", &FwiConfig::m_max)
-        .def_readwrite("nthreads", &FwiConfig::nthreads);
+        .def_readwrite("nthreads", &FwiConfig::nthreads)
+        .def_readwrite("devices", &FwiConfig::devices);
     py::class_<FwiResult>(m, "FwiResult")
         .def_readonly("objectives", &FwiResult::objectives)
         .def_readonly("model_rms", &FwiResult::model_rms)
