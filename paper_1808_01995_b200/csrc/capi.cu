@@ -148,8 +148,10 @@ void select_variant(Plan& P, int txv, int ty, int nst, int dual = -1) {
     SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, best->func, best->nthreads,
                                                            best->smem));
     if (bps < 1) bps = 1;
-    // split d0 into chunks so the grid fills whole waves; every chunk re-reads 2K planes
-    // of u[t] (4 of the 20 bytes per node), which the score charges
+    // split d0 into chunks so the grid fills whole waves; every chunk spends 2K extra
+    // iterations filling its register queue (re-reading 2K planes of u[t]), which the score
+    // charges at half an output plane each (measured on the 208-plane order-16 slab of
+    // config 5: tools/run_config5.py)
     const long long tiles = ((P.N[2] + best->tile_x - 1) / best->tile_x) *
                             ((P.N[1] + best->tile_y - 1) / best->tile_y);
     const long long slots = (long long)P.sm_count * bps;
@@ -162,7 +164,7 @@ void select_variant(Plan& P, int txv, int ty, int nst, int dual = -1) {
         const long long total = tiles * real;
         const long long waves = (total + slots - 1) / slots;
         const double fill = double(total) / double(waves * slots);
-        const double extra = 1.0 + (2.0 * P.K / chunk) * 0.2;
+        const double extra = 1.0 + (2.0 * P.K / chunk) * 0.5;
         const double score = fill / extra;
         if (score > best_score + 1e-9) {
             best_score = score;

@@ -64,7 +64,11 @@ point_step_kernel(const __grid_constant__ PointParams p, int nb_inj) {
         float s = 0.f;
         if (b >= 0) {
             const float* w = p.smp_w + (long long)i * p.ncorner;
-            for (int c = 0; c < p.ncorner; ++c) s = fmaf(w[c], p.field[b + p.corner_off[c]], s);
+            // corners with zero weight (points on lattice lines) are not fetched
+            for (int c = 0; c < p.ncorner; ++c) {
+                const float wc = w[c];
+                if (wc != 0.f) s = fmaf(wc, p.field[b + p.corner_off[c]], s);
+            }
         }
         p.smp_row[i] = s;
     }
