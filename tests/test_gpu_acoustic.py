@@ -315,3 +315,48 @@ def test_streamed_traces_with_many_receivers():
     plan.run_resident(capi.OP_FORWARD)
     assert np.array_equal(plan.download_traces(capi.CLOUD_REC), got)
     plan.close()
+
+
+def test_forward_parity_1d_and_tiny_grids():
+    # rank-1 grids (the reference's Grid allows ranks 1-3, proj/include/sf/grid.hpp:34-35)
+    _, _, ref, plan, rec, u, _, _ = _forward_both([60], 10.0, 12, 4, 90)
+    assert np.abs(ref["smp"]).max() > 0
+    assert rel_l2(rec, ref["smp"]) <= 1e-5 and rel_l2(u, ref["final"]) <= 1e-5
+    plan.close()
+    # grids smaller than one tile and than the stencil radius
+    for shape, order in (([3, 2, 4], 2), ([2, 2], 2), ([5, 4, 3], 8), ([2], 16)):
+        nd = len(shape)
+        src = [0.3 * 10.0 * (s - 1) for s in shape]
+        rec_c = [[0.0] * nd, [10.0 * (s - 1) for s in shape]]
+        _, _, ref, plan, rec, u, _, _ = _forward_both(shape, 10.0, 1, order, 25, src=src, rec=rec_c)
+        assert np.abs(ref["final"]).max() > 0
+        assert rel_l2(rec, ref["smp"]) <= 1e-5 and rel_l2(u, ref["final"]) <= 1e-5
+        plan.close()
+
+
+def test_concurrent_plans_from_two_threads():
+    """the C-ABI is re-entrant per plan (proj/tests/test_compiler.cpp:559-578 runs distinct
+    operators concurrently; fwi calls fwi_gradient from several threads)"""
+    import threading
+    probs = [make_problem([30, 26, 34], 10.0, 8, 8, 60), make_problem([28, 32, 24], 12.5, 6, 4, 70)]
+    orders = [8, 4]
+    serial = []
+    for (m, g), k in zip(probs, orders):
+        p = make_plan(m, g, k)
+        serial.append(p.forward(g.src)[0])
+        p.close()
+    out = [None, None]
+
+    def work(i):
+        m, g = probs[i]
+        p = make_plan(m, g, orders[i])
+        for _ in range(3):
+            out[i] = p.forward(g.src)[0]
+        p.close()
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert np.array_equal(out[0], serial[0]) and np.array_equal(out[1], serial[1])
