@@ -217,3 +217,16 @@ def test_verify_cli(capsys):
     assert verify.main(["adjoint", "--ndim", "2", "--n", "48", "--order", "4", "--tn", "200"]) == 0
     out = json.loads(capsys.readouterr().out)
     assert out["pass"] and out["forward_dot"] > 0
+
+
+def test_cpp_dropin_program():
+    """tests/cpp/test_seismic_dropin.cpp: the reference's own integration tests in C++,
+    compiled against include/sfb/*.hpp with `namespace sf = sfb;` (built by build())."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build",
+                       "test_seismic_dropin")
+    assert os.path.exists(exe), "run __graft_entry__.build() first"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
