@@ -951,9 +951,10 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
     if (rep) {
         const long steps = long(std::max<long long>(0, nt - 2));
         const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
-        // per node: 2 fields x (3 first derivatives + rotation) + 2 x divergence of 3 products
-        // + Laplacian + 2 updates, adds and multiplies counted as the reference counts them
-        const long long fpp = 2LL * (6 * P.K + 5) + 2LL * (12 * P.K) + (9LL * P.K + 3) + 24;
+        // adds + multiplies per node, counted as the reference counts its operators
+        // (proj/src/passes.cpp:318-327), D = 3: g(p), g(r): 2 (9K + 2); Hz(p), Hz(r):
+        // 2 (15K - 1); L(p): 9K + 3; right-hand sides and the two leapfrog updates: 24
+        const long long fpp = 57LL * P.K + 29;
         rep->seconds = ms * 1e-3;
         rep->steps = steps;
         rep->flops = (long long)(double(fpp) * own * steps);
