@@ -182,6 +182,10 @@ SFB_API int sfb_step_compute(sfb_plan* plan, int op, int64_t t, int part);
  * both boundary plane groups, on the boundary stream, so they are in place before the
  * planes are shipped; INTERIOR = the remaining nodes and the gather */
 SFB_API int sfb_step_points(sfb_plan* plan, int op, int64_t t, int part);
+/* the two halves of one slab step as single calls: boundary = compute LOW, compute HIGH,
+ * points LOW (boundary stream); interior = compute INTERIOR, points INTERIOR (main stream) */
+SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t);
+SFB_API int sfb_step_slab_interior(sfb_plan* plan, int op, int64_t t);
 SFB_API int sfb_step_end(sfb_plan* plan, int op);
 /* gradient accumulated by the last gradient sweep (owned planes only are written) */
 SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* grad);

@@ -45,7 +45,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_end", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune",
 ]
@@ -71,6 +71,8 @@ lib.sfb_step_begin.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_step_compute.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
 lib.sfb_step_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
 lib.sfb_step_end.argtypes = [C.c_void_p, C.c_int]
+lib.sfb_step_slab_boundary.argtypes = [C.c_void_p, C.c_int, C.c_int64]
+lib.sfb_step_slab_interior.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_get_gradient.argtypes = [C.c_void_p, C.POINTER(FieldView)]
 lib.sfb_halo_blocks.argtypes = [C.c_void_p, C.c_int, C.c_int64] + [C.POINTER(C.c_void_p)] * 4 + [C.POINTER(C.c_int64)]
 lib.sfb_stream_sync.argtypes = [C.c_void_p]
@@ -269,6 +271,12 @@ class Plan:
 
     def step_points(self, op, t, part):
         self._chk(lib.sfb_step_points(self.h, op, t, part))
+
+    def step_slab_boundary(self, op, t):
+        self._chk(lib.sfb_step_slab_boundary(self.h, op, t))
+
+    def step_slab_interior(self, op, t):
+        self._chk(lib.sfb_step_slab_interior(self.h, op, t))
 
     def step_end(self, op):
         self._chk(lib.sfb_step_end(self.h, op))

@@ -1463,6 +1463,23 @@ SFB_API int sfb_step_points(sfb_plan* plan, int op, int64_t t, int part) {
     return guarded(plan, [&] { step_points(*plan, op, t, part); });
 }
 
+SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        step_compute(*plan, op, t, SFB_PART_LOW);
+        step_compute(*plan, op, t, SFB_PART_HIGH);
+        step_points(*plan, op, t, SFB_PART_LOW);
+    });
+}
+
+SFB_API int sfb_step_slab_interior(sfb_plan* plan, int op, int64_t t) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        step_compute(*plan, op, t, SFB_PART_INTERIOR);
+        step_points(*plan, op, t, SFB_PART_INTERIOR);
+    });
+}
+
 SFB_API int sfb_step_end(sfb_plan* plan, int op) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {

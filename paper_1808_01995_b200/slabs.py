@@ -92,16 +92,23 @@ def step_loop(engine, exchanger: HaloExchanger, t_from: int, t_to: int, backward
     gather(t), blocks(t) -> (send_lo, send_hi, recv_lo, recv_hi), and the context managers
     boundary() / interior() that select where the work is queued."""
     steps = range(t_to - 1, t_from - 1, -1) if backward else range(t_from, t_to)
+    fused = hasattr(engine, "boundary_step")  # one native call per half step
     for t in steps:
         with engine.boundary():
-            engine.update("low", t)
-            engine.update("high", t)
-            engine.scatter("boundary", t)
+            if fused:
+                engine.boundary_step(t)
+            else:
+                engine.update("low", t)
+                engine.update("high", t)
+                engine.scatter("boundary", t)
             reqs = exchanger.start(*engine.blocks(t))
         with engine.interior():
-            engine.update("interior", t)
-            engine.scatter("interior", t)
-            engine.gather(t)
+            if fused:
+                engine.interior_step(t)
+            else:
+                engine.update("interior", t)
+                engine.scatter("interior", t)
+                engine.gather(t)
         with engine.boundary():
             exchanger.finish(reqs)
 
@@ -144,6 +151,12 @@ class PlanEngine:
 
     def gather(self, t):
         pass  # fused into the interior point launch
+
+    def boundary_step(self, t):
+        self.plan.step_slab_boundary(self.op, t)
+
+    def interior_step(self, t):
+        self.plan.step_slab_interior(self.op, t)
 
     def blocks(self, t):
         key = (t + 1) & 1
