@@ -179,6 +179,12 @@ def bench_distributed(args, K, W, build_workload, workload_config, bytes_per_poi
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
+    # NCCL prints its version banner on stdout; the contract is ONE JSON line there, so
+    # stdout is parked on stderr until the line is ready
+    import sys
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29577")
     dist.init_process_group("nccl", rank=rank, world_size=world,
@@ -217,6 +223,9 @@ def bench_distributed(args, K, W, build_workload, workload_config, bytes_per_poi
     plan.step_end(capi.OP_FORWARD)
     pts = float(np.prod(N))
     sec = float(ms.item()) * 1e-3
+    sys.stdout.flush()
+    os.dup2(saved_stdout, 1)
+    os.close(saved_stdout)
     if rank == 0:
         peak, kind = peaks()
         line = {
