@@ -187,6 +187,11 @@ SFB_API int sfb_step_points(sfb_plan* plan, int op, int64_t t, int part);
 SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t);
 SFB_API int sfb_step_slab_interior(sfb_plan* plan, int op, int64_t t);
 SFB_API int sfb_step_end(sfb_plan* plan, int op);
+/* binds one level of a forward history that lives in host memory (the reference's saved
+ * TimeFunction, proj/src/seismic_ops.cpp:113-114) as saved level `level` for sfb_gradient;
+ * levels that are never put stay zero */
+SFB_API int sfb_put_history(sfb_plan* plan, int64_t save_every, int64_t level,
+                            const sfb_field_view* u);
 /* gradient accumulated by the last gradient sweep (owned planes only are written) */
 SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* grad);
 /* ghost / boundary plane blocks of the level written at step t of `op`:

@@ -45,7 +45,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune",
 ]
@@ -73,6 +73,7 @@ lib.sfb_step_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
 lib.sfb_step_end.argtypes = [C.c_void_p, C.c_int]
 lib.sfb_step_slab_boundary.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_step_slab_interior.argtypes = [C.c_void_p, C.c_int, C.c_int64]
+lib.sfb_put_history.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(FieldView)]
 lib.sfb_get_gradient.argtypes = [C.c_void_p, C.POINTER(FieldView)]
 lib.sfb_halo_blocks.argtypes = [C.c_void_p, C.c_int, C.c_int64] + [C.POINTER(C.c_void_p)] * 4 + [C.POINTER(C.c_int64)]
 lib.sfb_stream_sync.argtypes = [C.c_void_p]

@@ -1435,6 +1435,32 @@ SFB_API int sfb_get_wavefield(sfb_plan* plan, int field, int64_t level, const sf
     });
 }
 
+SFB_API int sfb_put_history(sfb_plan* plan, int64_t save_every, int64_t level,
+                            const sfb_field_view* u) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(u && u->ptr && save_every >= 1, SFB_ERR_PARAMETER, "put_history: bad argument");
+        require(level >= 0 && level < P.desc.nt && level % save_every == 0, SFB_ERR_PARAMETER,
+                "put_history: level is not a saved level");
+        const long long nslots = (P.desc.nt - 1) / save_every + 1;
+        if (P.save_every != save_every || P.nslots != nslots || !P.snaps.p) {
+            P.save_every = save_every;
+            P.nslots = nslots;
+            P.snaps.alloc(size_t(nslots) * P.ccount * 4, true);
+        }
+        DevBuf tmp;
+        upload_f64(P, embed_view(P, u->ptr, u->stride), tmp);
+        const long long rows = (long long)P.n0 * P.N[1];
+        convert_f64_f32_pitched<<<row_grid(P, rows), 256, 0, P.s_main>>>(
+            tmp.as<double>(), P.snaps.as<float>() + (level / save_every) * P.ccount, rows,
+            int(P.N[2]), P.pitch);
+        SFB_CUDA(cudaGetLastError());
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        P.history_valid = true;
+    });
+}
+
 SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* out) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {

@@ -163,9 +163,7 @@ GradientOp gradient_operator(const SeismicModel& model, const AcquisitionGeometr
     check_cfl(model, geom, space_order);
     if (!saved_u || saved_u->time_buffered() || saved_u->time_slots() != geom.nt())
         throw ParameterError("gradient_operator: saved forward history required");
-    if (!saved_u->device_history)
-        throw ParameterError("gradient_operator: saved forward history required "
-                             "(run the saving forward operator first: the history lives in HBM)");
+
     GradientOp g;
     g.dt = geom.dt();
     g.nt = geom.nt();
@@ -174,8 +172,21 @@ GradientOp gradient_operator(const SeismicModel& model, const AcquisitionGeometr
     g.resid->locate();
     g.v = TimeFunction::create("v", model.grid(), space_order, 2);
     g.grad = Function::create("grad", model.grid(), space_order);
-    // the forward operator's engine holds the history, the model and both clouds
-    g.engine = std::static_pointer_cast<Engine>(saved_u->device_history);
+    if (saved_u->device_history) {
+        // the forward operator's engine holds the history, the model and both clouds
+        g.engine = std::static_pointer_cast<Engine>(saved_u->device_history);
+    } else {
+        // a history that exists in host memory only (filled by the caller, or produced by
+        // another engine): bind every level, as the reference reads u_saved[t] from RAM
+        g.engine = std::make_shared<Engine>(model, geom, space_order);
+        for (long t = 0; t < geom.nt(); ++t) {
+            sfb_field_mview mv = Engine::mview(*saved_u, t);
+            sfb_field_view v{};
+            v.ptr = mv.ptr;
+            for (int a = 0; a < 3; ++a) v.stride[a] = mv.stride[a];
+            g.engine->check(sfb_put_history(g.engine->plan(), 1, t, &v));
+        }
+    }
     return g;
 }
 

@@ -120,7 +120,10 @@ def test_gradient_operator_needs_saved_history():  # seismic_ops.cpp:113-114
     fwd = H.forward_operator(m, g, 8)
     H.run_wave(fwd)
     with pytest.raises(H.ParameterError):
-        H.gradient_operator(m, g, 8, fwd.wavefield)
+        H.gradient_operator(m, g, 8, fwd.wavefield)          # buffered, not saved
+    short = H.TimeFunction.create("u", m.grid, 8, 2, g.nt - 1)
+    with pytest.raises(H.ParameterError):
+        H.gradient_operator(m, g, 8, short)                   # wrong slot count
 
 
 def test_explicit_gradient_operator_path():  # the three-call sequence of fwi_gradient
@@ -137,6 +140,26 @@ def test_explicit_gradient_operator_path():  # the three-call sequence of fwi_gr
     r = o.forward(om, og, 8, save_every=1)
     gref = o.gradient_sweep(om, og, 8, og.rec * 0.5, r["snaps"], 1)
     assert rel_l2(gop.grad.array(), gref) <= 1e-3
+
+
+def test_gradient_operator_with_a_host_only_history():
+    """a saved wavefield that lives in host memory only (no engine attached) is uploaded
+    level by level, as the reference reads u_saved[t] from RAM"""
+    m = constant_model(21, 10.0, 1.5, 6)
+    g = H.AcquisitionGeometry(m, [100.0, 20.0], [40.0, 40.0, 160.0, 40.0], 0.0, 120.0,
+                              0.8 * m.critical_dt(), 0.01)
+    fwd = H.forward_operator(m, g, 8, True)
+    H.run_wave(fwd)
+    gop = H.gradient_operator(m, g, 8, fwd.wavefield)           # history in HBM
+    gop.resid.traces[:] = g.rec.traces * 0.5
+    H.run_gradient(gop)
+    want = gop.grad.array().copy()
+    host_u = H.TimeFunction.create("u", m.grid, 8, 2, g.nt)      # a plain host copy
+    host_u.array()[:] = fwd.wavefield.array()
+    gop2 = H.gradient_operator(m, g, 8, host_u)
+    gop2.resid.traces[:] = g.rec.traces * 0.5
+    H.run_gradient(gop2)
+    assert np.abs(want).max() > 0 and np.array_equal(gop2.grad.array(), want)
 
 
 def _observed_for(m, shot):
