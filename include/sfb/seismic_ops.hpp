@@ -45,6 +45,10 @@ struct WaveOp {
     // into `wavefield` as the reference does (proj/src/seismic_ops.cpp:66-68).
     long save_every = 0;
     bool host_history = true;
+    // with save: keep only the state at every checkpoint_every-th level (>= 2) and let the
+    // gradient sweep recompute the levels in between (imaging at every level, the
+    // reference's condition, without nt levels of memory).  No host mirror in this mode.
+    long checkpoint_every = 0;
     // TTI operator only: the auxiliary field r of the coupled pair (wavefield holds p)
     bool tti = false;
     std::shared_ptr<TimeFunction> wavefield_r;
@@ -111,10 +115,13 @@ struct GradientResult {
 };
 
 // proj/src/seismic_ops.cpp:197-216.  save_every is an extension (1 = reference): image
-// against every save_every-th forward level only, which divides the HBM the history needs.
+// against every save_every-th forward level only, which divides the HBM the history needs;
+// checkpoint_every >= 2 instead keeps the exact imaging condition and recomputes the history
+// segment by segment from sparse checkpoints (one extra forward pass).
 GradientResult fwi_gradient(const SeismicModel& model, AcquisitionGeometry& geom,
                             const std::vector<double>& observed, int space_order,
-                            Backend backend = Backend::Auto, long save_every = 1);
+                            Backend backend = Backend::Auto, long save_every = 1,
+                            long checkpoint_every = 0);
 
 // proj/include/sf/seismic_ops.hpp:75-97, proj/src/seismic_ops.cpp:218-286
 struct FwiConfig {
@@ -128,6 +135,8 @@ struct FwiConfig {
     // thread's device).  Shot gradients are still reduced in shot order on the host, so the
     // result does not depend on the device list.
     std::vector<int> devices;
+    // extension: memory strategy of every shot gradient (see fwi_gradient)
+    long save_every = 1, checkpoint_every = 0;
 };
 
 struct FwiResult {

@@ -140,6 +140,12 @@ SFB_API int sfb_locate(const sfb_plan_desc* desc, const double* origin, int64_t 
  * (save_every = 1 is the reference's save=true). */
 SFB_API int sfb_forward(sfb_plan* plan, const double* src, double* rec, int64_t save_every,
                 sfb_report* report);
+/* the same forward run keeping only the state at every checkpoint_every-th level (>= 2);
+ * sfb_gradient then recomputes the history one segment at a time and images against EVERY
+ * level (the reference's exact imaging condition) without holding nt levels: the memory
+ * strategy the reference leaves out of scope */
+SFB_API int sfb_forward_checkpointed(sfb_plan* plan, const double* src, double* rec,
+                                     int64_t checkpoint_every, sfb_report* report);
 /* adjoint_operator + run_wave (seismic_ops.cpp:84-107): rec [nt][n_rec] in, srca
  * [nt][n_src] out. */
 SFB_API int sfb_adjoint(sfb_plan* plan, const double* rec, double* srca, sfb_report* report);

@@ -42,7 +42,7 @@ class Report(C.Structure):
 SYMBOLS = [
     "sfb_abi_version", "sfb_last_error", "sfb_device_count", "sfb_plan_create",
     "sfb_plan_destroy", "sfb_fd_weights", "sfb_critical_dt", "sfb_set_model",
-    "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_adjoint",
+    "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
     "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
@@ -59,6 +59,7 @@ lib.sfb_set_model_tti.argtypes = [C.c_void_p] + [C.POINTER(FieldView)] * 4
 lib.sfb_tti_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Report)]
 lib.sfb_set_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
 lib.sfb_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Report)]
+lib.sfb_forward_checkpointed.argtypes = lib.sfb_forward.argtypes
 lib.sfb_adjoint.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Report)]
 lib.sfb_gradient.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(FieldView), C.POINTER(Report)]
 lib.sfb_get_wavefield.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.POINTER(FieldView)]
@@ -198,6 +199,14 @@ class Plan:
         rec = np.empty((self.nt, self.np[CLOUD_REC]))
         rep = Report()
         self._chk(lib.sfb_forward(self.h, src.ctypes.data, rec.ctypes.data, save_every, C.byref(rep)))
+        return rec, rep
+
+    def forward_checkpointed(self, src, checkpoint_every):
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        rec = np.empty((self.nt, self.np[CLOUD_REC]))
+        rep = Report()
+        self._chk(lib.sfb_forward_checkpointed(self.h, src.ctypes.data, rec.ctypes.data,
+                                               checkpoint_every, C.byref(rep)))
         return rec, rep
 
     def adjoint(self, rec):

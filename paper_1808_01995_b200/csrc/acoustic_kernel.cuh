@@ -85,8 +85,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// Consumer release of a pipeline stage.  An mbarrier.arrive does NOT wait for earlier
+// shared-memory loads of the warp that are still in flight (ptxas puts no scoreboard wait on
+// it), and on B200 the producer's next TMA write was observed to overtake such a load: rows
+// of a stage read one pipeline round too new, a run-to-run difference under load
+// (tools/probe_determinism4.py).  So every release carries a register dependency on data the
+// iteration loaded: `dep` must derive from every shared-memory load instruction of the
+// iteration; it is masked with an opaque zero (blockDim.z - 1) into the barrier address.
+__device__ __forceinline__ void mbar_release(uint64_t* bar, float dep) {
+    const uint32_t zero = blockDim.z - 1u;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                     smem_u32(bar) + (__float_as_uint(dep) & zero))
+                 : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar), ok;
@@ -237,9 +247,6 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
         constexpr int QC = (K + ROT) % (2 * K + 1);  // physical slot of the centre plane
         float acc[4];
         stencil_acc<K, KP, SW, ROT>(p.k, q, cp, tx, ty, acc);
-        // all shared-memory reads of this iteration are done
-        __syncwarp();
-        if (lane0) mbar_arrive(done_bar);
 
         const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
         const float ov[4] = {o4.x, o4.y, o4.z, o4.w};
@@ -275,6 +282,10 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
             un[2] = n23.x;
             un[3] = n23.y;
         }
+        // un[0] depends on every shared-memory load of this iteration (queue feed, centre
+        // box row and columns, aux boxes): the stage may be refilled once it is known
+        __syncwarp();
+        if (lane0) mbar_release(done_bar, un[0]);
         if (rin) {
             __stcs(reinterpret_cast<float4*>(po), make_float4(un[0], un[1], un[2], un[3]));
             if (p.snap)
@@ -417,7 +428,7 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
         q[Q - 1][2] = v.z;
         q[Q - 1][3] = v.w;
         __syncwarp();
-        if (lane0) mbar_arrive(done + (n % NAUX));
+        if (lane0) mbar_release(done + (n % NAUX), v.x);
         if (++s == NST) {
             s = 0;
             fph ^= 1;
@@ -618,7 +629,7 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
         }
         if (n < 2 * K) {
             __syncwarp();
-            if (lane0) mbar_arrive(done + s);
+            if (lane0) mbar_release(done + s, q[(Q - 1 + R) % Q][0]);
         } else {
             const float* ap = st + ABOX + CPAD + aown;
             const float4 o4 = *reinterpret_cast<const float4*>(ap);

@@ -107,6 +107,13 @@ void make_tensor_maps(Plan& P) {
         encode_map(&P.tm_o[b], P.u[b].p, P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
                    v.tile_x, v.tile_y);
     }
+    for (int b = 0; b < 2; ++b) {
+        if (!P.f[b].p) continue;
+        encode_map(&P.tm_fu[b], P.f[b].p, P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
+                   v.box_w, v.box_h);
+        encode_map(&P.tm_fo[b], P.f[b].p, P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
+                   v.tile_x, v.tile_y);
+    }
     if (P.r.p)
         encode_map(&P.tm_r, P.r.p, P.N[2], P.N[1], P.n0, P.pitch, P.plane, v.tile_x, v.tile_y);
     if (P.damp.p)
@@ -530,6 +537,7 @@ void step_begin(Plan& P, int op, long long save_every) {
     }
     if (op == SFB_OP_FORWARD) {
         P.history_valid = false;
+        P.ckpt_valid = false;
         P.save_every = save_every;
         if (save_every > 0) {
             P.nslots = (P.desc.nt - 1) / save_every + 1;
@@ -586,7 +594,15 @@ void mark_stream(Plan& P, int part) {
     }
 }
 
-void step_compute(Plan& P, int op, long long t, int part) {
+// explicit fused outputs / buffer set of one step (checkpointed runs); without it the
+// save_every rules of the plain runs apply
+struct StepExtras {
+    bool alt = false;            // step the recompute pair f[2] instead of u[2]
+    float* snap = nullptr;       // copy of the new level
+    const float* usave = nullptr;  // forward level to image against
+};
+
+void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex = nullptr) {
     const OpRoles ro = roles(op);
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;
@@ -599,7 +615,7 @@ void step_compute(Plan& P, int op, long long t, int part) {
     sp.dz = P.dz.as<float>();
     sp.dy = P.dy.as<float>();
     sp.dx = P.dx.as<float>();
-    sp.uo = P.u[oth].as<float>();
+    sp.uo = (ex && ex->alt) ? P.f[oth].as<float>() : P.u[oth].as<float>();
     sp.N1 = int(P.N[1]);
     sp.N2 = int(P.N[2]);
     sp.pitch = P.pitch;
@@ -607,11 +623,17 @@ void step_compute(Plan& P, int op, long long t, int part) {
     sp.z_lo = lo;
     sp.z_hi = hi;
     sp.chunk = (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? P.chunk : (hi - lo);
-    if (op == SFB_OP_FORWARD && P.save_every > 0 && tnew % P.save_every == 0)
-        sp.snap = P.snaps.as<float>() + (tnew / P.save_every) * P.ccount;
-    if (ro.imaging && t % P.save_every == 0) {
-        sp.usave = P.snaps.as<float>() + (t / P.save_every) * P.ccount;
-        sp.grad = P.grad.as<float>();
+    if (ex) {
+        sp.snap = ex->snap;
+        sp.usave = ex->usave;
+        if (ex->usave) sp.grad = P.grad.as<float>();
+    } else {
+        if (op == SFB_OP_FORWARD && P.save_every > 0 && tnew % P.save_every == 0)
+            sp.snap = P.snaps.as<float>() + (tnew / P.save_every) * P.ccount;
+        if (ro.imaging && t % P.save_every == 0) {
+            sp.usave = P.snaps.as<float>() + (t / P.save_every) * P.ccount;
+            sp.grad = P.grad.as<float>();
+        }
     }
     const StepVariant& v = *P.variant;
     dim3 grid(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x),
@@ -619,15 +641,16 @@ void step_compute(Plan& P, int op, long long t, int part) {
               unsigned((hi - lo + sp.chunk - 1) / sp.chunk));
     cudaStream_t st = part_stream(P, part);
     StepMaps maps;
-    maps.u = P.tm_u[cur];
-    maps.f = P.tm_o[cur];
-    maps.o = P.tm_o[oth];
+    const bool alt = ex && ex->alt;
+    maps.u = alt ? P.tm_fu[cur] : P.tm_u[cur];
+    maps.f = alt ? P.tm_fo[cur] : P.tm_o[cur];
+    maps.o = alt ? P.tm_fo[oth] : P.tm_o[oth];
     maps.r = P.tm_r;
     maps.d = P.sep ? P.tm_r : P.tm_d;
     SFB_CUDA(v.launch(maps, sp, grid, st));
     ++P.launches;
     mark_stream(P, part);
-    if (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) {
+    if (!alt && (part == SFB_PART_ALL || part == SFB_PART_INTERIOR)) {
         P.live_level[cur] = t;
         P.live_level[oth] = tnew;
     }
@@ -636,7 +659,7 @@ void step_compute(Plan& P, int op, long long t, int part) {
 // part: SFB_PART_ALL = every node + gather; SFB_PART_LOW = nodes of both boundary plane
 // groups (boundary stream); SFB_PART_INTERIOR = remaining nodes + gather
 void step_points(Plan& P, int op, long long t, int part, float* target_override = nullptr,
-                 bool allow_gather = true) {
+                 bool allow_gather = true, const StepExtras* ex = nullptr) {
     const OpRoles ro = roles(op);
     const int cur = int(t & 1), oth = cur ^ 1;
     const long long tnew = ro.backward ? t - 1 : t + 1;
@@ -675,11 +698,17 @@ void step_points(Plan& P, int op, long long t, int part, float* target_override 
         pp.target = target_override ? target_override : P.u[oth].as<float>();
         pp.r = P.r.as<float>();
         pp.inv_dt2 = P.coef.inv_dt2;
-        if (op == SFB_OP_FORWARD && P.save_every > 0 && tnew % P.save_every == 0)
-            pp.snap = P.snaps.as<float>() + (tnew / P.save_every) * P.ccount;
-        if (ro.imaging && t % P.save_every == 0) {
-            pp.usave = P.snaps.as<float>() + (t / P.save_every) * P.ccount;
-            pp.grad = P.grad.as<float>();
+        if (ex) {
+            pp.snap = ex->snap;
+            pp.usave = ex->usave;
+            if (ex->usave) pp.grad = P.grad.as<float>();
+        } else {
+            if (op == SFB_OP_FORWARD && P.save_every > 0 && tnew % P.save_every == 0)
+                pp.snap = P.snaps.as<float>() + (tnew / P.save_every) * P.ccount;
+            if (ro.imaging && t % P.save_every == 0) {
+                pp.usave = P.snaps.as<float>() + (t / P.save_every) * P.ccount;
+                pp.grad = P.grad.as<float>();
+            }
         }
         int nb_smp = 0;
         if (do_gather) {
@@ -806,6 +835,119 @@ void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stre
         rep->gpts_per_s = rep->seconds > 0 ? own * steps / rep->seconds / 1e9 : 0.0;
         rep->kernel_launches = P.launches;
         (void)pts;
+    }
+}
+
+// ---- checkpointed history: recompute instead of store ------------------
+// The reference keeps the whole forward history in RAM (proj/src/seismic_ops.cpp:66-68) and
+// marks checkpointing out of scope.  At config-3 size the full history is
+// 415 GB; save_every thins it, this removes the limit: the forward run keeps only the state
+// (levels kC-1 and kC) at every C-th level, and the backward sweep recomputes one segment of
+// C levels at a time into a small buffer before imaging against it -- every level, i.e. the
+// reference's exact imaging condition -- at the price of one extra forward pass.
+
+void forward_checkpointed(Plan& P, long long C, sfb_report* rep, double* stream_out) {
+    require(C >= 2, SFB_ERR_PARAMETER, "checkpoint_every must be >= 2");
+    require(P.n0 == P.N[0], SFB_ERR_CAPABILITY, "checkpointed runs are single-slab in this round");
+    const int op = SFB_OP_FORWARD;
+    step_begin(P, op, 0);
+    const long long nt = P.desc.nt;
+    P.ckpt_valid = false;
+    P.ckpt_every = C;
+    P.nseg = (nt - 1 + C - 1) / C;
+    P.ckpt.alloc(size_t(P.nseg + 1) * 2 * P.ccount * 4, false);
+    SFB_CUDA(cudaMemsetAsync(P.ckpt.p, 0, size_t(P.nseg + 1) * 2 * P.ccount * 4, P.s_main));
+    std::unique_ptr<RowStreamer> rs;
+    if (stream_out) rs.reset(new RowStreamer(P, P.cloud[SFB_CLOUD_REC], stream_out));
+    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+    for (long long t = 1; t < nt - 1; ++t) {
+        const long long tnew = t + 1;
+        StepExtras ex;
+        if (tnew % C == 0) ex.snap = P.ckpt.as<float>() + ((tnew / C) * 2 + 1) * P.ccount;
+        if (tnew % C == C - 1) ex.snap = P.ckpt.as<float>() + (((tnew + 1) / C) * 2 + 0) * P.ccount;
+        step_compute(P, op, t, SFB_PART_ALL, &ex);
+        step_points(P, op, t, SFB_PART_ALL, nullptr, true, &ex);
+        if (rs) rs->row_done(t);
+    }
+    SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    float ms = 0.f;
+    SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+    finite_guard(P, "forward");
+    if (rs) rs->finish();
+    P.ckpt_valid = true;
+    P.history_valid = false;
+    if (rep) {
+        const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
+        rep->seconds = ms * 1e-3;
+        rep->steps = long(std::max<long long>(0, nt - 2));
+        rep->flops = (long long)(double(3LL * P.K * P.ndim + 3LL * P.ndim + 11) * own * rep->steps);
+        rep->gflops = ms > 0 ? double(rep->flops) / (ms * 1e-3) / 1e9 : 0.0;
+        rep->gpts_per_s = ms > 0 ? own * rep->steps / (ms * 1e-3) / 1e9 : 0.0;
+        rep->kernel_launches = P.launches;
+    }
+}
+
+void gradient_checkpointed(Plan& P, sfb_report* rep) {
+    require(P.ckpt_valid, SFB_ERR_PARAMETER, "gradient_operator: saved forward history required");
+    const long long nt = P.desc.nt, C = P.ckpt_every;
+    const int G = SFB_OP_GRADIENT, F = SFB_OP_FORWARD;
+    // v (the adjoint wavefield) lives in u[2]; the recomputed forward pair in f[2]
+    const bool new_f = !P.f[0].p;
+    for (int b = 0; b < 2; ++b) P.f[b].alloc(size_t(P.ucount) * 4, true);
+    if (new_f) make_tensor_maps(P);
+    P.seg.alloc(size_t(C) * P.ccount * 4, false);
+    P.grad.alloc(size_t(P.ccount) * 4, false);
+    SFB_CUDA(cudaMemsetAsync(P.grad.p, 0, size_t(P.ccount) * 4, P.s_main));
+    SFB_CUDA(cudaMemsetAsync(P.u[0].p, 0, size_t(P.ucount) * 4, P.s_main));
+    SFB_CUDA(cudaMemsetAsync(P.u[1].p, 0, size_t(P.ucount) * 4, P.s_main));
+    P.launches = 0;
+    P.main_pending = P.bnd_pending = false;
+    Cloud& cr = P.cloud[SFB_CLOUD_REC];
+    require(cr.has_in && P.cloud[SFB_CLOUD_SRC].has_in, SFB_ERR_BINDING,
+            "checkpointed gradient needs the source and residual traces on the device");
+    const size_t lvl = size_t(P.ccount) * 4, ghost = size_t(P.K) * P.plane;
+    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+    for (long long k = P.nseg - 1; k >= 0; --k) {
+        const long long t_lo = k * C, t_top = std::min((k + 1) * C, nt - 2);
+        if (t_top <= t_lo) continue;
+        // restore the forward state (levels t_lo - 1, t_lo) of this segment
+        const float* ck = P.ckpt.as<float>() + (k * 2) * P.ccount;
+        SFB_CUDA(cudaMemcpyAsync(P.f[(t_lo + 1) & 1].as<float>() + ghost, ck, lvl,
+                                 cudaMemcpyDeviceToDevice, P.s_main));
+        SFB_CUDA(cudaMemcpyAsync(P.f[t_lo & 1].as<float>() + ghost, ck + P.ccount, lvl,
+                                 cudaMemcpyDeviceToDevice, P.s_main));
+        if (k == 0)  // level 1 is never produced by a step: it is identically zero
+            SFB_CUDA(cudaMemsetAsync(P.seg.p, 0, lvl, P.s_main));
+        // recompute levels t_lo+1 .. t_top into the segment buffer
+        for (long long t = std::max<long long>(t_lo, 1); t < t_top; ++t) {
+            StepExtras ex;
+            ex.alt = true;
+            ex.snap = P.seg.as<float>() + (t + 1 - t_lo - 1) * P.ccount;
+            step_compute(P, F, t, SFB_PART_ALL, &ex);
+            step_points(P, F, t, SFB_PART_ALL, P.f[(t & 1) ^ 1].as<float>(), false, &ex);
+        }
+        // backward sweep over the segment, imaging against every recomputed level
+        for (long long t = t_top; t > t_lo; --t) {
+            StepExtras ex;
+            ex.usave = P.seg.as<float>() + (t - t_lo - 1) * P.ccount;
+            step_compute(P, G, t, SFB_PART_ALL, &ex);
+            step_points(P, G, t, SFB_PART_ALL, nullptr, true, &ex);
+        }
+    }
+    SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    float ms = 0.f;
+    SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+    finite_guard(P, "gradient");
+    if (rep) {
+        const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
+        rep->seconds = ms * 1e-3;
+        rep->steps = long(std::max<long long>(0, nt - 2));
+        rep->flops = (long long)(double(2 * (3LL * P.K * P.ndim + 3LL * P.ndim + 11) + 7) * own * rep->steps);
+        rep->gflops = ms > 0 ? double(rep->flops) / (ms * 1e-3) / 1e9 : 0.0;
+        rep->gpts_per_s = ms > 0 ? own * rep->steps / (ms * 1e-3) / 1e9 : 0.0;
+        rep->kernel_launches = P.launches;
     }
 }
 
@@ -1376,6 +1518,18 @@ SFB_API int sfb_forward(sfb_plan* plan, const double* src, double* rec, int64_t 
     });
 }
 
+SFB_API int sfb_forward_checkpointed(sfb_plan* plan, const double* src, double* rec,
+                                     int64_t checkpoint_every, sfb_report* report) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(src && rec, SFB_ERR_PARAMETER, "forward: null trace table");
+        require(P.cloud[0].set && P.cloud[1].set, SFB_ERR_BINDING, "point clouds are not bound");
+        upload_traces(P, P.cloud[SFB_CLOUD_SRC], src);
+        forward_checkpointed(P, checkpoint_every, report, rec);
+    });
+}
+
 SFB_API int sfb_adjoint(sfb_plan* plan, const double* rec, double* srca, sfb_report* report) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
@@ -1394,10 +1548,13 @@ SFB_API int sfb_gradient(sfb_plan* plan, const double* resid, const sfb_field_mv
         Plan& P = *plan;
         require(resid && grad && grad->ptr, SFB_ERR_PARAMETER, "gradient: null argument");
         require(P.cloud[1].set, SFB_ERR_BINDING, "receiver cloud is not bound");
-        require(P.history_valid && P.save_every > 0, SFB_ERR_PARAMETER,
+        require((P.history_valid && P.save_every > 0) || P.ckpt_valid, SFB_ERR_PARAMETER,
                 "gradient_operator: saved forward history required");
         upload_traces(P, P.cloud[SFB_CLOUD_REC], resid);
-        run_op(P, SFB_OP_GRADIENT, P.save_every, report);
+        if (P.ckpt_valid && !P.history_valid)
+            gradient_checkpointed(P, report);
+        else
+            run_op(P, SFB_OP_GRADIENT, P.save_every, report);
         download_field(P, P.grad.as<float>(), grad);
     });
 }

@@ -163,6 +163,14 @@ struct Plan {
     const StepVariant* variant = nullptr;       // chosen tile shape
     int chunk = 0;                              // output planes per block
 
+    // checkpointed history (recompute strategy): levels (kC-1, kC) of
+    // the forward run for every segment start, a second wavefield pair for the recomputed
+    // forward segment, and the levels of one segment
+    DevBuf f[2], ckpt, seg;
+    CUtensorMap tm_fu[2], tm_fo[2];
+    long long ckpt_every = 0, nseg = 0;
+    bool ckpt_valid = false;
+
     // history of the last forward run
     long long save_every = 0, nslots = 0;
     bool history_valid = false;

@@ -54,9 +54,10 @@ point_step_kernel(const __grid_constant__ PointParams p, int nb_inj) {
         for (int e = e0; e < e1; ++e) s = fmaf(p.ent_w[e], p.inj_row[p.ent_point[e]], s);
         const long long cu = p.cell_u[i], cc = p.cell_c[i];
         const float add = s * p.r[cc];
-        p.target[cu] += add;
-        if (p.snap) p.snap[cc] += add;
-        if (p.usave) p.grad[cc] = fmaf(-p.usave[cc] * p.inv_dt2, add, p.grad[cc]);
+        p.target[cu] = __ldcg(p.target + cu) + add;
+        if (p.snap) p.snap[cc] = __ldcg(p.snap + cc) + add;
+        if (p.usave)
+            p.grad[cc] = fmaf(-__ldcg(p.usave + cc) * p.inv_dt2, add, __ldcg(p.grad + cc));
     } else {
         const int i = (blockIdx.x - nb_inj) * kPointThreads + threadIdx.x;
         if (i >= p.nsmp) return;
@@ -67,7 +68,7 @@ point_step_kernel(const __grid_constant__ PointParams p, int nb_inj) {
             // corners with zero weight (points on lattice lines) are not fetched
             for (int c = 0; c < p.ncorner; ++c) {
                 const float wc = w[c];
-                if (wc != 0.f) s = fmaf(wc, p.field[b + p.corner_off[c]], s);
+                if (wc != 0.f) s = fmaf(wc, __ldcg(p.field + b + p.corner_off[c]), s);
             }
         }
         p.smp_row[i] = s;

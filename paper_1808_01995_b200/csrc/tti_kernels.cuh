@@ -182,7 +182,7 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
         }
         if (n < 2 * K) {
             __syncwarp();
-            if (lane0) mbar_arrive(done + s);
+            if (lane0) mbar_release(done + s, q[Q - 1][0]);
         } else {
             const float* cp = st + OFF_CTR + field * CPAD;  // haloed centre box of this field
             float d0[4], d1[4], d2[4];
@@ -269,8 +269,9 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                 o[2] = fmaf(a4.z, d0[2], fmaf(b4.z, d1[2], c4.z * d2[2]));
                 o[3] = fmaf(a4.w, d0[3], fmaf(b4.w, d1[3], c4.w * d2[3]));
             }
+            // o[0] depends on every shared-memory load of the iteration (see mbar_release)
             __syncwarp();
-            if (lane0) mbar_arrive(done + s);
+            if (lane0) mbar_release(done + s, o[0]);
             if (rin) *reinterpret_cast<float4*>(outp) = make_float4(o[0], o[1], o[2], o[3]);
             outp += p.plane;
         }
@@ -427,7 +428,7 @@ tti_update_kernel(const __grid_constant__ UpdMaps tm, const __grid_constant__ Up
         }
         if (n < 2 * K) {
             __syncwarp();
-            if (lane0) mbar_arrive(done + s);
+            if (lane0) mbar_release(done + s, q[Q - 1][0]);
         } else {
             const float* ap = st + ABOX + CPAD + aown;
             float a[NARR][4];
@@ -443,8 +444,6 @@ tti_update_kernel(const __grid_constant__ UpdMaps tm, const __grid_constant__ Up
             if (SEP) dzv = __ldg(p.dz + (zb + n - 2 * K));
             float lap[4];
             stencil_acc<K, KP, SW>(lk, q, st + ABOX, tx, ty, lap);
-            __syncwarp();
-            if (lane0) mbar_arrive(done + s);
             float pn[4], rn[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -459,6 +458,9 @@ tti_update_kernel(const __grid_constant__ UpdMaps tm, const __grid_constant__ Up
                 pn[c] = fmaf(c1, fmaf(rm, rhs_p, 2.f * q[K][c]), -c2 * po);
                 rn[c] = fmaf(c1, fmaf(rm, rhs_r, 2.f * rc), -c2 * ro);
             }
+            // pn[0] + rn[0] depends on every shared-memory load of the iteration
+            __syncwarp();
+            if (lane0) mbar_release(done + s, pn[0] + rn[0]);
             if (rin) {
                 __stcs(reinterpret_cast<float4*>(pp), make_float4(pn[0], pn[1], pn[2], pn[3]));
                 __stcs(reinterpret_cast<float4*>(rp), make_float4(rn[0], rn[1], rn[2], rn[3]));

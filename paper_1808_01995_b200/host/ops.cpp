@@ -208,7 +208,11 @@ ExecutionReport run_wave(WaveOp& w, Backend, int) {
                 }
         return to_report(rep);
     }
-    if (!w.adjoint) {
+    const bool ckpt = !w.adjoint && w.save_every > 0 && w.checkpoint_every > 0;
+    if (ckpt) {
+        e.check(sfb_forward_checkpointed(e.plan(), w.inj->traces().data(),
+                                         w.smp->traces().data(), w.checkpoint_every, &rep));
+    } else if (!w.adjoint) {
         e.check(sfb_forward(e.plan(), w.inj->traces().data(), w.smp->traces().data(),
                             w.save_every, &rep));
     } else {
@@ -219,8 +223,8 @@ ExecutionReport run_wave(WaveOp& w, Backend, int) {
     TimeFunction& u = *w.wavefield;
     if (w.save_every > 0) {
         u.device_history = w.engine;
-        u.device_save_every = w.save_every;
-        if (w.host_history && !u.time_buffered())
+        u.device_save_every = ckpt ? 1 : w.save_every;
+        if (w.host_history && !ckpt && !u.time_buffered())
             for (long t = 2; t < w.nt; t += 1) {
                 if (t % w.save_every != 0) continue;
                 sfb_field_mview mv = Engine::mview(u, t);
@@ -296,10 +300,13 @@ std::vector<double> fold_gradient(const SeismicModel& model, const Function& gra
 // proj/src/seismic_ops.cpp:197-216
 GradientResult fwi_gradient(const SeismicModel& model, AcquisitionGeometry& geom,
                             const std::vector<double>& observed, int space_order, Backend backend,
-                            long save_every) {
+                            long save_every, long checkpoint_every) {
     if (save_every < 1) throw ParameterError("fwi_gradient: save_every must be >= 1");
+    if (checkpoint_every != 0 && (checkpoint_every < 2 || save_every != 1))
+        throw ParameterError("fwi_gradient: checkpoint_every must be >= 2 (with save_every 1)");
     WaveOp fwd = forward_operator(model, geom, space_order, true);
     fwd.save_every = save_every;
+    fwd.checkpoint_every = checkpoint_every;
     fwd.host_history = false;  // the history stays in HBM
     run_wave(fwd, backend);
     GradientResult res;
@@ -345,7 +352,7 @@ FwiResult fwi(SeismicModel& model, std::vector<AcquisitionGeometry>& shots,
                     set_device(cfg.devices.empty() ? dev : cfg.devices[s % cfg.devices.size()]);
                     try {
                         parts[s] = fwi_gradient(model, shots[s], observed[s], cfg.space_order,
-                                                cfg.backend);
+                                                cfg.backend, cfg.save_every, cfg.checkpoint_every);
                     } catch (const Error& e) {
                         failures[s] = e.what();
                     }

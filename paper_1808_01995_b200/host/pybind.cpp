@@ -171,7 +171,8 @@ PYBIND11_MODULE(_sfb_host, m) {
         .def_readonly("dt", &WaveOp::dt)
         .def_readonly("nt", &WaveOp::nt)
         .def_readwrite("save_every", &WaveOp::save_every)
-        .def_readwrite("host_history", &WaveOp::host_history);
+        .def_readwrite("host_history", &WaveOp::host_history)
+        .def_readwrite("checkpoint_every", &WaveOp::checkpoint_every);
     py::class_<TtiModel>(m, "TtiModel")
         .def(py::init([](const SeismicModel& model, const darray& e, const darray& d, const darray& t,
                          const darray& p) { return new TtiModel(model, flat(e), flat(d), flat(t), flat(p)); }))
@@ -206,9 +207,12 @@ PYBIND11_MODULE(_sfb_host, m) {
         .def_property_readonly("residual", [](const GradientResult& r) { return py::array(py::cast(r.residual)); });
     m.def("fwi_gradient",
           [](const SeismicModel& model, AcquisitionGeometry& geom, const darray& obs, int order,
-             long save_every) { return fwi_gradient(model, geom, flat(obs), order, Backend::Auto, save_every); },
+             long save_every, long checkpoint_every) {
+              return fwi_gradient(model, geom, flat(obs), order, Backend::Auto, save_every,
+                                  checkpoint_every);
+          },
           py::arg("model"), py::arg("geom"), py::arg("observed"), py::arg("space_order"),
-          py::arg("save_every") = 1);
+          py::arg("save_every") = 1, py::arg("checkpoint_every") = 0);
 
     py::class_<FwiConfig>(m, "FwiConfig")
         .def(py::init<>())
@@ -218,7 +222,9 @@ PYBIND11_MODULE(_sfb_host, m) {
         .def_readwrite("m_min", &FwiConfig::m_min)
         .def_readwrite("m_max", &FwiConfig::m_max)
         .def_readwrite("nthreads", &FwiConfig::nthreads)
-        .def_readwrite("devices", &FwiConfig::devices);
+        .def_readwrite("devices", &FwiConfig::devices)
+        .def_readwrite("save_every", &FwiConfig::save_every)
+        .def_readwrite("checkpoint_every", &FwiConfig::checkpoint_every);
     py::class_<FwiResult>(m, "FwiResult")
         .def_readonly("objectives", &FwiResult::objectives)
         .def_readonly("model_rms", &FwiResult::model_rms)

@@ -153,6 +153,69 @@ def test_gradient_parity(save_every):
     plan.close()
 
 
+@pytest.mark.parametrize("nt,C", [(96, 7), (96, 16), (50, 2), (41, 40), (30, 64)])
+def test_checkpointed_gradient_equals_full_history(nt, C):
+    # recompute strategy: same kernels in the same order, so the gradient is the full-history
+    # (save_every = 1, the reference's imaging condition) gradient bit for bit
+    model, geom = make_problem([30, 28, 34], 10.0, 8, 8, nt, dt_frac=0.9)
+    rng = np.random.default_rng(5)
+    plan = make_plan(model, geom, 8)
+    rec, _ = plan.forward(geom.src, save_every=1)
+    resid = rec + 0.1 * np.abs(rec).max() * rng.standard_normal(rec.shape)
+    g_full, _ = plan.gradient(resid)
+    rec_c, _ = plan.forward_checkpointed(geom.src, C)
+    g_ck, rep = plan.gradient(resid)
+    assert np.array_equal(rec_c, rec)
+    assert np.abs(g_full).max() > 0
+    assert np.array_equal(g_ck, g_full)
+    assert rep.steps == geom.nt - 2
+    # a second gradient from the same checkpoints, and a plain forward invalidates them
+    g_again, _ = plan.gradient(0.5 * resid)
+    assert rel_l2(g_again, 0.5 * g_full) <= 1e-6
+    plan.forward(geom.src)
+    from paper_1808_01995_b200 import capi
+    with pytest.raises(capi.SfbError):
+        plan.gradient(resid)
+    plan.close()
+
+
+@pytest.mark.parametrize("order,tile", [(8, None), (8, (16, 16, -3)), (12, None), (4, None)])
+def test_gradient_runs_are_bitwise_repeatable(order, tile):
+    """Regression for a pipeline race found at sizes that fill the SMs with several blocks:
+    a stage was released to the TMA producer while a warp's shared-memory loads were still
+    in flight, so single rows of a plane came out one pipeline round too new, differently
+    from run to run, once the imaging traffic stretched the warps apart.  A dense carpet of
+    injection points and six repeats expose it (tools/probe_determinism4.py)."""
+    shape, h = [560, 128, 96], 10.0
+    ii, jj = np.meshgrid(np.arange(0, shape[0] - 1, 2), np.arange(0, shape[1] - 1, 2), indexing="ij")
+    rec = np.stack([ii.ravel() * h + 0.3 * h, jj.ravel() * h + 0.4 * h,
+                    np.full(ii.size, 4.5 * h)], axis=1)
+    model, geom = make_problem(shape, h, 8, order, 6, dt_frac=0.9, rec=rec)
+    plan = make_plan(model, geom, order)
+    if tile:
+        plan.set_tile(*tile)
+    rec_tr, _ = plan.forward(geom.src, save_every=1)
+    resid = np.random.default_rng(5).standard_normal(rec_tr.shape)
+    g0, _ = plan.gradient(resid)
+    v0 = plan.wavefield(0)
+    assert np.abs(g0).max() > 0
+    for _ in range(5):
+        g, _ = plan.gradient(resid)
+        assert np.array_equal(plan.wavefield(0), v0)
+        assert np.array_equal(g, g0)
+    plan.close()
+
+
+def test_checkpoint_interval_is_checked():
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([20, 20, 20], 10.0, 6, 8, 20)
+    plan = make_plan(model, geom, 8)
+    with pytest.raises(capi.SfbError) as e:
+        plan.forward_checkpointed(geom.src, 1)
+    assert e.value.code == capi.ERR_PARAMETER
+    plan.close()
+
+
 def test_zero_residual_gives_zero_gradient():  # proj/tests/test_seismic.cpp:247-260
     model, geom = make_problem([20, 20, 20], 10.0, 6, 8, 40)
     plan = make_plan(model, geom, 8)

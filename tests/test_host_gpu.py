@@ -114,6 +114,25 @@ def test_zero_residual_zero_gradient():  # test_seismic.cpp:247-260
     assert res.objective == 0.0 and (res.gradient == 0.0).all()
 
 
+def test_fwi_gradient_checkpointed_equals_full_history():
+    """fwi_gradient(checkpoint_every=C): the recompute strategy images at every level like the
+    reference and returns the full-history gradient bit for bit."""
+    m = constant_model(21, 10.0, 1.5, 6)
+    g = H.AcquisitionGeometry(m, [100.0, 20.0], [40.0, 40.0, 160.0, 40.0], 0.0, 120.0,
+                              0.8 * m.critical_dt(), 0.01)
+    H.run_wave(H.forward_operator(m, g, 8))
+    observed = 0.7 * g.rec.traces.copy()
+    full = H.fwi_gradient(m, g, observed, 8)
+    for C in (2, 5, 1000):
+        ck = H.fwi_gradient(m, g, observed, 8, checkpoint_every=C)
+        assert ck.objective == full.objective
+        assert np.array_equal(ck.gradient, full.gradient)
+    with pytest.raises(H.ParameterError):
+        H.fwi_gradient(m, g, observed, 8, checkpoint_every=1)
+    with pytest.raises(H.ParameterError):
+        H.fwi_gradient(m, g, observed, 8, save_every=2, checkpoint_every=4)
+
+
 def test_gradient_operator_needs_saved_history():  # seismic_ops.cpp:113-114
     m = constant_model(21, 10.0, 1.5, 6)
     g = H.AcquisitionGeometry(m, [100.0, 20.0], [40.0, 40.0], 0.0, 60.0, 0.8 * m.critical_dt(), 0.01)
