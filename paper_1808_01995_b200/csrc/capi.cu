@@ -975,13 +975,22 @@ void tti_coef(const Plan& P, TtiCoef& k) {
 // tensor maps of every TTI field for the (fixed) TTI tile shape
 void tti_make_maps(Plan& P) {
     const TtiVariant& v = *P.tti_variant;
-    void* wf[Plan::TF_COUNT] = {P.u[0].p, P.u[1].p, P.t_r[0].p, P.t_r[1].p, P.t_gp.p,
-                                P.t_gr.p, P.t_a.p, P.t_b.p, P.t_c.p};
+    void* wf[Plan::TF_COUNT] = {P.u[0].p, P.u[1].p, P.t_r[0].p, P.t_r[1].p,
+                                P.t_a.p,  P.t_b.p,  P.t_c.p};
     for (int i = 0; i < Plan::TF_COUNT; ++i) {
         encode_map(&P.tt_halo[i], wf[i], P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane, v.box_w,
                    v.box_h);
         encode_map(&P.tt_plain[i], wf[i], P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
                    v.tile_x, v.tile_y);
+    }
+    for (int f = 0; f < 2; ++f) {
+        const long long n0g = P.n0 + 2 * P.K;
+        encode_map(&P.tt_ag[f], P.t_ag[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.tile_x,
+                   v.tile_y);
+        encode_map(&P.tt_bg[f], P.t_bg[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.tile_x,
+                   v.box_h);
+        encode_map(&P.tt_cg[f], P.t_cg[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.box_w,
+                   v.tile_y);
     }
     void* cf[Plan::TC_COUNT] = {P.r.p, P.t_e1.p, P.t_e2.p, P.t_hzp.p, P.t_hzr.p,
                                 P.sep ? P.r.p : P.damp.p};
@@ -996,17 +1005,43 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
     step_begin(P, op, 0);
     for (int b = 0; b < 2; ++b)
         SFB_CUDA(cudaMemsetAsync(P.t_r[b].p, 0, size_t(P.ucount) * 4, P.s_main));
-    SFB_CUDA(cudaMemsetAsync(P.t_gp.p, 0, size_t(P.ucount) * 4, P.s_main));
-    SFB_CUDA(cudaMemsetAsync(P.t_gr.p, 0, size_t(P.ucount) * 4, P.s_main));
+    for (DevBuf* d : {&P.t_ag[0], &P.t_ag[1], &P.t_bg[0], &P.t_bg[1], &P.t_cg[0], &P.t_cg[1]})
+        SFB_CUDA(cudaMemsetAsync(d->p, 0, size_t(P.ucount) * 4, P.s_main));
     const TtiVariant& v = *P.tti_variant;
     const long long nt = P.desc.nt;
     const int sepi = P.sep ? 1 : 0;
-    // one chunk of d0 per block column so the grid fills the SMs (the rings allow one
-    // block per SM)
+    // split d0 into chunks so each grid fills whole waves of its kernel's resident blocks;
+    // every chunk re-reads 2K planes to fill its register queues, charged at half a plane
     const long long tiles = ((P.N[2] + v.tile_x - 1) / v.tile_x) * ((P.N[1] + v.tile_y - 1) / v.tile_y);
-    int nch = int(std::max<long long>(1, (2LL * P.sm_count + tiles - 1) / tiles));
-    nch = std::min(nch, std::max(1, P.n0 / std::max(1, 2 * P.K)));
-    const int chunk = (P.n0 + nch - 1) / nch;
+    auto chunk_for = [&](const void* func, int nthreads, size_t smem) {
+        int bps = 1;
+        SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, func, nthreads, smem));
+        const long long slots = (long long)P.sm_count * std::max(1, bps);
+        int nch = 1;
+        double best = -1;
+        const int max_nch = std::max(1, P.n0 / std::max(1, 4 * P.K));
+        for (int c = 1; c <= max_nch; ++c) {
+            const int ch = (P.n0 + c - 1) / c;
+            const long long total = tiles * ((P.n0 + ch - 1) / ch);
+            const long long waves = (total + slots - 1) / slots;
+            const double fill = double(total) / double(waves * slots);
+            const double score = fill / (1.0 + (2.0 * P.K / ch) * 0.5);
+            if (score > best + 1e-9) {
+                best = score;
+                nch = c;
+            }
+            if (total > 16 * slots) break;
+        }
+        return (P.n0 + nch - 1) / nch;
+    };
+    const int chunk = chunk_for(v.f_rot, v.rot_threads, v.smem_rot);
+    const int chunk_div = chunk_for(v.f_div, v.rot_threads, v.smem_div);
+    const int chunk_upd = chunk_for(v.f_upd[sepi], v.upd_threads, v.smem_upd[sepi]);
+    auto grid_for = [&](int ch) {
+        return dim3(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x),
+                    unsigned((P.N[1] + v.tile_y - 1) / v.tile_y), unsigned((P.n0 + ch - 1) / ch));
+    };
+    const dim3 grid_div = grid_for(chunk_div), grid_upd = grid_for(chunk_upd);
     dim3 grid(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x), unsigned((P.N[1] + v.tile_y - 1) / v.tile_y),
               unsigned((P.n0 + chunk - 1) / chunk));
     RotParams rp{};
@@ -1018,6 +1053,15 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
     rp.z_lo = 0;
     rp.z_hi = P.n0;
     rp.chunk = chunk;
+    DivParams dp{};
+    dp.k = rp.k;
+    dp.N1 = rp.N1;
+    dp.N2 = rp.N2;
+    dp.pitch = P.pitch;
+    dp.plane = P.plane;
+    dp.z_lo = 0;
+    dp.z_hi = P.n0;
+    dp.chunk = chunk_div;
     UpdParams up{};
     up.k = rp.k;
     up.dz = P.dz.as<float>();
@@ -1029,7 +1073,7 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
     up.plane = P.plane;
     up.z_lo = 0;
     up.z_hi = P.n0;
-    up.chunk = chunk;
+    up.chunk = chunk_upd;
     std::unique_ptr<RowStreamer> rs;
     if (stream_out) rs.reset(new RowStreamer(P, P.cloud[SFB_CLOUD_REC], stream_out));
     SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
@@ -1044,23 +1088,24 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
         m1.a = P.tt_plain[Plan::TF_A];
         m1.b = P.tt_plain[Plan::TF_B];
         m1.c = P.tt_plain[Plan::TF_C];
-        rp.out0 = P.t_gp.as<float>();
-        rp.out1 = P.t_gr.as<float>();
+        for (int f = 0; f < 2; ++f) {
+            rp.ag[f] = P.t_ag[f].as<float>();
+            rp.bg[f] = P.t_bg[f].as<float>();
+            rp.cg[f] = P.t_cg[f].as<float>();
+        }
         rp.out_off = (long long)P.K * P.plane;
-        SFB_CUDA(v.rot[0](m1, rp, grid, P.s_main));
+        SFB_CUDA(v.rot(m1, rp, grid, P.s_main));
         // 2. Hz(p), Hz(r)
-        RotMaps m2;
-        m2.f0_feed = P.tt_plain[Plan::TF_GP];
-        m2.f1_feed = P.tt_plain[Plan::TF_GR];
-        m2.f0_ctr = P.tt_halo[Plan::TF_GP];
-        m2.f1_ctr = P.tt_halo[Plan::TF_GR];
-        m2.a = P.tt_plain[Plan::TF_A];
-        m2.b = P.tt_halo[Plan::TF_B];
-        m2.c = P.tt_halo[Plan::TF_C];
-        rp.out0 = P.t_hzp.as<float>();
-        rp.out1 = P.t_hzr.as<float>();
-        rp.out_off = 0;
-        SFB_CUDA(v.rot[1](m2, rp, grid, P.s_main));
+        DivMaps m2;
+        m2.ag0 = P.tt_ag[0];
+        m2.ag1 = P.tt_ag[1];
+        m2.bg0 = P.tt_bg[0];
+        m2.bg1 = P.tt_bg[1];
+        m2.cg0 = P.tt_cg[0];
+        m2.cg1 = P.tt_cg[1];
+        dp.out0 = P.t_hzp.as<float>();
+        dp.out1 = P.t_hzr.as<float>();
+        SFB_CUDA(v.div(m2, dp, grid_div, P.s_main));
         // 3. L(p), right-hand sides, leapfrog of both fields (in place over level t-1)
         UpdMaps m3;
         m3.p_feed = P.tt_plain[Plan::TF_P0 + cur];
@@ -1076,7 +1121,7 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
         m3.d = P.tt_c[Plan::TC_DAMP];
         up.po = P.u[oth].as<float>();
         up.ro = P.t_r[oth].as<float>();
-        SFB_CUDA(v.upd[sepi](m3, up, grid, P.s_main));
+        SFB_CUDA(v.upd[sepi](m3, up, grid_upd, P.s_main));
         P.launches += 3;
         step_points(P, op, t, SFB_PART_ALL);                                   // p: scatter + gather
         step_points(P, op, t, SFB_PART_ALL, P.t_r[oth].as<float>(), false);    // r: scatter
@@ -1394,16 +1439,21 @@ SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
         upload_f64(P, embed_view(P, theta->ptr, theta->stride), tt);
         upload_f64(P, embed_view(P, phi->ptr, phi->stride), tph);
         for (int b = 0; b < 2; ++b) P.t_r[b].alloc(size_t(P.ucount) * 4);
-        for (DevBuf* d : {&P.t_gp, &P.t_gr, &P.t_a, &P.t_b, &P.t_c}) d->alloc(size_t(P.ucount) * 4);
+        for (DevBuf* d : {&P.t_a, &P.t_b, &P.t_c, &P.t_ag[0], &P.t_ag[1], &P.t_bg[0], &P.t_bg[1],
+                          &P.t_cg[0], &P.t_cg[1]})
+            d->alloc(size_t(P.ucount) * 4);
         for (DevBuf* d : {&P.t_e1, &P.t_e2, &P.t_hzp, &P.t_hzr}) d->alloc(size_t(P.ccount) * 4);
         P.tti_variant = nullptr;
         for (const TtiVariant& tv : tti_variant_registry())
             if (tv.K == P.K) P.tti_variant = &tv;
         require(P.tti_variant != nullptr, SFB_ERR_CAPABILITY, "no TTI kernel image for this order");
+        SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_rot,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(P.tti_variant->smem_rot)));
+        SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_div,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(P.tti_variant->smem_div)));
         for (int i = 0; i < 2; ++i) {
-            SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_rot[i],
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(P.tti_variant->smem_rot[i])));
             SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_upd[i],
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(P.tti_variant->smem_upd[i])));
