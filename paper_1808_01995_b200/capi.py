@@ -19,6 +19,7 @@ lib = C.CDLL(LIB_PATH)
 OK, ERR_PARAMETER, ERR_STABILITY, ERR_LOCATION, ERR_CAPABILITY, ERR_BINDING, ERR_CUDA, ERR_ORDER = range(8)
 CLOUD_SRC, CLOUD_REC = 0, 1
 OP_FORWARD, OP_ADJOINT, OP_GRADIENT, OP_TTI_FORWARD = 0, 1, 2, 3
+TTI_HALO_AG_P, TTI_HALO_AG_R, TTI_HALO_P, TTI_HALO_R = 0, 1, 2, 3
 PART_ALL, PART_LOW, PART_HIGH, PART_INTERIOR = 0, 1, 2, 3
 
 
@@ -45,7 +46,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune",
 ]
@@ -77,6 +78,9 @@ lib.sfb_step_slab_interior.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_put_history.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(FieldView)]
 lib.sfb_get_gradient.argtypes = [C.c_void_p, C.POINTER(FieldView)]
 lib.sfb_halo_blocks.argtypes = [C.c_void_p, C.c_int, C.c_int64] + [C.POINTER(C.c_void_p)] * 4 + [C.POINTER(C.c_int64)]
+lib.sfb_tti_step_rot.argtypes = [C.c_void_p, C.c_int64, C.c_int]
+lib.sfb_tti_step_update.argtypes = [C.c_void_p, C.c_int64, C.c_int]
+lib.sfb_tti_halo_blocks.argtypes = lib.sfb_halo_blocks.argtypes
 lib.sfb_stream_sync.argtypes = [C.c_void_p]
 lib.sfb_streams.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
 lib.sfb_set_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -295,6 +299,19 @@ class Plan:
         p = [C.c_void_p() for _ in range(4)]
         n = C.c_int64()
         self._chk(lib.sfb_halo_blocks(self.h, op, t, *[C.byref(x) for x in p], C.byref(n)))
+        return dict(send_lo=p[0].value, send_hi=p[1].value, recv_lo=p[2].value,
+                    recv_hi=p[3].value, count=n.value)
+
+    def tti_step_rot(self, t, part):
+        self._chk(lib.sfb_tti_step_rot(self.h, t, part))
+
+    def tti_step_update(self, t, part):
+        self._chk(lib.sfb_tti_step_update(self.h, t, part))
+
+    def tti_halo_blocks(self, which, t):
+        p = [C.c_void_p() for _ in range(4)]
+        n = C.c_int64()
+        self._chk(lib.sfb_tti_halo_blocks(self.h, which, t, *[C.byref(x) for x in p], C.byref(n)))
         return dict(send_lo=p[0].value, send_hi=p[1].value, recv_lo=p[2].value,
                     recv_hi=p[3].value, count=n.value)
 

@@ -998,104 +998,119 @@ void tti_make_maps(Plan& P) {
         encode_map(&P.tt_c[i], cf[i], P.N[2], P.N[1], P.n0, P.pitch, P.plane, v.tile_x, v.tile_y);
 }
 
-void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
+// d0 chunk length of one TTI launch: the grid should be a whole number of waves of the
+// kernel's resident blocks; every chunk re-reads 2K planes to fill its register queues,
+// charged at half a plane
+int tti_chunk_for(Plan& P, const void* func, int nthreads, size_t smem) {
+    const TtiVariant& v = *P.tti_variant;
+    const long long tiles = ((P.N[2] + v.tile_x - 1) / v.tile_x) * ((P.N[1] + v.tile_y - 1) / v.tile_y);
+    int bps = 1;
+    SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, func, nthreads, smem));
+    const long long slots = (long long)P.sm_count * std::max(1, bps);
+    int nch = 1;
+    double best = -1;
+    const int max_nch = std::max(1, P.n0 / std::max(1, 4 * P.K));
+    for (int c = 1; c <= max_nch; ++c) {
+        const int ch = (P.n0 + c - 1) / c;
+        const long long total = tiles * ((P.n0 + ch - 1) / ch);
+        const long long waves = (total + slots - 1) / slots;
+        const double fill = double(total) / double(waves * slots);
+        const double score = fill / (1.0 + (2.0 * P.K / ch) * 0.5);
+        if (score > best + 1e-9) {
+            best = score;
+            nch = c;
+        }
+        if (total > 16 * slots) break;
+    }
+    return (P.n0 + nch - 1) / nch;
+}
+
+// run_wave for the TTI pair: zero p, r, the products between the passes and the traces
+void tti_begin(Plan& P) {
     require(P.tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
-    require(P.n0 == P.N[0], SFB_ERR_CAPABILITY, "the TTI operator is single-slab in this round");
-    const int op = SFB_OP_TTI_FORWARD;
-    step_begin(P, op, 0);
+    step_begin(P, SFB_OP_TTI_FORWARD, 0);
     for (int b = 0; b < 2; ++b)
         SFB_CUDA(cudaMemsetAsync(P.t_r[b].p, 0, size_t(P.ucount) * 4, P.s_main));
     for (DevBuf* d : {&P.t_ag[0], &P.t_ag[1], &P.t_bg[0], &P.t_bg[1], &P.t_cg[0], &P.t_cg[1]})
         SFB_CUDA(cudaMemsetAsync(d->p, 0, size_t(P.ucount) * 4, P.s_main));
     const TtiVariant& v = *P.tti_variant;
-    const long long nt = P.desc.nt;
     const int sepi = P.sep ? 1 : 0;
-    // split d0 into chunks so each grid fills whole waves of its kernel's resident blocks;
-    // every chunk re-reads 2K planes to fill its register queues, charged at half a plane
-    const long long tiles = ((P.N[2] + v.tile_x - 1) / v.tile_x) * ((P.N[1] + v.tile_y - 1) / v.tile_y);
-    auto chunk_for = [&](const void* func, int nthreads, size_t smem) {
-        int bps = 1;
-        SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, func, nthreads, smem));
-        const long long slots = (long long)P.sm_count * std::max(1, bps);
-        int nch = 1;
-        double best = -1;
-        const int max_nch = std::max(1, P.n0 / std::max(1, 4 * P.K));
-        for (int c = 1; c <= max_nch; ++c) {
-            const int ch = (P.n0 + c - 1) / c;
-            const long long total = tiles * ((P.n0 + ch - 1) / ch);
-            const long long waves = (total + slots - 1) / slots;
-            const double fill = double(total) / double(waves * slots);
-            const double score = fill / (1.0 + (2.0 * P.K / ch) * 0.5);
-            if (score > best + 1e-9) {
-                best = score;
-                nch = c;
-            }
-            if (total > 16 * slots) break;
-        }
-        return (P.n0 + nch - 1) / nch;
-    };
-    const int chunk = chunk_for(v.f_rot, v.rot_threads, v.smem_rot);
-    const int chunk_div = chunk_for(v.f_div, v.rot_threads, v.smem_div);
-    const int chunk_upd = chunk_for(v.f_upd[sepi], v.upd_threads, v.smem_upd[sepi]);
-    auto grid_for = [&](int ch) {
-        return dim3(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x),
-                    unsigned((P.N[1] + v.tile_y - 1) / v.tile_y), unsigned((P.n0 + ch - 1) / ch));
-    };
-    const dim3 grid_div = grid_for(chunk_div), grid_upd = grid_for(chunk_upd);
-    dim3 grid(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x), unsigned((P.N[1] + v.tile_y - 1) / v.tile_y),
-              unsigned((P.n0 + chunk - 1) / chunk));
+    P.tti_chunk[0] = tti_chunk_for(P, v.f_rot, v.rot_threads, v.smem_rot);
+    P.tti_chunk[1] = tti_chunk_for(P, v.f_div, v.rot_threads, v.smem_div);
+    P.tti_chunk[2] = tti_chunk_for(P, v.f_upd[sepi], v.upd_threads, v.smem_upd[sepi]);
+}
+
+dim3 tti_grid(const Plan& P, int lo, int hi, int chunk) {
+    const TtiVariant& v = *P.tti_variant;
+    return dim3(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x),
+                unsigned((P.N[1] + v.tile_y - 1) / v.tile_y), unsigned((hi - lo + chunk - 1) / chunk));
+}
+
+int tti_part_chunk(const Plan& P, int which, int part, int lo, int hi) {
+    return (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? std::min(P.tti_chunk[which], hi - lo)
+                                                               : (hi - lo);
+}
+
+// pass 1 on the planes of `part`: the products a g, b g, c g of p and r (level t)
+void tti_rot(Plan& P, long long t, int part) {
+    require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
+    int lo, hi;
+    part_range(P, part, lo, hi);
+    if (hi <= lo) return;
+    const TtiVariant& v = *P.tti_variant;
+    const int cur = int(t & 1);
     RotParams rp{};
     tti_coef(P, rp.k);
     rp.N1 = int(P.N[1]);
     rp.N2 = int(P.N[2]);
     rp.pitch = P.pitch;
     rp.plane = P.plane;
-    rp.z_lo = 0;
-    rp.z_hi = P.n0;
-    rp.chunk = chunk;
-    DivParams dp{};
-    dp.k = rp.k;
-    dp.N1 = rp.N1;
-    dp.N2 = rp.N2;
-    dp.pitch = P.pitch;
-    dp.plane = P.plane;
-    dp.z_lo = 0;
-    dp.z_hi = P.n0;
-    dp.chunk = chunk_div;
-    UpdParams up{};
-    up.k = rp.k;
-    up.dz = P.dz.as<float>();
-    up.dy = P.dy.as<float>();
-    up.dx = P.dx.as<float>();
-    up.N1 = rp.N1;
-    up.N2 = rp.N2;
-    up.pitch = P.pitch;
-    up.plane = P.plane;
-    up.z_lo = 0;
-    up.z_hi = P.n0;
-    up.chunk = chunk_upd;
-    std::unique_ptr<RowStreamer> rs;
-    if (stream_out) rs.reset(new RowStreamer(P, P.cloud[SFB_CLOUD_REC], stream_out));
-    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
-    for (long long t = 1; t < nt - 1; ++t) {
-        const int cur = int(t & 1), oth = cur ^ 1;
-        // 1. g(p), g(r)
-        RotMaps m1;
-        m1.f0_feed = P.tt_plain[Plan::TF_P0 + cur];
-        m1.f1_feed = P.tt_plain[Plan::TF_R0 + cur];
-        m1.f0_ctr = P.tt_halo[Plan::TF_P0 + cur];
-        m1.f1_ctr = P.tt_halo[Plan::TF_R0 + cur];
-        m1.a = P.tt_plain[Plan::TF_A];
-        m1.b = P.tt_plain[Plan::TF_B];
-        m1.c = P.tt_plain[Plan::TF_C];
-        for (int f = 0; f < 2; ++f) {
-            rp.ag[f] = P.t_ag[f].as<float>();
-            rp.bg[f] = P.t_bg[f].as<float>();
-            rp.cg[f] = P.t_cg[f].as<float>();
-        }
-        rp.out_off = (long long)P.K * P.plane;
-        SFB_CUDA(v.rot(m1, rp, grid, P.s_main));
-        // 2. Hz(p), Hz(r)
+    rp.z_lo = lo;
+    rp.z_hi = hi;
+    rp.chunk = tti_part_chunk(P, 0, part, lo, hi);
+    for (int f = 0; f < 2; ++f) {
+        rp.ag[f] = P.t_ag[f].as<float>();
+        rp.bg[f] = P.t_bg[f].as<float>();
+        rp.cg[f] = P.t_cg[f].as<float>();
+    }
+    rp.out_off = (long long)P.K * P.plane;
+    RotMaps m1;
+    m1.f0_feed = P.tt_plain[Plan::TF_P0 + cur];
+    m1.f1_feed = P.tt_plain[Plan::TF_R0 + cur];
+    m1.f0_ctr = P.tt_halo[Plan::TF_P0 + cur];
+    m1.f1_ctr = P.tt_halo[Plan::TF_R0 + cur];
+    m1.a = P.tt_plain[Plan::TF_A];
+    m1.b = P.tt_plain[Plan::TF_B];
+    m1.c = P.tt_plain[Plan::TF_C];
+    cudaStream_t st = part_stream(P, part);
+    SFB_CUDA(v.rot(m1, rp, tti_grid(P, lo, hi, rp.chunk), st));
+    ++P.launches;
+    mark_stream(P, part);
+}
+
+// pass 2 and the update on the planes of `part`, then the point work of the part: Hz(p),
+// Hz(r) from the products (ghost planes of a g included), L(p), both leapfrog updates in
+// place over level t-1, injection into p and r, sampling of p
+void tti_update(Plan& P, long long t, int part) {
+    require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
+    int lo, hi;
+    part_range(P, part, lo, hi);
+    const TtiVariant& v = *P.tti_variant;
+    const int cur = int(t & 1), oth = cur ^ 1;
+    const int sepi = P.sep ? 1 : 0;
+    cudaStream_t st = part_stream(P, part);
+    if (hi > lo) {
+        DivParams dp{};
+        tti_coef(P, dp.k);
+        dp.N1 = int(P.N[1]);
+        dp.N2 = int(P.N[2]);
+        dp.pitch = P.pitch;
+        dp.plane = P.plane;
+        dp.z_lo = lo;
+        dp.z_hi = hi;
+        dp.chunk = tti_part_chunk(P, 1, part, lo, hi);
+        dp.out0 = P.t_hzp.as<float>();
+        dp.out1 = P.t_hzr.as<float>();
         DivMaps m2;
         m2.ag0 = P.tt_ag[0];
         m2.ag1 = P.tt_ag[1];
@@ -1103,10 +1118,21 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
         m2.bg1 = P.tt_bg[1];
         m2.cg0 = P.tt_cg[0];
         m2.cg1 = P.tt_cg[1];
-        dp.out0 = P.t_hzp.as<float>();
-        dp.out1 = P.t_hzr.as<float>();
-        SFB_CUDA(v.div(m2, dp, grid_div, P.s_main));
-        // 3. L(p), right-hand sides, leapfrog of both fields (in place over level t-1)
+        SFB_CUDA(v.div(m2, dp, tti_grid(P, lo, hi, dp.chunk), st));
+        UpdParams up{};
+        up.k = dp.k;
+        up.dz = P.dz.as<float>();
+        up.dy = P.dy.as<float>();
+        up.dx = P.dx.as<float>();
+        up.N1 = dp.N1;
+        up.N2 = dp.N2;
+        up.pitch = P.pitch;
+        up.plane = P.plane;
+        up.z_lo = lo;
+        up.z_hi = hi;
+        up.chunk = tti_part_chunk(P, 2, part, lo, hi);
+        up.po = P.u[oth].as<float>();
+        up.ro = P.t_r[oth].as<float>();
         UpdMaps m3;
         m3.p_feed = P.tt_plain[Plan::TF_P0 + cur];
         m3.p_ctr = P.tt_halo[Plan::TF_P0 + cur];
@@ -1119,14 +1145,35 @@ void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
         m3.hzp = P.tt_c[Plan::TC_HZP];
         m3.hzr = P.tt_c[Plan::TC_HZR];
         m3.d = P.tt_c[Plan::TC_DAMP];
-        up.po = P.u[oth].as<float>();
-        up.ro = P.t_r[oth].as<float>();
-        SFB_CUDA(v.upd[sepi](m3, up, grid_upd, P.s_main));
-        P.launches += 3;
-        step_points(P, op, t, SFB_PART_ALL);                                   // p: scatter + gather
-        step_points(P, op, t, SFB_PART_ALL, P.t_r[oth].as<float>(), false);    // r: scatter
+        SFB_CUDA(v.upd[sepi](m3, up, tti_grid(P, lo, hi, up.chunk), st));
+        P.launches += 2;
+        mark_stream(P, part);
+    }
+    if (part != SFB_PART_LOW) {
+        // HIGH (called after LOW) carries the point work of both boundary plane groups, so
+        // the injections land after both groups have been overwritten by the update
+        const int op = SFB_OP_TTI_FORWARD;
+        const int pp = part == SFB_PART_HIGH ? SFB_PART_LOW : part;
+        step_points(P, op, t, pp);                                    // p: scatter + gather
+        step_points(P, op, t, pp, P.t_r[oth].as<float>(), false);     // r: scatter
+    }
+    if (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) {
         P.live_level[cur] = t;
         P.live_level[oth] = t + 1;
+    }
+}
+
+void run_tti(Plan& P, sfb_report* rep, double* stream_out) {
+    require(P.n0 == P.N[0], SFB_ERR_CAPABILITY,
+            "sfb_tti_forward runs one whole domain; slabs step with sfb_tti_step_*");
+    tti_begin(P);
+    const long long nt = P.desc.nt;
+    std::unique_ptr<RowStreamer> rs;
+    if (stream_out) rs.reset(new RowStreamer(P, P.cloud[SFB_CLOUD_REC], stream_out));
+    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+    for (long long t = 1; t < nt - 1; ++t) {
+        tti_rot(P, t, SFB_PART_ALL);
+        tti_update(P, t, SFB_PART_ALL);
         if (rs) rs->row_done(t);
     }
     SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
@@ -1681,8 +1728,51 @@ SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* out) {
 SFB_API int sfb_step_begin(sfb_plan* plan, int op, int64_t save_every) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
+        if (op == SFB_OP_TTI_FORWARD) {
+            tti_begin(*plan);
+            return;
+        }
         if (op == SFB_OP_GRADIENT) save_every = plan->save_every;
         step_begin(*plan, op, save_every);
+    });
+}
+
+SFB_API int sfb_tti_step_rot(sfb_plan* plan, int64_t t, int part) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        require(plan->tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
+        tti_rot(*plan, t, part);
+    });
+}
+
+SFB_API int sfb_tti_step_update(sfb_plan* plan, int64_t t, int part) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        require(plan->tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
+        tti_update(*plan, t, part);
+    });
+}
+
+SFB_API int sfb_tti_halo_blocks(sfb_plan* plan, int which, int64_t t, void** send_lo,
+                                void** send_hi, void** recv_lo, void** recv_hi, int64_t* count) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(P.tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
+        float* u = nullptr;
+        switch (which) {
+        case SFB_TTI_HALO_AG_P: u = P.t_ag[0].as<float>(); break;
+        case SFB_TTI_HALO_AG_R: u = P.t_ag[1].as<float>(); break;
+        case SFB_TTI_HALO_P: u = P.u[(t + 1) & 1].as<float>(); break;
+        case SFB_TTI_HALO_R: u = P.t_r[(t + 1) & 1].as<float>(); break;
+        default: throw Failure(SFB_ERR_PARAMETER, "unknown TTI halo field");
+        }
+        const long long blk = (long long)P.K * P.plane;
+        if (recv_lo) *recv_lo = u;
+        if (send_lo) *send_lo = u + blk;
+        if (send_hi) *send_hi = u + (long long)P.n0 * P.plane;
+        if (recv_hi) *recv_hi = u + (long long)(P.n0 + P.K) * P.plane;
+        if (count) *count = blk;
     });
 }
 

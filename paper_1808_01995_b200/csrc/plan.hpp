@@ -161,6 +161,7 @@ struct Plan {
     enum { TC_RM, TC_E1, TC_E2, TC_HZP, TC_HZR, TC_DAMP, TC_COUNT };
     CUtensorMap tt_c[TC_COUNT];
     double w1[kMaxK + 1] = {0};                             // first-derivative weights
+    int tti_chunk[3] = {0, 0, 0};                           // d0 chunk of rot / div / update
 
     const StepVariant* variant = nullptr;       // chosen tile shape
     int chunk = 0;                              // output planes per block

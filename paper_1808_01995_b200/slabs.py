@@ -113,6 +113,35 @@ def step_loop(engine, exchanger: HaloExchanger, t_from: int, t_to: int, backward
             exchanger.finish(reqs)
 
 
+def tti_step_loop(engine, exchanger: HaloExchanger, t_from: int, t_to: int):
+    """Per-step protocol of the two-pass TTI operator (include/sfb200.h, "TTI slab
+    stepping"): the second pass differentiates the intermediate a*g along d0, so its K
+    boundary planes are exchanged between the passes -- SURVEY.md 8e's "extra exchange of
+    the intermediate" -- and the new p and r levels are exchanged at the end of the step,
+    overlapped with the interior update as in the acoustic loop.
+
+    `engine` provides rot(t) (first pass on every owned plane: the exchange that follows
+    needs all of it), update(part, t) with part in low/high/interior (update
+    "high" also does the point work of both boundary groups), blocks(which, t) for which in
+    ("ag_p", "ag_r", "p", "r"), the stream contexts boundary() / interior(), and
+    join(first, then): make stream `then` wait for the work queued on `first`."""
+    for t in range(t_from, t_to):
+        with engine.interior():
+            engine.rot(t)
+            for which in ("ag_p", "ag_r"):
+                exchanger.finish(exchanger.start(*engine.blocks(which, t)))
+        engine.join("interior", "boundary")
+        with engine.boundary():
+            engine.update("low", t)
+            engine.update("high", t)
+            reqs = exchanger.start(*engine.blocks("p", t)) + exchanger.start(*engine.blocks("r", t))
+        with engine.interior():
+            engine.update("interior", t)
+        with engine.boundary():
+            exchanger.finish(reqs)
+        engine.join("boundary", "interior")
+
+
 class _DeviceFloats:
     """Zero-copy torch view of `count` floats at a raw device pointer."""
 
@@ -162,6 +191,49 @@ class PlanEngine:
         key = (t + 1) & 1
         if key not in self._views:
             b = self.plan.halo_blocks(self.op, t)
+            dev = f"cuda:{self.device}"
+            self._views[key] = tuple(
+                self.torch.as_tensor(_DeviceFloats(b[k], b["count"]), device=dev)
+                for k in ("send_lo", "send_hi", "recv_lo", "recv_hi"))
+        return self._views[key]
+
+
+class TtiPlanEngine:
+    """tti_step_loop engine over one capi.Plan with the TTI fields bound."""
+
+    def __init__(self, plan, device):
+        import torch
+        from . import capi
+        self.torch, self.capi, self.plan, self.device = torch, capi, plan, device
+        self.s_main = torch.cuda.Stream(device=device)
+        self.s_bnd = torch.cuda.Stream(device=device, priority=-1)
+        plan._chk(capi.lib.sfb_set_streams(plan.h, self.s_main.cuda_stream, self.s_bnd.cuda_stream))
+        self._views = {}
+        self._part = {"low": capi.PART_LOW, "high": capi.PART_HIGH, "interior": capi.PART_INTERIOR}
+        self._which = {"ag_p": capi.TTI_HALO_AG_P, "ag_r": capi.TTI_HALO_AG_R,
+                       "p": capi.TTI_HALO_P, "r": capi.TTI_HALO_R}
+
+    def boundary(self):
+        return self.torch.cuda.stream(self.s_bnd)
+
+    def interior(self):
+        return self.torch.cuda.stream(self.s_main)
+
+    def join(self, first, then):
+        a = self.s_main if first == "interior" else self.s_bnd
+        b = self.s_main if then == "interior" else self.s_bnd
+        b.wait_stream(a)
+
+    def rot(self, t):
+        self.plan.tti_step_rot(t, self.capi.PART_ALL)
+
+    def update(self, part, t):
+        self.plan.tti_step_update(t, self._part[part])
+
+    def blocks(self, which, t):
+        key = (which, (t + 1) & 1 if which in ("p", "r") else 0)
+        if key not in self._views:
+            b = self.plan.tti_halo_blocks(self._which[which], t)
             dev = f"cuda:{self.device}"
             self._views[key] = tuple(
                 self.torch.as_tensor(_DeviceFloats(b[k], b["count"]), device=dev)

@@ -124,3 +124,96 @@ def test_tti_through_the_host_layer():
                                   1.2 * dt, 0.02)
     with pytest.raises(H.StabilityError):
         H.tti_forward_operator(model, tti, geom2, order)
+
+
+def _run_tti_slabs(model, geom, order, fields, cuts, overlap_parts=True):
+    """N TTI plans on one device stepping in lockstep with device-to-device ghost copies:
+    the single-GPU emulation of the two-exchange slab protocol (include/sfb200.h)."""
+    from paper_1808_01995_b200 import capi
+    plans = [make_plan(model, geom, order, slab=(cuts[i], cuts[i + 1])) for i in range(len(cuts) - 1)]
+    for p in plans:
+        p.set_model_tti(*fields)
+        p.upload_traces(capi.CLOUD_SRC, geom.src)
+        p.step_begin(capi.OP_TTI_FORWARD)
+
+    def exchange(which, t):
+        for p in plans:
+            p.sync()
+        for i in range(len(plans) - 1):
+            a, b = plans[i].tti_halo_blocks(which, t), plans[i + 1].tti_halo_blocks(which, t)
+            plans[i + 1].copy_halo(b["recv_lo"], a["send_hi"], a["count"])
+            plans[i].copy_halo(a["recv_hi"], b["send_lo"], a["count"])
+        for p in plans:
+            p.sync()
+
+    parts = ([capi.PART_LOW, capi.PART_HIGH, capi.PART_INTERIOR] if overlap_parts
+             else [capi.PART_ALL])
+    for t in range(1, geom.nt - 1):
+        for p in plans:
+            for part in parts:
+                p.tti_step_rot(t, part)
+        exchange(capi.TTI_HALO_AG_P, t)
+        exchange(capi.TTI_HALO_AG_R, t)
+        for p in plans:
+            for part in parts:
+                p.tti_step_update(t, part)
+        exchange(capi.TTI_HALO_P, t)
+        exchange(capi.TTI_HALO_R, t)
+    rec = np.zeros((geom.nt, geom.n_rec))
+    pf, rf = np.zeros(model.N), np.zeros(model.N)
+    for p in plans:
+        p.step_end(capi.OP_TTI_FORWARD)
+        rec += p.download_traces(capi.CLOUD_REC)
+        p.wavefield(geom.nt - 1, out=pf, field=0)
+        p.wavefield(geom.nt - 1, out=rf, field=1)
+        p.close()
+    return rec, pf, rf
+
+
+@pytest.mark.parametrize("order,parts", [(8, True), (8, False), (12, True)])
+def test_tti_slab_decomposition_matches_single_domain_bitwise(order, parts):
+    """SURVEY.md 8e for the TTI pair: slabs along d0 with K ghost planes of p and r plus one
+    exchange of the intermediate a g per step reproduce the single-domain run bit for bit
+    (receivers straddling the cuts, the source next to one)."""
+    model, geom = tti_problem([48, 26, 30], order, 40)
+    fields = tti_fields(model.N, seed=3)
+    plan = make_plan(model, geom, order)
+    plan.set_model_tti(*fields)
+    rec1, _ = plan.tti_forward(geom.src)
+    p1 = plan.wavefield(geom.nt - 1, field=0)
+    r1 = plan.wavefield(geom.nt - 1, field=1)
+    plan.close()
+    assert np.abs(rec1).max() > 0
+    n0 = model.N[0]
+    K = order // 2
+    src_plane = int(geom.src_base[0][0])
+    cuts = [0, 2 * K + 3, src_plane + 1, n0]      # the source cell straddles the second cut
+    rec3, p3, r3 = _run_tti_slabs(model, geom, order, fields, cuts, overlap_parts=parts)
+    assert np.array_equal(rec3, rec1)
+    assert np.array_equal(p3, p1) and np.array_equal(r3, r1)
+
+
+def test_tti_step_loop_engine_single_rank():
+    """slabs.tti_step_loop over slabs.TtiPlanEngine (two torch streams, the stream joins of
+    the protocol) at world size 1 equals sfb_tti_forward bit for bit."""
+    import torch
+    from paper_1808_01995_b200 import capi, slabs
+    model, geom = tti_problem([40, 26, 30], 8, 30)
+    fields = tti_fields(model.N, seed=5)
+    plan = make_plan(model, geom, 8)
+    plan.set_model_tti(*fields)
+    rec1, _ = plan.tti_forward(geom.src)
+    p1 = plan.wavefield(geom.nt - 1, field=0)
+    plan.close()
+    plan = make_plan(model, geom, 8)
+    plan.set_model_tti(*fields)
+    plan.upload_traces(capi.CLOUD_SRC, geom.src)
+    eng = slabs.TtiPlanEngine(plan, 0)
+    with eng.interior():
+        plan.step_begin(capi.OP_TTI_FORWARD)
+    slabs.tti_step_loop(eng, slabs.HaloExchanger(0, 1), 1, geom.nt - 1)
+    torch.cuda.synchronize()
+    plan.step_end(capi.OP_TTI_FORWARD)
+    assert np.array_equal(plan.download_traces(capi.CLOUD_REC), rec1)
+    assert np.array_equal(plan.wavefield(geom.nt - 1, field=0), p1)
+    plan.close()
