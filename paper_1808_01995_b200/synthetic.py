@@ -65,7 +65,32 @@ def config(number: int, n: int | None = None, nsteps: int | None = None):
         return dict(name=f"cfg5_acoustic_so16_{n}", shape=[n, n, n], h=h, nbl=40, order=16,
                     f0=0.015, velocity=lambda: smooth_field([n, n, n], SEED + 6, 8.0, 1.5, 4.5),
                     src=src, rec=receiver_grid(n, n, h, 25.0), tn=None, nsteps=nsteps or 1000)
-    raise ValueError(f"no acoustic config {number}")
+    if number == 4:
+        n = n or 512
+        h = 12.5
+        c = h * (n - 1) / 2.0 + h / 4.0
+        return dict(name=f"cfg4_tti_so12_{n}", shape=[n, n, n], h=h, nbl=40, order=12, f0=0.015,
+                    velocity=lambda: smooth_field([n, n, n], SEED + 1, 8.0, 1.5, 4.5),
+                    tti=lambda: tti_fields([n, n, n]), src=[[c, c, 18.75]],
+                    rec=receiver_grid(n, n, h, 25.0), tn=None, nsteps=nsteps or 500)
+    raise ValueError(f"no config {number}")
+
+
+def tti_fields(shape, sigma=8.0):
+    """Config 4's Thomsen parameters and angles: independent smooth
+    fields, epsilon in [0, 0.3], delta in [0, 0.2] clipped to delta <= epsilon (the
+    pseudo-acoustic system is ill-posed otherwise), tilt and azimuth
+    in [0, pi/4].  Physical extent; the caller extends them over the absorbing layer."""
+    eps = smooth_field(shape, SEED + 2, sigma, 0.0, 0.3)
+    delta = np.minimum(smooth_field(shape, SEED + 3, sigma, 0.0, 0.2), eps)
+    theta = smooth_field(shape, SEED + 4, sigma, 0.0, np.pi / 4)
+    phi = smooth_field(shape, SEED + 5, sigma, 0.0, np.pi / 4)
+    return eps, delta, theta, phi
+
+
+def extend(field, nbl):
+    """Edge-clamped extension over the absorbing layer (the rule of proj/src/model.cpp:92-100)."""
+    return np.pad(field, nbl, mode="edge")
 
 
 def time_axis(critical_dt, nsteps=None, tn=None):
