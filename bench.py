@@ -17,7 +17,9 @@ stream with all inputs resident in HBM; `e2e` is the same metric through the C-A
 sfb_forward with host buffers (source traces H2D, receiver traces D2H inside the timed
 region); `roofline` is the dense-update kernel alone; `cpu_baseline` is the f64 oracle on
 the host cores.  `--impl reference` times the CPU implementation (oracle/_ref when the
-reference's own sources were compiled here, else the oracle port).
+reference's own sources were compiled here, else the oracle port).  At N = 1 the line also
+carries `other_operators`: device-timed GPts/s of the adjoint, the gradient sweep and the TTI
+forward operator on the same grid (extras, not the contract metric; --no-other-ops skips them).
 """
 from __future__ import annotations
 
@@ -125,6 +127,55 @@ def make_plan(model, geom, device=0, slab=None):
     plan.set_points(capi.CLOUD_REC, np.array(geom.rec.base_table).reshape(-1, nd),
                     np.array(geom.rec.weight_table).reshape(-1, 8))
     return plan
+
+
+def other_operators(plan, geom, rec, model, device):
+    """Device-timed throughput of the other operators of the path on the same grid (not part
+    of the contract's metric; reported so that every operator has a number from this box):
+    adjoint and FWI-gradient sweep at order 8 on the bench plan, TTI forward at order 12
+    (config 4's size) on its own plan with cheap analytic Thomsen fields."""
+    from paper_1808_01995_b200 import capi
+    out = {"unit": "GPts/s", "grid": list(model.grid.shape)}
+    try:
+        plan.upload_traces(capi.CLOUD_REC, rec)
+        out["adjoint_so8"] = plan.run_resident(capi.OP_ADJOINT).gpts_per_s
+        se = max(4, -(-geom.nt // 100))
+        f = plan.run_resident(capi.OP_FORWARD, se)
+        g = plan.run_resident(capi.OP_GRADIENT)
+        out["forward_saving_so8"] = f.gpts_per_s
+        out["gradient_sweep_so8"] = g.gpts_per_s
+        out["gradient_images_every"] = se
+        out["gradient_roofline_28B"] = peaks()[0] / 28.0
+    except Exception as e:  # never lose the contract line over an extra
+        out["error_acoustic"] = repr(e)
+    try:
+        N = list(model.grid.shape)
+        steps = 20
+        lin = [np.linspace(0.0, 1.0, n) for n in N]
+        ones = np.ones(N)
+        eps = 0.3 * lin[0][:, None, None] * ones
+        delta = 0.2 * lin[1][None, :, None] * lin[0][:, None, None] * ones
+        theta = (np.pi / 4) * lin[2][None, None, :] * ones
+        phi = (np.pi / 4) * lin[1][None, :, None] * ones
+        dt = 0.9 * capi.critical_dt(list(model.grid.spacing), model.v_max, 12) / np.sqrt(1.6)
+        tp = capi.Plan(N, model.grid.spacing, 12, dt, steps + 2, device)
+        tp.set_model(model.m.array(), model.damp.array(), model.v_max)
+        tp.set_model_tti(eps, delta, theta, phi)
+        del eps, delta, theta, phi, ones
+        tp.set_points(capi.CLOUD_SRC, np.array(geom.src.base_table).reshape(-1, 3),
+                      np.array(geom.src.weight_table).reshape(-1, 8))
+        tp.set_points(capi.CLOUD_REC, np.array(geom.rec.base_table).reshape(-1, 3),
+                      np.array(geom.rec.weight_table).reshape(-1, 8))
+        tp.upload_traces(capi.CLOUD_SRC, np.sin(np.arange(steps + 2) * 0.1).reshape(-1, 1))
+        tp.run_resident(capi.OP_TTI_FORWARD)
+        r = tp.run_resident(capi.OP_TTI_FORWARD)
+        out["tti_forward_so12"] = r.gpts_per_s
+        out["tti_roofline_48B"] = peaks()[0] / 48.0
+        out["tti_tflops"] = r.gflops / 1e3
+        tp.close()
+    except Exception as e:
+        out["error_tti"] = repr(e)
+    return out
 
 
 def peaks():
@@ -294,6 +345,9 @@ def ours(args):
     e2e_s = time.perf_counter() - t0
     e2e = pts * K / e2e_s / 1e9
     assert np.isfinite(rec).all() and float(np.abs(rec).max()) > 0.0
+    other = None
+    if not args.no_other_ops:
+        other = other_operators(plan2, geom2, rec, model, local)
     plan2.close()
 
     # --- CPU baseline on this box's host cores (bounded sample) -------------------------
@@ -330,6 +384,8 @@ def ours(args):
         "gpu_launches": int(rep.kernel_launches),
         "clocks": clocks,
     }
+    if other is not None:
+        line["other_operators"] = other
     print(json.dumps(line), flush=True)
 
 
@@ -339,6 +395,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-other-ops", action="store_true",
+                    help="skip the adjoint / gradient / TTI extras of the JSON line")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.impl == "reference":
