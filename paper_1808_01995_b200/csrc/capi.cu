@@ -992,8 +992,7 @@ void tti_make_maps(Plan& P) {
         encode_map(&P.tt_cg[f], P.t_cg[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.box_w,
                    v.tile_y);
     }
-    void* cf[Plan::TC_COUNT] = {P.r.p, P.t_e1.p, P.t_e2.p, P.t_hzp.p, P.t_hzr.p,
-                                P.sep ? P.r.p : P.damp.p};
+    void* cf[Plan::TC_COUNT] = {P.r.p, P.t_e1.p, P.t_e2.p, P.t_lp.p, P.sep ? P.r.p : P.damp.p};
     for (int i = 0; i < Plan::TC_COUNT; ++i)
         encode_map(&P.tt_c[i], cf[i], P.N[2], P.N[1], P.n0, P.pitch, P.plane, v.tile_x, v.tile_y);
 }
@@ -1035,9 +1034,8 @@ void tti_begin(Plan& P) {
         SFB_CUDA(cudaMemsetAsync(d->p, 0, size_t(P.ucount) * 4, P.s_main));
     const TtiVariant& v = *P.tti_variant;
     const int sepi = P.sep ? 1 : 0;
-    P.tti_chunk[0] = tti_chunk_for(P, v.f_rot, v.rot_threads, v.smem_rot);
-    P.tti_chunk[1] = tti_chunk_for(P, v.f_div, v.rot_threads, v.smem_div);
-    P.tti_chunk[2] = tti_chunk_for(P, v.f_upd[sepi], v.upd_threads, v.smem_upd[sepi]);
+    P.tti_chunk[0] = tti_chunk_for(P, v.f_rot, v.threads, v.smem_rot);
+    P.tti_chunk[1] = tti_chunk_for(P, v.f_div[sepi], v.threads, v.smem_div[sepi]);
 }
 
 dim3 tti_grid(const Plan& P, int lo, int hi, int chunk) {
@@ -1073,6 +1071,7 @@ void tti_rot(Plan& P, long long t, int part) {
         rp.bg[f] = P.t_bg[f].as<float>();
         rp.cg[f] = P.t_cg[f].as<float>();
     }
+    rp.lp = P.t_lp.as<float>();
     rp.out_off = (long long)P.K * P.plane;
     RotMaps m1;
     m1.f0_feed = P.tt_plain[Plan::TF_P0 + cur];
@@ -1102,6 +1101,9 @@ void tti_update(Plan& P, long long t, int part) {
     if (hi > lo) {
         DivParams dp{};
         tti_coef(P, dp.k);
+        dp.dz = P.dz.as<float>();
+        dp.dy = P.dy.as<float>();
+        dp.dx = P.dx.as<float>();
         dp.N1 = int(P.N[1]);
         dp.N2 = int(P.N[2]);
         dp.pitch = P.pitch;
@@ -1109,8 +1111,8 @@ void tti_update(Plan& P, long long t, int part) {
         dp.z_lo = lo;
         dp.z_hi = hi;
         dp.chunk = tti_part_chunk(P, 1, part, lo, hi);
-        dp.out0 = P.t_hzp.as<float>();
-        dp.out1 = P.t_hzr.as<float>();
+        dp.po = P.u[oth].as<float>();
+        dp.ro = P.t_r[oth].as<float>();
         DivMaps m2;
         m2.ag0 = P.tt_ag[0];
         m2.ag1 = P.tt_ag[1];
@@ -1118,35 +1120,17 @@ void tti_update(Plan& P, long long t, int part) {
         m2.bg1 = P.tt_bg[1];
         m2.cg0 = P.tt_cg[0];
         m2.cg1 = P.tt_cg[1];
-        SFB_CUDA(v.div(m2, dp, tti_grid(P, lo, hi, dp.chunk), st));
-        UpdParams up{};
-        up.k = dp.k;
-        up.dz = P.dz.as<float>();
-        up.dy = P.dy.as<float>();
-        up.dx = P.dx.as<float>();
-        up.N1 = dp.N1;
-        up.N2 = dp.N2;
-        up.pitch = P.pitch;
-        up.plane = P.plane;
-        up.z_lo = lo;
-        up.z_hi = hi;
-        up.chunk = tti_part_chunk(P, 2, part, lo, hi);
-        up.po = P.u[oth].as<float>();
-        up.ro = P.t_r[oth].as<float>();
-        UpdMaps m3;
-        m3.p_feed = P.tt_plain[Plan::TF_P0 + cur];
-        m3.p_ctr = P.tt_halo[Plan::TF_P0 + cur];
-        m3.po = P.tt_plain[Plan::TF_P0 + oth];
-        m3.ro = P.tt_plain[Plan::TF_R0 + oth];
-        m3.rc = P.tt_plain[Plan::TF_R0 + cur];
-        m3.rm = P.tt_c[Plan::TC_RM];
-        m3.e1 = P.tt_c[Plan::TC_E1];
-        m3.e2 = P.tt_c[Plan::TC_E2];
-        m3.hzp = P.tt_c[Plan::TC_HZP];
-        m3.hzr = P.tt_c[Plan::TC_HZR];
-        m3.d = P.tt_c[Plan::TC_DAMP];
-        SFB_CUDA(v.upd[sepi](m3, up, tti_grid(P, lo, hi, up.chunk), st));
-        P.launches += 2;
+        m2.lp = P.tt_c[Plan::TC_LP];
+        m2.po = P.tt_plain[Plan::TF_P0 + oth];
+        m2.ro = P.tt_plain[Plan::TF_R0 + oth];
+        m2.pc = P.tt_plain[Plan::TF_P0 + cur];
+        m2.rc = P.tt_plain[Plan::TF_R0 + cur];
+        m2.rm = P.tt_c[Plan::TC_RM];
+        m2.e1 = P.tt_c[Plan::TC_E1];
+        m2.e2 = P.tt_c[Plan::TC_E2];
+        m2.d = P.tt_c[Plan::TC_DAMP];
+        SFB_CUDA(v.div[sepi](m2, dp, tti_grid(P, lo, hi, dp.chunk), st));
+        ++P.launches;
         mark_stream(P, part);
     }
     if (part != SFB_PART_LOW) {
@@ -1489,7 +1473,7 @@ SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
         for (DevBuf* d : {&P.t_a, &P.t_b, &P.t_c, &P.t_ag[0], &P.t_ag[1], &P.t_bg[0], &P.t_bg[1],
                           &P.t_cg[0], &P.t_cg[1]})
             d->alloc(size_t(P.ucount) * 4);
-        for (DevBuf* d : {&P.t_e1, &P.t_e2, &P.t_hzp, &P.t_hzr}) d->alloc(size_t(P.ccount) * 4);
+        for (DevBuf* d : {&P.t_e1, &P.t_e2, &P.t_lp}) d->alloc(size_t(P.ccount) * 4);
         P.tti_variant = nullptr;
         for (const TtiVariant& tv : tti_variant_registry())
             if (tv.K == P.K) P.tti_variant = &tv;
@@ -1497,14 +1481,10 @@ SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
         SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_rot,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(P.tti_variant->smem_rot)));
-        SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_div,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(P.tti_variant->smem_div)));
-        for (int i = 0; i < 2; ++i) {
-            SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_upd[i],
+        for (int i = 0; i < 2; ++i)
+            SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_div[i],
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(P.tti_variant->smem_upd[i])));
-        }
+                                          int(P.tti_variant->smem_div[i])));
         tti_make_maps(P);
         const long long rows = (long long)P.n0 * P.N[1];
         tti_setup_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(

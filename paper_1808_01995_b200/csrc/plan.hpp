@@ -150,7 +150,7 @@ struct Plan {
 
     // TTI operator state (builder-defined formulation, csrc/tti_kernels.cuh)
     bool tti_set = false;
-    DevBuf t_r[2], t_a, t_b, t_c, t_e1, t_e2, t_hzp, t_hzr;  // p lives in u[2]
+    DevBuf t_r[2], t_a, t_b, t_c, t_e1, t_e2, t_lp;  // p lives in u[2]; t_lp = L(p)
     DevBuf t_ag[2], t_bg[2], t_cg[2];   // a g, b g, c g of p and r between the two passes
     const TtiVariant* tti_variant = nullptr;
     // tensor maps for the TTI tile: wavefield-layout fields (haloed / plain box) ...
@@ -158,10 +158,10 @@ struct Plan {
     CUtensorMap tt_halo[TF_COUNT], tt_plain[TF_COUNT];
     CUtensorMap tt_ag[2], tt_bg[2], tt_cg[2];   // plain / d1-haloed / d2-haloed boxes
     // ... and compact fields (plain box)
-    enum { TC_RM, TC_E1, TC_E2, TC_HZP, TC_HZR, TC_DAMP, TC_COUNT };
+    enum { TC_RM, TC_E1, TC_E2, TC_LP, TC_DAMP, TC_COUNT };
     CUtensorMap tt_c[TC_COUNT];
     double w1[kMaxK + 1] = {0};                             // first-derivative weights
-    int tti_chunk[3] = {0, 0, 0};                           // d0 chunk of rot / div / update
+    int tti_chunk[2] = {0, 0};                              // d0 chunk of the two launches
 
     const StepVariant* variant = nullptr;       // chosen tile shape
     int chunk = 0;                              // output planes per block
