@@ -198,9 +198,14 @@ class Plan:
         self.np[cloud] = base.shape[0]
         self._chk(lib.sfb_set_points(self.h, cloud, base.shape[0], base.ctypes.data, w.ctypes.data))
 
-    def forward(self, src, save_every=0):
+    def forward(self, src, save_every=0, out=None):
+        """out: optional C-contiguous f64 [nt][n_rec] table to fill (the reference's callers
+        own their trace tables, proj/include/sf/sparse.hpp:46-49); allocated when omitted."""
         src = np.ascontiguousarray(src, dtype=np.float64)
-        rec = np.empty((self.nt, self.np[CLOUD_REC]))
+        rec = np.empty((self.nt, self.np[CLOUD_REC])) if out is None else out
+        if rec.shape != (self.nt, self.np[CLOUD_REC]) or rec.dtype != np.float64 \
+                or not rec.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 [nt][n_rec] array")
         rep = Report()
         self._chk(lib.sfb_forward(self.h, src.ctypes.data, rec.ctypes.data, save_every, C.byref(rep)))
         return rec, rep
