@@ -205,14 +205,14 @@ SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* grad);
  * fill; each is `*count` contiguous floats. */
 SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, void** send_hi,
                     void** recv_lo, void** recv_hi, int64_t* count);
-/* ---- TTI slab stepping.  One step of a slab is: sfb_tti_step_rot(part) (pass 1: the
- * products a g, b g, c g on the owned planes; needs the ghost planes of p and r), the
- * caller's exchange of the K boundary planes of a g (SFB_TTI_HALO_AG_P / _AG_R),
+/* ---- TTI slab stepping.  One step of a slab is: sfb_tti_step_rot(part) (pass 1: g,
+ * b g and L(p) on the owned planes; needs the ghost planes of p and r), the
+ * caller's exchange of the K boundary planes of g (SFB_TTI_HALO_G_P / _G_R),
  * sfb_tti_step_update(part) (pass 2 + update + scatter/gather; call LOW before HIGH: HIGH
  * carries the point work of both boundary groups), the caller's exchange of the new p and r levels
  * (SFB_TTI_HALO_P / _R).  SURVEY.md 8e: "an extra exchange of the intermediate".
  * sfb_step_begin(SFB_OP_TTI_FORWARD) zeroes the state, sfb_step_end closes the run. */
-enum { SFB_TTI_HALO_AG_P = 0, SFB_TTI_HALO_AG_R = 1, SFB_TTI_HALO_P = 2, SFB_TTI_HALO_R = 3 };
+enum { SFB_TTI_HALO_G_P = 0, SFB_TTI_HALO_G_R = 1, SFB_TTI_HALO_P = 2, SFB_TTI_HALO_R = 3 };
 SFB_API int sfb_tti_step_rot(sfb_plan* plan, int64_t t, int part);
 SFB_API int sfb_tti_step_update(sfb_plan* plan, int64_t t, int part);
 SFB_API int sfb_tti_halo_blocks(sfb_plan* plan, int which, int64_t t, void** send_lo,

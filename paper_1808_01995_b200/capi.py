@@ -19,7 +19,7 @@ lib = C.CDLL(LIB_PATH)
 OK, ERR_PARAMETER, ERR_STABILITY, ERR_LOCATION, ERR_CAPABILITY, ERR_BINDING, ERR_CUDA, ERR_ORDER = range(8)
 CLOUD_SRC, CLOUD_REC = 0, 1
 OP_FORWARD, OP_ADJOINT, OP_GRADIENT, OP_TTI_FORWARD = 0, 1, 2, 3
-TTI_HALO_AG_P, TTI_HALO_AG_R, TTI_HALO_P, TTI_HALO_R = 0, 1, 2, 3
+TTI_HALO_G_P, TTI_HALO_G_R, TTI_HALO_P, TTI_HALO_R = 0, 1, 2, 3
 PART_ALL, PART_LOW, PART_HIGH, PART_INTERIOR = 0, 1, 2, 3
 
 

@@ -197,14 +197,14 @@ IntView embed_view(const Plan& P, const double* ptr, const int64_t* stride) {
     return v;
 }
 
-// owned planes of a strided host f64 field -> compact device f64 [n0][N1][N2]
-void upload_f64(Plan& P, const IntView& v, DevBuf& tmp) {
+// planes [gz0, gz0 + cnt) of a strided host f64 field -> compact device f64 [cnt][N1][N2]
+void upload_f64_planes(Plan& P, const IntView& v, DevBuf& tmp, long long gz0, long long cnt) {
     const size_t rowb = size_t(P.N[2]) * 8;
-    tmp.alloc(size_t(P.n0) * P.N[1] * rowb, false);
+    tmp.alloc(size_t(cnt) * P.N[1] * rowb, false);
     double* d = tmp.as<double>();
     if (v.s[2] == 1 || P.N[2] == 1) {
-        for (long long z = 0; z < P.n0; ++z) {
-            const double* src = v.ptr + (P.z_lo + z) * v.s[0];
+        for (long long z = 0; z < cnt; ++z) {
+            const double* src = v.ptr + (gz0 + z) * v.s[0];
             const size_t spitch = P.N[1] > 1 ? size_t(v.s[1]) * 8 : rowb;
             SFB_CUDA(cudaMemcpy2DAsync(d + z * P.N[1] * P.N[2], rowb, src, spitch, rowb,
                                        size_t(P.N[1]), cudaMemcpyHostToDevice, P.s_main));
@@ -212,15 +212,20 @@ void upload_f64(Plan& P, const IntView& v, DevBuf& tmp) {
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
     } else {
         std::vector<double> row(size_t(P.N[1]) * P.N[2]);
-        for (long long z = 0; z < P.n0; ++z) {
+        for (long long z = 0; z < cnt; ++z) {
             for (long long j = 0; j < P.N[1]; ++j)
                 for (long long l = 0; l < P.N[2]; ++l)
-                    row[j * P.N[2] + l] = v.ptr[(P.z_lo + z) * v.s[0] + j * v.s[1] + l * v.s[2]];
+                    row[j * P.N[2] + l] = v.ptr[(gz0 + z) * v.s[0] + j * v.s[1] + l * v.s[2]];
             SFB_CUDA(cudaMemcpyAsync(d + z * P.N[1] * P.N[2], row.data(), row.size() * 8,
                                      cudaMemcpyHostToDevice, P.s_main));
             SFB_CUDA(cudaStreamSynchronize(P.s_main));
         }
     }
+}
+
+// owned planes of a strided host f64 field -> compact device f64 [n0][N1][N2]
+void upload_f64(Plan& P, const IntView& v, DevBuf& tmp) {
+    upload_f64_planes(P, v, tmp, P.z_lo, P.n0);
 }
 
 // compact device f64 [n0][N1][N2] -> owned planes of a strided host f64 field
@@ -983,15 +988,16 @@ void tti_make_maps(Plan& P) {
         encode_map(&P.tt_plain[i], wf[i], P.N[2], P.N[1], P.n0 + 2 * P.K, P.pitch, P.plane,
                    v.tile_x, v.tile_y);
     }
+    const long long n0g = P.n0 + 2 * P.K;
     for (int f = 0; f < 2; ++f) {
-        const long long n0g = P.n0 + 2 * P.K;
-        encode_map(&P.tt_ag[f], P.t_ag[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.tile_x,
+        encode_map(&P.tt_g[f], P.t_g[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.tile_x,
                    v.tile_y);
         encode_map(&P.tt_bg[f], P.t_bg[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.tile_x,
                    v.box_h);
-        encode_map(&P.tt_cg[f], P.t_cg[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.box_w,
+        encode_map(&P.tt_gx[f], P.t_g[f].p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.box_w,
                    v.tile_y);
     }
+    encode_map(&P.tt_cx, P.t_c.p, P.N[2], P.N[1], n0g, P.pitch, P.plane, v.box_w, v.tile_y);
     void* cf[Plan::TC_COUNT] = {P.r.p, P.t_e1.p, P.t_e2.p, P.t_lp.p, P.sep ? P.r.p : P.damp.p};
     for (int i = 0; i < Plan::TC_COUNT; ++i)
         encode_map(&P.tt_c[i], cf[i], P.N[2], P.N[1], P.n0, P.pitch, P.plane, v.tile_x, v.tile_y);
@@ -1030,7 +1036,7 @@ void tti_begin(Plan& P) {
     step_begin(P, SFB_OP_TTI_FORWARD, 0);
     for (int b = 0; b < 2; ++b)
         SFB_CUDA(cudaMemsetAsync(P.t_r[b].p, 0, size_t(P.ucount) * 4, P.s_main));
-    for (DevBuf* d : {&P.t_ag[0], &P.t_ag[1], &P.t_bg[0], &P.t_bg[1], &P.t_cg[0], &P.t_cg[1]})
+    for (DevBuf* d : {&P.t_g[0], &P.t_g[1], &P.t_bg[0], &P.t_bg[1]})
         SFB_CUDA(cudaMemsetAsync(d->p, 0, size_t(P.ucount) * 4, P.s_main));
     const TtiVariant& v = *P.tti_variant;
     const int sepi = P.sep ? 1 : 0;
@@ -1067,9 +1073,8 @@ void tti_rot(Plan& P, long long t, int part) {
     rp.z_hi = hi;
     rp.chunk = tti_part_chunk(P, 0, part, lo, hi);
     for (int f = 0; f < 2; ++f) {
-        rp.ag[f] = P.t_ag[f].as<float>();
+        rp.g[f] = P.t_g[f].as<float>();
         rp.bg[f] = P.t_bg[f].as<float>();
-        rp.cg[f] = P.t_cg[f].as<float>();
     }
     rp.lp = P.t_lp.as<float>();
     rp.out_off = (long long)P.K * P.plane;
@@ -1114,12 +1119,14 @@ void tti_update(Plan& P, long long t, int part) {
         dp.po = P.u[oth].as<float>();
         dp.ro = P.t_r[oth].as<float>();
         DivMaps m2;
-        m2.ag0 = P.tt_ag[0];
-        m2.ag1 = P.tt_ag[1];
+        m2.g0 = P.tt_g[0];
+        m2.g1 = P.tt_g[1];
+        m2.a = P.tt_plain[Plan::TF_A];
         m2.bg0 = P.tt_bg[0];
         m2.bg1 = P.tt_bg[1];
-        m2.cg0 = P.tt_cg[0];
-        m2.cg1 = P.tt_cg[1];
+        m2.g0x = P.tt_gx[0];
+        m2.g1x = P.tt_gx[1];
+        m2.cx = P.tt_cx;
         m2.lp = P.tt_c[Plan::TC_LP];
         m2.po = P.tt_plain[Plan::TF_P0 + oth];
         m2.ro = P.tt_plain[Plan::TF_R0 + oth];
@@ -1470,8 +1477,7 @@ SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
         upload_f64(P, embed_view(P, theta->ptr, theta->stride), tt);
         upload_f64(P, embed_view(P, phi->ptr, phi->stride), tph);
         for (int b = 0; b < 2; ++b) P.t_r[b].alloc(size_t(P.ucount) * 4);
-        for (DevBuf* d : {&P.t_a, &P.t_b, &P.t_c, &P.t_ag[0], &P.t_ag[1], &P.t_bg[0], &P.t_bg[1],
-                          &P.t_cg[0], &P.t_cg[1]})
+        for (DevBuf* d : {&P.t_a, &P.t_b, &P.t_c, &P.t_g[0], &P.t_g[1], &P.t_bg[0], &P.t_bg[1]})
             d->alloc(size_t(P.ucount) * 4);
         for (DevBuf* d : {&P.t_e1, &P.t_e2, &P.t_lp}) d->alloc(size_t(P.ccount) * 4);
         P.tti_variant = nullptr;
@@ -1492,6 +1498,22 @@ SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
             P.t_b.as<float>(), P.t_c.as<float>(), P.t_e1.as<float>(), P.t_e2.as<float>(), rows,
             int(P.N[2]), P.pitch, (long long)P.K * P.plane);
         SFB_CUDA(cudaGetLastError());
+        // a slab's second pass forms a g on the ghost planes of g too: the axis component a
+        // is static, so its ghost planes are filled here from the caller's global arrays
+        for (int side = 0; side < 2; ++side) {
+            const long long g0 = side == 0 ? std::max<long long>(0, P.z_lo - P.K) : P.z_hi;
+            const long long g1 = side == 0 ? P.z_lo : std::min<long long>(P.N[0], P.z_hi + P.K);
+            if (g1 <= g0) continue;
+            DevBuf gt, gp;
+            upload_f64_planes(P, embed_view(P, theta->ptr, theta->stride), gt, g0, g1 - g0);
+            upload_f64_planes(P, embed_view(P, phi->ptr, phi->stride), gp, g0, g1 - g0);
+            const long long grow = (g1 - g0) * P.N[1];
+            tti_axis_a_kernel<<<row_grid(P, grow), 256, 0, P.s_main>>>(
+                gt.as<double>(), gp.as<double>(), P.t_a.as<float>(), grow, int(P.N[2]), P.pitch,
+                (g0 - P.z_lo + P.K) * P.plane);
+            SFB_CUDA(cudaGetLastError());
+            SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        }
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
         P.tti_set = true;
     });
@@ -1741,8 +1763,8 @@ SFB_API int sfb_tti_halo_blocks(sfb_plan* plan, int which, int64_t t, void** sen
         require(P.tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
         float* u = nullptr;
         switch (which) {
-        case SFB_TTI_HALO_AG_P: u = P.t_ag[0].as<float>(); break;
-        case SFB_TTI_HALO_AG_R: u = P.t_ag[1].as<float>(); break;
+        case SFB_TTI_HALO_G_P: u = P.t_g[0].as<float>(); break;
+        case SFB_TTI_HALO_G_R: u = P.t_g[1].as<float>(); break;
         case SFB_TTI_HALO_P: u = P.u[(t + 1) & 1].as<float>(); break;
         case SFB_TTI_HALO_R: u = P.t_r[(t + 1) & 1].as<float>(); break;
         default: throw Failure(SFB_ERR_PARAMETER, "unknown TTI halo field");

@@ -151,12 +151,12 @@ struct Plan {
     // TTI operator state (builder-defined formulation, csrc/tti_kernels.cuh)
     bool tti_set = false;
     DevBuf t_r[2], t_a, t_b, t_c, t_e1, t_e2, t_lp;  // p lives in u[2]; t_lp = L(p)
-    DevBuf t_ag[2], t_bg[2], t_cg[2];   // a g, b g, c g of p and r between the two passes
+    DevBuf t_g[2], t_bg[2];             // g and b g of p and r between the two passes
     const TtiVariant* tti_variant = nullptr;
     // tensor maps for the TTI tile: wavefield-layout fields (haloed / plain box) ...
     enum { TF_P0, TF_P1, TF_R0, TF_R1, TF_A, TF_B, TF_C, TF_COUNT };
     CUtensorMap tt_halo[TF_COUNT], tt_plain[TF_COUNT];
-    CUtensorMap tt_ag[2], tt_bg[2], tt_cg[2];   // plain / d1-haloed / d2-haloed boxes
+    CUtensorMap tt_g[2], tt_bg[2], tt_gx[2], tt_cx;   // plain / d1-haloed / d2-haloed boxes
     // ... and compact fields (plain box)
     enum { TC_RM, TC_E1, TC_E2, TC_LP, TC_DAMP, TC_COUNT };
     CUtensorMap tt_c[TC_COUNT];

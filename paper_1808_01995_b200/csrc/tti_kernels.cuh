@@ -11,12 +11,12 @@
 //
 // One time step is two launches, both streamed along d0 with TMA boxes, shared-memory
 // stage rings and register queues exactly like the acoustic kernel (acoustic_kernel.cuh):
-//   1. tti_rot_kernel: g(p), g(r), written as the products a g, b g, c g, and L(p)
+//   1. tti_rot_kernel: g(p), g(r) -- stored as g and the product b g -- and L(p)
 //   2. tti_div_update_kernel: Hz(p), Hz(r) -- each product differentiated along its own
 //      axis -- the two right-hand sides and both leapfrog updates
 // In both kernels the two fields are handled by two groups of consumer warps of the same
 // block ("field-parallel warps"): each thread carries the d0 queue of ONE field.  The
-// products and L(p) go through HBM once (48 + 64 = 112 bytes per node against the 48 of a
+// intermediates and L(p) go through HBM once (40 + 64 = 104 bytes per node against the 48 of a
 // fully fused kernel); keeping g on chip needs a (2K+1)-plane ring of a haloed region per
 // field, which does not fit in 227 KB at order 12 -- see DESIGN.md section 3.4.
 #pragma once
@@ -45,9 +45,8 @@ struct RotMaps {
 
 struct RotParams {
     TtiCoef k;
-    float* ag[2];       // a g, b g, c g of field 0 / field 1 (wavefield layout)
+    float* g[2];        // g and b g of field 0 / field 1 (wavefield layout)
     float* bg[2];
-    float* cg[2];
     float* lp;          // L(field 0) (compact layout): its operands are all on chip here
     long long out_off;  // element offset of local plane 0 inside the outputs
     int N1, N2, pitch;
@@ -142,9 +141,8 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
     const bool rin = x < p.N2 && y < p.N1;
     const bool lane0 = (tid & 31) == 0;
     long long go = p.out_off + (long long)zb * p.plane + (long long)y * p.pitch + x;
-    float* const oa = p.ag[field];
+    float* const og = p.g[field];
     float* const ob = p.bg[field];
-    float* const oc = p.cg[field];
     long long lo_off = (long long)zb * p.plane + (long long)y * p.pitch + x;   // compact
 
     float q[Q][4];
@@ -266,13 +264,11 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                     if (LAP)
                         __stcs(reinterpret_cast<float4*>(p.lp + lo_off),
                                make_float4(lap[0], lap[1], lap[2], lap[3]));
-                    // the second pass differentiates each product along one axis only
-                    __stcs(reinterpret_cast<float4*>(oa + go),
-                           make_float4(a4.x * g[0], a4.y * g[1], a4.z * g[2], a4.w * g[3]));
+                    // the second pass needs b g at 2K neighbours per node (the expensive
+                    // product: stored); a g and c g are rebuilt there from g
+                    __stcs(reinterpret_cast<float4*>(og + go), make_float4(g[0], g[1], g[2], g[3]));
                     __stcs(reinterpret_cast<float4*>(ob + go),
                            make_float4(b4.x * g[0], b4.y * g[1], b4.z * g[2], b4.w * g[3]));
-                    __stcs(reinterpret_cast<float4*>(oc + go),
-                           make_float4(c4.x * g[0], c4.y * g[1], c4.z * g[2], c4.w * g[3]));
                 }
             };
             if (field == 0)   // warp-uniform
@@ -290,15 +286,16 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
 }
 
 // ---- pass 2 + update ------------------------------------------------------------------
-// Hz(f) = D0(a g) + D1(b g) + D2(c g) for f = p (warp group 0) and f = r (group 1), then the
+// Hz(f) = D0(a g) + D1(b g) + D2(c g) for f = p (warp group 0) and f = r (group 1) -- a g is
+// formed when a plane of g enters the register queue, c g along the row segment -- then the
 // point-wise rest of the step in the same threads: the groups swap Hz(p) / Hz(r) through
 // the feed boxes of the stage they have just consumed, form the two right-hand sides from
 // L(p) (written by pass 1) and update p (group 0) and r (group 1) in place.
 
 struct DivMaps {
-    CUtensorMap ag0, ag1;   // plain box (feeds the d0 queue)
-    CUtensorMap bg0, bg1;   // box with a d1 halo only
-    CUtensorMap cg0, cg1;   // box with a d2 halo only
+    CUtensorMap g0, g1, a;      // plain boxes of the newest plane: a g feeds the d0 queue
+    CUtensorMap bg0, bg1;       // box with a d1 halo only
+    CUtensorMap g0x, g1x, cx;   // g and c in a box with a d2 halo only
     CUtensorMap lp, po, ro, pc, rc, rm, e1, e2, d;   // plain boxes of the output plane
 };
 
@@ -323,8 +320,8 @@ struct DivShape {
     static constexpr int XBOX = SW * TY;            // d2-haloed box
     static constexpr int XPAD = ((XBOX + 31) / 32) * 32;
     static constexpr int NPL = SEP ? 8 : 9;         // lp po ro pc rc rm e1 e2 (damp)
-    // stage: feed ag0, ag1 | bg0, bg1 | cg0, cg1 | plain boxes
-    static constexpr int STAGE = 2 * ABOX + 2 * YBOX + 2 * XPAD + NPL * ABOX;
+    // stage: feed g0, g1, a | bg0, bg1 | g0x, g1x, cx | plain boxes
+    static constexpr int STAGE = 3 * ABOX + 2 * YBOX + 3 * XPAD + NPL * ABOX;
     static constexpr int GROUP = TXV * TY;
     static constexpr int NTHREADS = 2 * GROUP + 32;
     static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8 + 128;
@@ -338,7 +335,7 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
     constexpr int KP = S::KP, SW = S::SW, STAGE = S::STAGE, Q = 2 * K + 1;
     constexpr int ABOX = S::ABOX, YBOX = S::YBOX, XPAD = S::XPAD, TX = S::TX, NPL = S::NPL;
     constexpr int NCW = 2 * S::GROUP / 32;
-    constexpr int OFF_Y = 2 * ABOX, OFF_X = OFF_Y + 2 * YBOX, OFF_P = OFF_X + 2 * XPAD;
+    constexpr int OFF_Y = 3 * ABOX, OFF_X = OFF_Y + 2 * YBOX, OFF_P = OFF_X + 3 * XPAD;
     enum { A_LP, A_PO, A_RO, A_PC, A_RC, A_RM, A_E1, A_E2, A_D };
 
     extern __shared__ unsigned char smem_raw[];
@@ -372,16 +369,18 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
                 const bool out = n >= 2 * K;
                 float* st = ring + s * STAGE;
                 mbar_arrive_expect_tx(
-                    full + s, (2 * ABOX + (out ? 2 * YBOX + 2 * S::XBOX + NPL * ABOX : 0)) * 4);
-                tma_load_3d(st, &tm.ag0, x0, y0, zb + n, full + s);
-                tma_load_3d(st + ABOX, &tm.ag1, x0, y0, zb + n, full + s);
+                    full + s, (3 * ABOX + (out ? 2 * YBOX + 3 * S::XBOX + NPL * ABOX : 0)) * 4);
+                tma_load_3d(st, &tm.g0, x0, y0, zb + n, full + s);
+                tma_load_3d(st + ABOX, &tm.g1, x0, y0, zb + n, full + s);
+                tma_load_3d(st + 2 * ABOX, &tm.a, x0, y0, zb + n, full + s);
                 if (out) {
                     const int zo = zb + n - 2 * K;  // output plane (compact); buffer plane zo + K
                     const int zc = zo + K;
                     tma_load_3d(st + OFF_Y, &tm.bg0, x0, y0 - K, zc, full + s);
                     tma_load_3d(st + OFF_Y + YBOX, &tm.bg1, x0, y0 - K, zc, full + s);
-                    tma_load_3d(st + OFF_X, &tm.cg0, x0 - KP, y0, zc, full + s);
-                    tma_load_3d(st + OFF_X + XPAD, &tm.cg1, x0 - KP, y0, zc, full + s);
+                    tma_load_3d(st + OFF_X, &tm.g0x, x0 - KP, y0, zc, full + s);
+                    tma_load_3d(st + OFF_X + XPAD, &tm.g1x, x0 - KP, y0, zc, full + s);
+                    tma_load_3d(st + OFF_X + 2 * XPAD, &tm.cx, x0 - KP, y0, zc, full + s);
                     float* ad = st + OFF_P;
                     tma_load_3d(ad + A_LP * ABOX, &tm.lp, x0, y0, zo, full + s);
                     tma_load_3d(ad + A_PO * ABOX, &tm.po, x0, y0, zc, full + s);
@@ -433,7 +432,12 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
         mbar_wait(full + s, fph);
         float* st = ring + s * STAGE;
         {
-            const float4 v = *reinterpret_cast<const float4*>(st + field * ABOX + aown);
+            float4 v = *reinterpret_cast<const float4*>(st + field * ABOX + aown);
+            const float4 a4 = *reinterpret_cast<const float4*>(st + 2 * ABOX + aown);
+            v.x *= a4.x;   // the queue holds a g
+            v.y *= a4.y;
+            v.z *= a4.z;
+            v.w *= a4.w;
 #pragma unroll
             for (int j = 0; j < Q - 1; ++j)
 #pragma unroll
@@ -468,16 +472,18 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
                 }
             }
             float d2[4] = {0.f, 0.f, 0.f, 0.f};
-            {   // D2 (c g): one aligned row segment of the d2-haloed box
+            {   // D2 (c g): one aligned row segment of g and of c in the d2-haloed boxes
                 float xr[2 * KP + 4];
                 const float* rowp = st + OFF_X + field * XPAD + ty * SW + 4 * tx;
+                const float* crow = st + OFF_X + 2 * XPAD + ty * SW + 4 * tx;
 #pragma unroll
                 for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
                     const float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
-                    xr[4 * v + 0] = t4.x;
-                    xr[4 * v + 1] = t4.y;
-                    xr[4 * v + 2] = t4.z;
-                    xr[4 * v + 3] = t4.w;
+                    const float4 n4 = *reinterpret_cast<const float4*>(crow + 4 * v);
+                    xr[4 * v + 0] = t4.x * n4.x;
+                    xr[4 * v + 1] = t4.y * n4.y;
+                    xr[4 * v + 2] = t4.z * n4.z;
+                    xr[4 * v + 3] = t4.w * n4.w;
                 }
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
@@ -557,6 +563,20 @@ static __global__ void tti_setup_kernel(const double* __restrict__ eps, const do
         c[ghost_off + d] = (float)ct;
         e1[d] = (float)(1.0 + 2.0 * eps[s]);
         e2[d] = (float)sqrt(1.0 + 2.0 * delta[s]);
+    }
+}
+
+// a = sin(theta) cos(phi) on extra planes (the ghost planes of a slab)
+static __global__ void tti_axis_a_kernel(const double* __restrict__ theta,
+                                         const double* __restrict__ phi, float* a, long long rows,
+                                         int n2, int pitch, long long off) {
+    const long long row = blockIdx.y * (long long)gridDim.z + blockIdx.z;
+    if (row >= rows) return;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n2; x += gridDim.x * blockDim.x) {
+        double st, ct, sp, cp;
+        sincos(theta[row * n2 + x], &st, &ct);
+        sincos(phi[row * n2 + x], &sp, &cp);
+        a[off + row * pitch + x] = (float)(st * cp);
     }
 }
 

@@ -123,12 +123,12 @@ def tti_step_loop(engine, exchanger: HaloExchanger, t_from: int, t_to: int):
     `engine` provides rot(t) (first pass on every owned plane: the exchange that follows
     needs all of it), update(part, t) with part in low/high/interior (update
     "high" also does the point work of both boundary groups), blocks(which, t) for which in
-    ("ag_p", "ag_r", "p", "r"), the stream contexts boundary() / interior(), and
+    ("g_p", "g_r", "p", "r"), the stream contexts boundary() / interior(), and
     join(first, then): make stream `then` wait for the work queued on `first`."""
     for t in range(t_from, t_to):
         with engine.interior():
             engine.rot(t)
-            for which in ("ag_p", "ag_r"):
+            for which in ("g_p", "g_r"):
                 exchanger.finish(exchanger.start(*engine.blocks(which, t)))
         engine.join("interior", "boundary")
         with engine.boundary():
@@ -210,7 +210,7 @@ class TtiPlanEngine:
         plan._chk(capi.lib.sfb_set_streams(plan.h, self.s_main.cuda_stream, self.s_bnd.cuda_stream))
         self._views = {}
         self._part = {"low": capi.PART_LOW, "high": capi.PART_HIGH, "interior": capi.PART_INTERIOR}
-        self._which = {"ag_p": capi.TTI_HALO_AG_P, "ag_r": capi.TTI_HALO_AG_R,
+        self._which = {"g_p": capi.TTI_HALO_G_P, "g_r": capi.TTI_HALO_G_R,
                        "p": capi.TTI_HALO_P, "r": capi.TTI_HALO_R}
 
     def boundary(self):

@@ -152,8 +152,8 @@ def _run_tti_slabs(model, geom, order, fields, cuts, overlap_parts=True):
         for p in plans:
             for part in parts:
                 p.tti_step_rot(t, part)
-        exchange(capi.TTI_HALO_AG_P, t)
-        exchange(capi.TTI_HALO_AG_R, t)
+        exchange(capi.TTI_HALO_G_P, t)
+        exchange(capi.TTI_HALO_G_R, t)
         for p in plans:
             for part in parts:
                 p.tti_step_update(t, part)

@@ -192,7 +192,7 @@ class TwoPassEngine:
                     self.rec[t, i] = 0.4 * cur[c, y, x] + 0.6 * cur[c + 1, y, x]
 
     def blocks(self, which, t):
-        u = self.g[which[3:]] if which.startswith("ag_") else self.f[which][(t + 1) & 1]
+        u = self.g[which[2:]] if which.startswith("g_") else self.f[which][(t + 1) & 1]
         n0 = self.n0
         f = torch.from_numpy
         return f(u[K:2 * K]), f(u[n0:n0 + K]), f(u[0:K]), f(u[n0 + K:n0 + 2 * K])
