@@ -89,33 +89,33 @@ std::shared_ptr<Function> build_damping(const std::shared_ptr<Grid>& grid, long 
 SeismicModel::SeismicModel(std::vector<long> shape, std::vector<double> spacing,
                            std::vector<double> origin, const std::vector<double>& velocity,
                            long nbl, int space_order, DampProfile profile)
-    : shape_(std::move(shape)), spacing_(std::move(spacing)), origin_(std::move(origin)),
-      nbl_(nbl), space_order_(space_order) {
-    if (shape_.empty() || shape_.size() != spacing_.size() || shape_.size() != origin_.size())
+    : box_(std::move(shape)), h_(std::move(spacing)), corner_(std::move(origin)),
+      layer_(nbl), order_(space_order) {
+    if (box_.empty() || box_.size() != h_.size() || box_.size() != corner_.size())
         throw ParameterError("SeismicModel: rank mismatch");
-    if (nbl_ < 0) throw ParameterError("SeismicModel: nbl must be >= 0");
-    std::vector<long> padded(shape_);
-    std::vector<double> porigin(origin_);
-    for (std::size_t d = 0; d < shape_.size(); ++d) {
-        padded[d] += 2 * nbl_;
-        porigin[d] -= double(nbl_) * spacing_[d];
+    if (layer_ < 0) throw ParameterError("SeismicModel: nbl must be >= 0");
+    std::vector<long> padded(box_);
+    std::vector<double> porigin(corner_);
+    for (std::size_t d = 0; d < box_.size(); ++d) {
+        padded[d] += 2 * layer_;
+        porigin[d] -= double(layer_) * h_[d];
     }
-    grid_ = std::make_shared<Grid>(padded, spacing_, porigin);
-    m_ = Function::create("m", grid_, space_order_);
+    padded_grid_ = std::make_shared<Grid>(padded, h_, porigin);
+    slowness2_ = Function::create("m", padded_grid_, order_);
     set_velocity(velocity);
-    damp_ = build_damping(grid_, nbl_, v_max_, profile, space_order_);
+    absorber_ = build_damping(padded_grid_, layer_, vel_hi_, profile, order_);
 }
 
 // edge-clamped extension p = clamp(idx - nbl, 0, n-1), proj/src/model.cpp:92-100
 template <typename Fn>
 void SeismicModel::extend_into_layer(Fn&& value_of_physical_cell) {
-    const View3 v(*m_);
-    const int off = 3 - int(shape_.size());
+    const View3 v(*slowness2_);
+    const int off = 3 - int(box_.size());
     long pn[3] = {1, 1, 1};
     std::vector<long> tab[3];
     for (int a = 0; a < 3; ++a) {
-        if (a >= off) pn[a] = shape_[std::size_t(a - off)];
-        tab[a] = clamp_table(v.n[a], a >= off ? nbl_ : 0, pn[a]);
+        if (a >= off) pn[a] = box_[std::size_t(a - off)];
+        tab[a] = clamp_table(v.n[a], a >= off ? layer_ : 0, pn[a]);
     }
 #pragma omp parallel for collapse(2) schedule(static)
     for (long i = 0; i < v.n[0]; ++i)
@@ -131,20 +131,20 @@ void SeismicModel::extend_into_layer(Fn&& value_of_physical_cell) {
 
 void SeismicModel::set_velocity(const std::vector<double>& velocity) {
     std::size_t n = 1;
-    for (long e : shape_) n *= std::size_t(e);
+    for (long e : box_) n *= std::size_t(e);
     if (velocity.size() != n) throw ParameterError("SeismicModel: velocity size does not match shape");
     for (double v : velocity)
         if (!(v > 0.0)) throw ParameterError("SeismicModel: velocity must be positive");
     auto [lo, hi] = std::minmax_element(velocity.begin(), velocity.end());
-    v_min_ = *lo;
-    v_max_ = *hi;
+    vel_lo_ = *lo;
+    vel_hi_ = *hi;
     extend_into_layer([&](std::size_t flat) { return 1.0 / (velocity[flat] * velocity[flat]); });
 }
 
 // proj/src/model.cpp:103-111 (arithmetic behind the C-ABI)
 double SeismicModel::critical_dt(int space_order, double gamma) const {
     double out = 0;
-    int rc = sfb_critical_dt(int(shape_.size()), spacing_.data(), v_max_, space_order, &out);
+    int rc = sfb_critical_dt(int(box_.size()), h_.data(), vel_hi_, space_order, &out);
     if (rc == SFB_ERR_PARAMETER) {
         check_space_order(space_order);
         throw OrderError("critical_dt: unsupported space order");
@@ -154,12 +154,12 @@ double SeismicModel::critical_dt(int space_order, double gamma) const {
 }
 
 std::vector<double> SeismicModel::physical_m() const {
-    const View3 v(*m_);
-    const int off = 3 - int(shape_.size());
+    const View3 v(*slowness2_);
+    const int off = 3 - int(box_.size());
     long pn[3] = {1, 1, 1}, pad[3] = {0, 0, 0};
     for (int a = off; a < 3; ++a) {
-        pn[a] = shape_[std::size_t(a - off)];
-        pad[a] = nbl_;
+        pn[a] = box_[std::size_t(a - off)];
+        pad[a] = layer_;
     }
     std::vector<double> out(std::size_t(pn[0]) * std::size_t(pn[1]) * std::size_t(pn[2]));
     for (long i = 0; i < pn[0]; ++i)
@@ -173,15 +173,15 @@ std::vector<double> SeismicModel::physical_m() const {
 // proj/src/model.cpp:124-147: values stored verbatim, velocity statistics through sqrt
 void SeismicModel::set_physical_m(const std::vector<double>& m_values) {
     std::size_t n = 1;
-    for (long e : shape_) n *= std::size_t(e);
+    for (long e : box_) n *= std::size_t(e);
     if (m_values.size() != n) throw ParameterError("SeismicModel: m size does not match shape");
     for (double mv : m_values)
         if (!(mv > 0.0)) throw ParameterError("SeismicModel: m must be positive");
-    v_min_ = v_max_ = 1.0 / std::sqrt(m_values[0]);
+    vel_lo_ = vel_hi_ = 1.0 / std::sqrt(m_values[0]);
     for (double mv : m_values) {
         const double v = 1.0 / std::sqrt(mv);
-        v_min_ = std::min(v_min_, v);
-        v_max_ = std::max(v_max_, v);
+        vel_lo_ = std::min(vel_lo_, v);
+        vel_hi_ = std::max(vel_hi_, v);
     }
     extend_into_layer([&](std::size_t flat) { return m_values[flat]; });
 }
@@ -215,7 +215,7 @@ double dgauss4_value(double fp, double t) {
 AcquisitionGeometry::AcquisitionGeometry(const SeismicModel& model, std::vector<double> src_coords,
                                          std::vector<double> rec_coords, double t0, double tn,
                                          double dt, double f0)
-    : t0_(t0), tn_(tn), dt_(dt), f0_(f0) {
+    : axis_{t0, tn, dt, 0}, peak_freq_(f0) {
     if (!(dt > 0.0) || !(tn > t0)) throw ParameterError("AcquisitionGeometry: bad time axis");
     if (dt > model.critical_dt() * (1.0 + 1e-12))
         throw StabilityError("AcquisitionGeometry: dt exceeds the stable limit " +
@@ -224,16 +224,16 @@ AcquisitionGeometry::AcquisitionGeometry(const SeismicModel& model, std::vector<
     if (src_coords.empty() || src_coords.size() % rank != 0 || rec_coords.empty() ||
         rec_coords.size() % rank != 0)
         throw ParameterError("AcquisitionGeometry: coordinate list rank mismatch");
-    n_src_ = long(src_coords.size() / rank);
-    n_rec_ = long(rec_coords.size() / rank);
-    nt_ = long(std::floor((tn - t0) / dt)) + 1;
-    src_ = SparseFunction::create("src", model.grid(), std::move(src_coords), nt_);
-    rec_ = SparseFunction::create("rec", model.grid(), std::move(rec_coords), nt_);
-    src_->locate();
-    rec_->locate();
-    const std::vector<double> w = ricker(f0, t0, dt, nt_);
-    for (long t = 0; t < nt_; ++t)
-        for (long p = 0; p < n_src_; ++p) src_->trace(t, p) = w[std::size_t(t)];
+    count_[0] = long(src_coords.size() / rank);
+    count_[1] = long(rec_coords.size() / rank);
+    axis_.nt = long(std::floor((tn - t0) / dt)) + 1;
+    cloud_[0] = SparseFunction::create("src", model.grid(), std::move(src_coords), axis_.nt);
+    cloud_[1] = SparseFunction::create("rec", model.grid(), std::move(rec_coords), axis_.nt);
+    cloud_[0]->locate();
+    cloud_[1]->locate();
+    const std::vector<double> w = ricker(f0, t0, dt, axis_.nt);
+    for (long t = 0; t < axis_.nt; ++t)
+        for (long p = 0; p < count_[0]; ++p) cloud_[0]->trace(t, p) = w[std::size_t(t)];
 }
 
 }  // namespace sfb
