@@ -143,3 +143,42 @@ def test_short_oracle_anchor_on_the_full_grid(full):
     assert rel_l2(rec, ref["smp"]) <= 1e-5
     assert rel_l2(plan.wavefield(og.nt - 1), ref["final"]) <= 1e-5
     plan.close()
+
+
+def test_tti_properties_at_full_size(full):
+    """Config 4's grid (592^3, order 12): the f64 oracle cannot run it in seconds, so the TTI
+    pair is checked through size-independent properties -- linearity in the source, zero in /
+    zero out, and the isotropic limit p == r."""
+    from paper_1808_01995_b200 import capi
+    model, geom0 = full
+    N = list(model.grid.shape)
+    steps = 24
+    lin = [np.linspace(0.0, 1.0, n) for n in N]
+    ones = np.ones(N)
+    eps = 0.3 * lin[0][:, None, None] * ones
+    delta = 0.2 * lin[1][None, :, None] * lin[0][:, None, None] * ones      # <= eps
+    theta = (np.pi / 4) * lin[2][None, None, :] * ones
+    phi = (np.pi / 4) * lin[1][None, :, None] * ones
+    dt = 0.9 * capi.critical_dt(list(model.grid.spacing), model.v_max, 12) / np.sqrt(1.6)
+    plan = capi.Plan(N, model.grid.spacing, 12, dt, steps + 2)
+    plan.set_model(model.m.array(), model.damp.array(), model.v_max)
+    plan.set_points(capi.CLOUD_SRC, np.array(geom0.src.base_table).reshape(-1, 3),
+                    np.array(geom0.src.weight_table).reshape(-1, 8))
+    plan.set_points(capi.CLOUD_REC, np.array(geom0.rec.base_table).reshape(-1, 3),
+                    np.array(geom0.rec.weight_table).reshape(-1, 8))
+    plan.set_model_tti(eps, delta, theta, phi)
+    src = np.sin(np.arange(steps + 2) * 0.3).reshape(-1, 1)
+    rec, rep = plan.tti_forward(src)
+    assert rep.steps == steps and np.isfinite(rec).all() and np.abs(rec).max() > 0
+    rec2, _ = plan.tti_forward(2.0 * src)
+    assert rel_l2(rec2, 2.0 * rec) <= 1e-7
+    zero, _ = plan.tti_forward(np.zeros_like(src))
+    assert (zero == 0.0).all()
+    # isotropic limit: the two fields of the pair coincide bit for bit
+    z = np.zeros(N)
+    plan.set_model_tti(z, z, z, z)
+    plan.tti_forward(src)
+    p = plan.wavefield(steps + 1, field=0)
+    r = plan.wavefield(steps + 1, field=1)
+    assert np.abs(p).max() > 0 and np.array_equal(p, r)
+    plan.close()
