@@ -62,6 +62,8 @@ struct StepParams {
     long long plane;     // floats per plane
     int z_lo, z_hi;      // owned output planes [z_lo, z_hi) handled by this launch
     int chunk;           // output planes per block
+    int z_jump;          // extra plane offset of blocks with blockIdx.z >= 1 (0 = contiguous):
+                         // one launch covers the two boundary plane groups of a slab
 };
 
 // the tensor maps of one launch: u[t] with halo box (u) and with plain box (f); u[t-1], r,
@@ -341,7 +343,7 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
 
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int zb = p.z_lo + blockIdx.z * p.chunk;
+    const int zb = p.z_lo + blockIdx.z * p.chunk + (blockIdx.z ? p.z_jump : 0);
     const int ze = min(zb + p.chunk, p.z_hi);
     const int nplanes = (ze - zb) + 2 * K;  // u buffer planes zb .. ze+2K-1 (ghost offset K)
 
@@ -532,7 +534,7 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
 
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int zb = p.z_lo + blockIdx.z * p.chunk;
+    const int zb = p.z_lo + blockIdx.z * p.chunk + (blockIdx.z ? p.z_jump : 0);
     const int ze = min(zb + p.chunk, p.z_hi);
     const int nplanes = (ze - zb) + 2 * K;
 

@@ -561,6 +561,8 @@ void step_begin(Plan& P, int op, long long save_every) {
     P.main_pending = P.bnd_pending = false;
 }
 
+constexpr int kPartBoundaryPair = 100;   // internal: LOW and HIGH plane groups in one launch
+
 void part_range(const Plan& P, int part, int& lo, int& hi) {
     const int K = P.K, n0 = P.n0;
     switch (part) {
@@ -573,7 +575,7 @@ void part_range(const Plan& P, int part, int& lo, int& hi) {
 }
 
 cudaStream_t part_stream(Plan& P, int part) {
-    const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH;
+    const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartBoundaryPair;
     cudaStream_t st = bnd ? P.s_bnd : P.s_main;
     // the other stream's last work of the previous step wrote planes this launch reads
     if (bnd && P.main_pending) {
@@ -588,7 +590,7 @@ cudaStream_t part_stream(Plan& P, int part) {
 }
 
 void mark_stream(Plan& P, int part) {
-    const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH;
+    const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartBoundaryPair;
     if (P.s_bnd == P.s_main) return;
     if (bnd) {
         SFB_CUDA(cudaEventRecord(P.ev_bnd, P.s_bnd));
@@ -611,7 +613,13 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex =
     const OpRoles ro = roles(op);
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;
-    part_range(P, part, lo, hi);
+    const bool pair = part == kPartBoundaryPair;   // needs n0 >= 2K (split_slabs guarantees it)
+    if (pair) {
+        lo = 0;
+        hi = P.n0;
+    } else {
+        part_range(P, part, lo, hi);
+    }
     if (hi <= lo) return;
     const int cur = int(t & 1), oth = cur ^ 1;
     const long long tnew = ro.backward ? t - 1 : t + 1;
@@ -627,7 +635,9 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex =
     sp.plane = P.plane;
     sp.z_lo = lo;
     sp.z_hi = hi;
-    sp.chunk = (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? P.chunk : (hi - lo);
+    sp.chunk = pair ? P.K
+                    : (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? P.chunk : (hi - lo);
+    sp.z_jump = pair ? P.n0 - 2 * P.K : 0;   // block z = 1 starts at plane n0 - K
     if (ex) {
         sp.snap = ex->snap;
         sp.usave = ex->usave;
@@ -643,7 +653,7 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex =
     const StepVariant& v = *P.variant;
     dim3 grid(unsigned((P.N[2] + v.tile_x - 1) / v.tile_x),
               unsigned((P.N[1] + v.tile_y - 1) / v.tile_y),
-              unsigned((hi - lo + sp.chunk - 1) / sp.chunk));
+              pair ? 2u : unsigned((hi - lo + sp.chunk - 1) / sp.chunk));
     cudaStream_t st = part_stream(P, part);
     StepMaps maps;
     const bool alt = ex && ex->alt;
@@ -1791,8 +1801,12 @@ SFB_API int sfb_step_points(sfb_plan* plan, int op, int64_t t, int part) {
 SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
-        step_compute(*plan, op, t, SFB_PART_LOW);
-        step_compute(*plan, op, t, SFB_PART_HIGH);
+        if (plan->n0 >= 2 * plan->K) {
+            step_compute(*plan, op, t, kPartBoundaryPair);   // both plane groups, one launch
+        } else {
+            step_compute(*plan, op, t, SFB_PART_LOW);
+            step_compute(*plan, op, t, SFB_PART_HIGH);
+        }
         step_points(*plan, op, t, SFB_PART_LOW);
     });
 }

@@ -255,7 +255,8 @@ def test_unstable_dt_and_nan_guard():
     plan2.close()
 
 
-def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_forward=False):
+def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_forward=False,
+               fused=False):
     """N plans on one device stepping in lockstep with device-to-device ghost copies:
     the single-GPU emulation of the multi-GPU slab protocol.  Returns the summed sampled
     traces, the assembled last level and (gradient) the assembled grad."""
@@ -271,6 +272,10 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
         ts = range(geom.nt - 2, 0, -1) if o != capi.OP_FORWARD else range(1, geom.nt - 1)
         for t in ts:
             for p in plans:
+                if fused:   # the two native half-step calls of slabs.PlanEngine
+                    p.step_slab_boundary(o, t)
+                    p.step_slab_interior(o, t)
+                    continue
                 p.step_compute(o, t, capi.PART_LOW)
                 p.step_compute(o, t, capi.PART_HIGH)
                 p.step_points(o, t, capi.PART_LOW)
@@ -307,14 +312,15 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
     return rec, u, grad
 
 
-def test_slab_decomposition_matches_single_domain_bitwise():
+@pytest.mark.parametrize("fused", [False, True])
+def test_slab_decomposition_matches_single_domain_bitwise(fused):
     model, geom = make_problem([48, 30, 34], 10.0, 8, 8, 60)
     plan = make_plan(model, geom, 8)
     rec1, _ = plan.forward(geom.src)
     u1 = plan.wavefield(geom.nt - 1)
     plan.close()
     n0 = model.N[0]
-    rec3, u3, _ = _run_slabs(model, geom, 8, [0, 20, 41, n0])
+    rec3, u3, _ = _run_slabs(model, geom, 8, [0, 20, 41, n0], fused=fused)
     assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
 
 
@@ -330,11 +336,13 @@ def test_slab_decomposition_adjoint_and_gradient_bitwise():
     g1, _ = plan.gradient(data)
     plan.close()
     n0 = model.N[0]
-    srca3, v3, _ = _run_slabs(model, geom, 8, [0, 20, 41, n0], op=capi.OP_ADJOINT, inj=data)
-    assert np.array_equal(srca3, srca1) and np.array_equal(v3, v1)
-    _, _, g3 = _run_slabs(model, geom, 8, [0, 20, 41, n0], op=capi.OP_GRADIENT, save_every=2,
-                          inj=data, prior_forward=True)
-    assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
+    for fused in (False, True):
+        srca3, v3, _ = _run_slabs(model, geom, 8, [0, 20, 41, n0], op=capi.OP_ADJOINT, inj=data,
+                                  fused=fused)
+        assert np.array_equal(srca3, srca1) and np.array_equal(v3, v1)
+        _, _, g3 = _run_slabs(model, geom, 8, [0, 20, 41, n0], op=capi.OP_GRADIENT, save_every=2,
+                              inj=data, prior_forward=True, fused=fused)
+        assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
 
 
 def test_step_loop_engine_on_one_rank_matches_forward():
