@@ -44,7 +44,7 @@ struct PointParams {
 constexpr int kPointThreads = 128;
 
 // blocks [0, nb_inj) scatter, the rest gather
-__global__ void __launch_bounds__(kPointThreads)
+static __global__ void __launch_bounds__(kPointThreads)
 point_step_kernel(const __grid_constant__ PointParams p, int nb_inj) {
     if ((int)blockIdx.x < nb_inj) {
         const int i = blockIdx.x * kPointThreads + threadIdx.x;
@@ -78,7 +78,7 @@ point_step_kernel(const __grid_constant__ PointParams p, int nb_inj) {
 // ---- setup / conversion kernels ------------------------------------------------------
 
 // r = dt^2 / m evaluated in f64, stored fp32 in the pitched device layout
-__global__ void convert_r_kernel(const double* __restrict__ m, float* __restrict__ r,
+static __global__ void convert_r_kernel(const double* __restrict__ m, float* __restrict__ r,
                                  long long rows, int n2, int pitch, double dt2) {
     const long long row = blockIdx.y * (long long)gridDim.z + blockIdx.z;
     if (row >= rows) return;
@@ -86,7 +86,7 @@ __global__ void convert_r_kernel(const double* __restrict__ m, float* __restrict
         r[row * pitch + x] = (float)(dt2 / m[row * n2 + x]);
 }
 
-__global__ void convert_f64_f32_pitched(const double* __restrict__ src, float* __restrict__ dst,
+static __global__ void convert_f64_f32_pitched(const double* __restrict__ src, float* __restrict__ dst,
                                         long long rows, int n2, int pitch) {
     const long long row = blockIdx.y * (long long)gridDim.z + blockIdx.z;
     if (row >= rows) return;
@@ -94,7 +94,7 @@ __global__ void convert_f64_f32_pitched(const double* __restrict__ src, float* _
         dst[row * pitch + x] = (float)src[row * n2 + x];
 }
 
-__global__ void convert_f32_pitched_f64(const float* __restrict__ src, double* __restrict__ dst,
+static __global__ void convert_f32_pitched_f64(const float* __restrict__ src, double* __restrict__ dst,
                                         long long rows, int n2, int pitch) {
     const long long row = blockIdx.y * (long long)gridDim.z + blockIdx.z;
     if (row >= rows) return;
@@ -102,14 +102,14 @@ __global__ void convert_f32_pitched_f64(const float* __restrict__ src, double* _
         dst[row * n2 + x] = (double)src[row * pitch + x];
 }
 
-__global__ void convert_f64_f32_flat(const double* __restrict__ src, float* __restrict__ dst,
+static __global__ void convert_f64_f32_flat(const double* __restrict__ src, float* __restrict__ dst,
                                      long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         dst[i] = (float)src[i];
 }
 
-__global__ void convert_f32_f64_flat(const float* __restrict__ src, double* __restrict__ dst,
+static __global__ void convert_f32_f64_flat(const float* __restrict__ src, double* __restrict__ dst,
                                      long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
@@ -118,7 +118,7 @@ __global__ void convert_f32_f64_flat(const float* __restrict__ src, double* __re
 
 // NaN/Inf guard of the reference engines (proj/src/execute.cpp:397-417,
 // proj/src/emit.cpp:333-341): flag = 1 if any value is non-finite
-__global__ void finite_check_kernel(const float* __restrict__ a, long long n, int* flag) {
+static __global__ void finite_check_kernel(const float* __restrict__ a, long long n, int* flag) {
     int bad = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
