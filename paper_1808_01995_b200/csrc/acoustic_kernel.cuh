@@ -100,6 +100,15 @@ __device__ __forceinline__ void mbar_release(uint64_t* bar, float dep) {
                      smem_u32(bar) + (__float_as_uint(dep) & zero))
                  : "memory");
 }
+// Programmatic dependent launch: the kernels of the time loop are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel may start (barrier set-up,
+// parameter loads) while its predecessor in the stream drains.  pdl_enter() lets the NEXT
+// kernel start early and then waits until every earlier kernel has completed and its writes
+// are visible: nothing a predecessor wrote may be touched before it.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar), ok;
     do {
@@ -355,6 +364,7 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_enter();
 
     if (tid >= S::NCONS) {
         // ---- producer warp: one lane streams the planes of this block ----------------
@@ -547,6 +557,7 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_enter();
 
     if (tid >= S::NCONS) {
         if (tid == S::NCONS) {

@@ -86,6 +86,9 @@ cudaStream_t part_stream(Plan& P, int part) {
 }
 
 void mark_stream(Plan& P, int part) {
+    // whole-domain launches have no other stream to order against, and an event record
+    // between two kernels would break their programmatic dependent launch
+    if (part == SFB_PART_ALL) return;
     const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartBoundaryPair;
     if (P.s_bnd == P.s_main) return;
     if (bnd) {
@@ -234,8 +237,8 @@ void step_points(Plan& P, int op, long long t, int part, float* target_override,
         }
         const int nb_inj = int((ncell + kPointThreads - 1) / kPointThreads);
         if (nb_inj + nb_smp == 0) continue;
-        point_step_kernel<<<nb_inj + nb_smp, kPointThreads, 0, st>>>(pp, nb_inj);
-        SFB_CUDA(cudaGetLastError());
+        SFB_CUDA(launch_pdl(&point_step_kernel, dim3(unsigned(nb_inj + nb_smp)), kPointThreads, 0, st,
+                            pp, nb_inj));
         ++P.launches;
     }
     mark_stream(P, part);

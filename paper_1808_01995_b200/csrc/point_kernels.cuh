@@ -46,6 +46,9 @@ constexpr int kPointThreads = 128;
 // blocks [0, nb_inj) scatter, the rest gather
 static __global__ void __launch_bounds__(kPointThreads)
 point_step_kernel(const __grid_constant__ PointParams p, int nb_inj) {
+    // launched with programmatic stream serialization (see pdl_enter in acoustic_kernel.cuh)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if ((int)blockIdx.x < nb_inj) {
         const int i = blockIdx.x * kPointThreads + threadIdx.x;
         if (i >= p.ncell) return;

@@ -102,6 +102,7 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_enter();
 
     if (tid >= 2 * S::GROUP) {
         if (tid == 2 * S::GROUP) {
@@ -359,6 +360,7 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_enter();
 
     if (tid >= 2 * S::GROUP) {
         if (tid == 2 * S::GROUP) {

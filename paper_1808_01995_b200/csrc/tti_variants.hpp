@@ -3,6 +3,7 @@
 
 #include <vector>
 
+#include "launch.hpp"
 #include "tti_kernels.cuh"
 
 namespace sfb {
@@ -35,16 +36,14 @@ std::vector<TtiVariant>& tti_variant_registry();
 template <int K>
 cudaError_t launch_rot(const RotMaps& tm, const RotParams& p, dim3 grid, cudaStream_t st) {
     using S = RotShape<K, kTtiTXV, kTtiTY, kTtiNS>;
-    tti_rot_kernel<K, kTtiTXV, kTtiTY, kTtiNS><<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
-    return cudaGetLastError();
+    return launch_pdl(&tti_rot_kernel<K, kTtiTXV, kTtiTY, kTtiNS>, grid, S::NTHREADS, S::SMEM, st, tm, p);
 }
 
 template <int K, bool SEP>
 cudaError_t launch_div(const DivMaps& tm, const DivParams& p, dim3 grid, cudaStream_t st) {
     using S = DivShape<K, kTtiTXV, kTtiTY, kTtiNSDiv, SEP>;
-    tti_div_update_kernel<K, kTtiTXV, kTtiTY, kTtiNSDiv, SEP>
-        <<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
-    return cudaGetLastError();
+    return launch_pdl(&tti_div_update_kernel<K, kTtiTXV, kTtiTY, kTtiNSDiv, SEP>, grid, S::NTHREADS,
+                      S::SMEM, st, tm, p);
 }
 
 template <int K>

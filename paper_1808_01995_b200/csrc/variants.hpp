@@ -4,9 +4,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <utility>
 #include <vector>
 
 #include "acoustic_kernel.cuh"
+#include "launch.hpp"
 
 namespace sfb {
 
@@ -29,8 +31,8 @@ std::vector<StepVariant>& step_variant_registry();
 template <int K, int TXV, int TY, int NST, bool SEP>
 cudaError_t launch_step(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
     using S = StepShape<K, TXV, TY, NST, SEP>;
-    acoustic_step_kernel<K, TXV, TY, NST, SEP><<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
-    return cudaGetLastError();
+    return launch_pdl(&acoustic_step_kernel<K, TXV, TY, NST, SEP>, grid, S::NTHREADS, S::SMEM, st,
+                      tm, p);
 }
 
 template <int K, int TXV, int TY, int NST, bool SEP>
@@ -50,9 +52,8 @@ void register_step() {
 template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROT>
 cudaError_t launch_dual(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
     using S = DualShape<K, TXV, TY, NS, SEP>;
-    acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT>
-        <<<grid, S::NTHREADS, S::SMEM, st>>>(tm, p);
-    return cudaGetLastError();
+    return launch_pdl(&acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT>, grid, S::NTHREADS,
+                      S::SMEM, st, tm, p);
 }
 
 template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROT = false>
