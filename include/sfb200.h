@@ -205,6 +205,17 @@ SFB_API int sfb_get_gradient(sfb_plan* plan, const sfb_field_mview* grad);
  * fill; each is `*count` contiguous floats. */
 SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, void** send_hi,
                     void** recv_lo, void** recv_hi, int64_t* count);
+/* ---- fused halo push (one process driving several slabs / GPUs).  After sfb_link_peers the
+ * boundary half-step (sfb_step_slab_boundary) writes its K boundary planes -- and the nodes
+ * injected into them -- directly into the neighbours' ghost planes as it computes them (peer
+ * stores over NVLink): no copy, no send/recv.  Ordering is by events: before its next
+ * step a plan calls sfb_peer_wait(plan, neighbour) for each neighbour, which makes both of
+ * its streams wait for that neighbour's last boundary half-step (its pushes have landed, and
+ * it has finished reading the ghost planes this plan will overwrite next).  Acoustic
+ * operators; lo / hi are the plans of the slabs below / above, or NULL at an outer face. */
+SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi);
+SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour);
+
 /* ---- TTI slab stepping.  One step of a slab is: sfb_tti_step_rot(part) (pass 1: g,
  * b g and L(p) on the owned planes; needs the ghost planes of p and r), the
  * caller's exchange of the K boundary planes of g (SFB_TTI_HALO_G_P / _G_R),

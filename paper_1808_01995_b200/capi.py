@@ -46,7 +46,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune",
 ]
@@ -81,6 +81,8 @@ lib.sfb_halo_blocks.argtypes = [C.c_void_p, C.c_int, C.c_int64] + [C.POINTER(C.c
 lib.sfb_tti_step_rot.argtypes = [C.c_void_p, C.c_int64, C.c_int]
 lib.sfb_tti_step_update.argtypes = [C.c_void_p, C.c_int64, C.c_int]
 lib.sfb_tti_halo_blocks.argtypes = lib.sfb_halo_blocks.argtypes
+lib.sfb_link_peers.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+lib.sfb_peer_wait.argtypes = [C.c_void_p, C.c_void_p]
 lib.sfb_stream_sync.argtypes = [C.c_void_p]
 lib.sfb_streams.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
 lib.sfb_set_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -319,6 +321,12 @@ class Plan:
         self._chk(lib.sfb_tti_halo_blocks(self.h, which, t, *[C.byref(x) for x in p], C.byref(n)))
         return dict(send_lo=p[0].value, send_hi=p[1].value, recv_lo=p[2].value,
                     recv_hi=p[3].value, count=n.value)
+
+    def link_peers(self, lo=None, hi=None):
+        self._chk(lib.sfb_link_peers(self.h, lo.h if lo else None, hi.h if hi else None))
+
+    def peer_wait(self, neighbour):
+        self._chk(lib.sfb_peer_wait(self.h, neighbour.h))
 
     def copy_halo(self, dst, src, count):
         self._chk(lib.sfb_copy_halo(self.h, dst, src, count))

@@ -64,6 +64,12 @@ struct StepParams {
     int chunk;           // output planes per block
     int z_jump;          // extra plane offset of blocks with blockIdx.z >= 1 (0 = contiguous):
                          // one launch covers the two boundary plane groups of a slab
+    // fused halo push: distance (in floats, 0 = none) from a node of `uo` written by the
+    // blocks with blockIdx.z == 0 / >= 1 to its mirror in the neighbouring slab's ghost planes
+    // (peer memory).  Boundary launches only (a block's chunk is exactly one boundary plane
+    // group).  A block-uniform offset instead of a second pointer: no per-thread register.
+    long long peer_delta0;
+    long long peer_delta1;
 };
 
 // the tensor maps of one launch: u[t] with halo box (u) and with plain box (f); u[t-1], r,
@@ -249,7 +255,7 @@ __device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&
 // One output plane for the four nodes of a thread: stencil from the register queue (d0)
 // and the centre plane in shared memory `cp` (d1, d2), then -- after telling the producer
 // that this iteration's shared-memory reads are over -- damping, leapfrog and the stores.
-template <int K, int KP, int SW, bool SEP, int ROT = 0>
+template <int K, int KP, int SW, bool SEP, int ROT = 0, bool PUSH = false>
 __device__ __forceinline__ void plane_update(const StepParams& p, const float (&q)[2 * K + 1][4],
                                              const float* cp, int tx, int ty, float4 o4, float4 r4,
                                              float4 d4, const float (&dxy)[4], float dzv,
@@ -299,6 +305,15 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
         if (lane0) mbar_release(done_bar, un[0]);
         if (rin) {
             __stcs(reinterpret_cast<float4*>(po), make_float4(un[0], un[1], un[2], un[3]));
+            // PUSH kernels (boundary launches of linked slabs): the same plane goes straight
+            // into the neighbour's ghost planes over NVLink.  A separate instantiation: even a
+            // never-taken branch here costs the issue-bound kernels 2-3 %.
+            if constexpr (PUSH) {
+                const long long peer_delta = blockIdx.z ? p.peer_delta1 : p.peer_delta0;
+                if (peer_delta)
+                    *reinterpret_cast<float4*>(po + peer_delta) =
+                        make_float4(un[0], un[1], un[2], un[3]);
+            }
             if (p.snap)
                 __stcs(reinterpret_cast<float4*>(p.snap + gc),
                        make_float4(un[0], un[1], un[2], un[3]));
@@ -335,7 +350,7 @@ struct StepShape {
     static_assert((ABOX * 4) % 128 == 0, "aux boxes must keep 128-byte alignment");
 };
 
-template <int K, int TXV, int TY, int NST, bool SEP>
+template <int K, int TXV, int TY, int NST, bool SEP, bool PUSH = false>
 __global__ void __launch_bounds__(StepShape<K, TXV, TY, NST, SEP>::NTHREADS)
 acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant__ StepParams p) {
     using S = StepShape<K, TXV, TY, NST, SEP>;
@@ -477,7 +492,7 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
         const float dzv = dzn;
         if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
 
-        plane_update<K, KP, SW, SEP>(p, q, ring + cs * STAGE, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
+        plane_update<K, KP, SW, SEP, 0, PUSH>(p, q, ring + cs * STAGE, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
                                      rin, lane0, done + ds, po, gc);
         po += p.plane;
         gc += p.plane;
@@ -527,7 +542,7 @@ __device__ __forceinline__ void rotate_run(F& f, int& n, int nplanes) {
     }
 }
 
-template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROTATE>
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROTATE, bool PUSH = false>
 __global__ void __launch_bounds__(DualShape<K, TXV, TY, NS, SEP>::NTHREADS, MINB)
 acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
                           const __grid_constant__ StepParams p) {
@@ -651,7 +666,7 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
             if (!SEP) d4 = *reinterpret_cast<const float4*>(ap + 2 * ABOX);
             const float dzv = dzn;
             if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
-            plane_update<K, KP, SW, SEP, R>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
+            plane_update<K, KP, SW, SEP, R, PUSH>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
                                             rin, lane0, done + s, po, gc);
             po += p.plane;
             gc += p.plane;

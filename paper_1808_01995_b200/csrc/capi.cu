@@ -189,6 +189,7 @@ SFB_API int sfb_plan_create(const sfb_plan_desc* desc, sfb_plan** out) {
         SFB_CUDA(cudaStreamCreateWithPriority(&P.s_bnd, cudaStreamNonBlocking, hi_pri));
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_main, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_bnd, cudaEventDisableTiming));
+        SFB_CUDA(cudaEventCreateWithFlags(&P.ev_push, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreate(&P.ev_t0));
         SFB_CUDA(cudaEventCreate(&P.ev_t1));
         P.u[0].alloc(size_t(P.ucount) * 4);
@@ -214,6 +215,7 @@ SFB_API int sfb_plan_destroy(sfb_plan* plan) {
     }
     if (plan->ev_main) cudaEventDestroy(plan->ev_main);
     if (plan->ev_bnd) cudaEventDestroy(plan->ev_bnd);
+    if (plan->ev_push) cudaEventDestroy(plan->ev_push);
     if (plan->ev_t0) cudaEventDestroy(plan->ev_t0);
     if (plan->ev_t1) cudaEventDestroy(plan->ev_t1);
     delete plan;
@@ -597,6 +599,57 @@ SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t) {
             step_compute(*plan, op, t, SFB_PART_HIGH);
         }
         step_points(*plan, op, t, SFB_PART_LOW);
+        if (plan->peer_lo[0] || plan->peer_hi[0])   // linked: the push of this step ends here
+            SFB_CUDA(cudaEventRecord(plan->ev_push, plan->s_bnd));
+    });
+}
+
+SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        auto compatible = [&](const Plan& Q) {
+            return Q.K == P.K && Q.N[1] == P.N[1] && Q.N[2] == P.N[2] && Q.pitch == P.pitch &&
+                   Q.plane == P.plane;
+        };
+        for (int b = 0; b < 2; ++b) P.peer_lo[b] = P.peer_hi[b] = nullptr;
+        if ((lo || hi) && !P.variant->launch_push) {
+            select_variant(P, 0, 0, 0);   // the default shape of the order carries the push kernel
+            require(P.variant->launch_push != nullptr, SFB_ERR_CAPABILITY,
+                    "link_peers: no halo-push kernel for this order");
+        }
+        if (lo) {
+            require(compatible(*lo) && lo->z_hi == P.z_lo, SFB_ERR_PARAMETER,
+                    "link_peers: the lower plan is not the slab below this one");
+            for (int b = 0; b < 2; ++b)   // its high ghost planes: buffer planes n0 + K ...
+                P.peer_lo[b] = lo->u[b].as<float>() + (long long)(lo->n0 + lo->K) * lo->plane;
+        }
+        if (hi) {
+            require(compatible(*hi) && hi->z_lo == P.z_hi, SFB_ERR_PARAMETER,
+                    "link_peers: the upper plan is not the slab above this one");
+            for (int b = 0; b < 2; ++b) P.peer_hi[b] = hi->u[b].as<float>();   // planes 0 .. K-1
+        }
+        if ((lo && lo->device != P.device) || (hi && hi->device != P.device)) {
+            // one process driving several GPUs: map the neighbours' memory
+            for (sfb_plan* q : {lo, hi}) {
+                if (!q || q->device == P.device) continue;
+                int can = 0;
+                SFB_CUDA(cudaDeviceCanAccessPeer(&can, P.device, q->device));
+                require(can != 0, SFB_ERR_CAPABILITY, "link_peers: no peer access between the devices");
+                cudaError_t e = cudaDeviceEnablePeerAccess(q->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SFB_CUDA(e);
+                (void)cudaGetLastError();
+            }
+        }
+    });
+}
+
+SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour) {
+    if (!plan || !neighbour) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        SFB_CUDA(cudaStreamWaitEvent(plan->s_main, neighbour->ev_push, 0));
+        if (plan->s_bnd != plan->s_main)
+            SFB_CUDA(cudaStreamWaitEvent(plan->s_bnd, neighbour->ev_push, 0));
     });
 }
 

@@ -96,6 +96,9 @@ void select_variant(Plan& P, int txv, int ty, int nst, int dual) {
     P.variant = best;
     SFB_CUDA(cudaFuncSetAttribute(best->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(best->smem)));
+    if (best->func_push)
+        SFB_CUDA(cudaFuncSetAttribute(best->func_push, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(best->smem)));
     int bps = 1;
     SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, best->func, best->nthreads,
                                                            best->smem));

@@ -130,6 +130,21 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
     sp.chunk = pair ? P.K
                     : (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? P.chunk : (hi - lo);
     sp.z_jump = pair ? P.n0 - 2 * P.K : 0;   // block z = 1 starts at plane n0 - K
+    // linked slabs: the boundary plane groups are also written into the neighbours' ghosts
+    if (!(ex && ex->alt)) {
+        // mirror of owned plane z: low group -> peer_lo + z planes, high group -> peer_hi +
+        // (z - (n0 - K)) planes; owned plane z itself sits at uo + (z + K) planes
+        const long long d_lo = P.peer_lo[oth] ? P.peer_lo[oth] - (sp.uo + (long long)P.K * P.plane) : 0;
+        const long long d_hi = P.peer_hi[oth] ? P.peer_hi[oth] - (sp.uo + (long long)P.n0 * P.plane) : 0;
+        if (pair) {
+            sp.peer_delta0 = d_lo;
+            sp.peer_delta1 = d_hi;
+        } else if (part == SFB_PART_LOW) {
+            sp.peer_delta0 = d_lo;
+        } else if (part == SFB_PART_HIGH) {
+            sp.peer_delta0 = d_hi;
+        }
+    }
     if (ex) {
         sp.snap = ex->snap;
         sp.usave = ex->usave;
@@ -154,7 +169,13 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
     maps.o = alt ? P.tm_fo[oth] : P.tm_o[oth];
     maps.r = P.tm_r;
     maps.d = P.sep ? P.tm_r : P.tm_d;
-    SFB_CUDA(v.launch(maps, sp, grid, st));
+    if (sp.peer_delta0 || sp.peer_delta1) {
+        require(v.launch_push != nullptr, SFB_ERR_CAPABILITY,
+                "the selected tile shape has no halo-push kernel (sfb_link_peers picks one that has)");
+        SFB_CUDA(v.launch_push(maps, sp, grid, st));
+    } else {
+        SFB_CUDA(v.launch(maps, sp, grid, st));
+    }
     ++P.launches;
     mark_stream(P, part);
     if (!alt && (part == SFB_PART_ALL || part == SFB_PART_INTERIOR)) {
@@ -205,6 +226,13 @@ void step_points(Plan& P, int op, long long t, int part, float* target_override,
         pp.target = target_override ? target_override : P.u[oth].as<float>();
         pp.r = P.r.as<float>();
         pp.inv_dt2 = P.coef.inv_dt2;
+        if (!target_override && (part == SFB_PART_LOW || part == SFB_PART_HIGH)) {
+            pp.peer_lo = P.peer_lo[oth];
+            pp.peer_hi = P.peer_hi[oth];
+            pp.plane = P.plane;
+            pp.K = P.K;
+            pp.n0 = P.n0;
+        }
         if (ex) {
             pp.snap = ex->snap;
             pp.usave = ex->usave;

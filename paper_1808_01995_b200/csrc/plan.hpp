@@ -137,6 +137,12 @@ struct Plan {
     cudaStream_t s_main = nullptr, s_bnd = nullptr;
     bool own_streams = true;
     cudaEvent_t ev_main = nullptr, ev_bnd = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    // fused halo push (sfb_link_peers): the neighbours' wavefield buffers by level parity,
+    // offset to the ghost planes this slab fills, and the event that closes a boundary
+    // half-step (the neighbours wait on it before their next step)
+    float* peer_lo[2] = {nullptr, nullptr};
+    float* peer_hi[2] = {nullptr, nullptr};
+    cudaEvent_t ev_push = nullptr;
     bool main_pending = false, bnd_pending = false;
 
     DevBuf u[2], r, damp, dz, dy, dx, grad, snaps, flag;

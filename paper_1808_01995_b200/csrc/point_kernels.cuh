@@ -31,6 +31,12 @@ struct PointParams {
     const float* usave;           // optional: imaging correction for the injected amount
     float* grad;
     float inv_dt2;
+    // fused halo push: an injected node of a boundary plane group is mirrored into the
+    // neighbour's ghost plane (peer memory), like the planes themselves
+    float* peer_lo;               // neighbour below: its high ghost planes
+    float* peer_hi;               // neighbour above: its low ghost planes
+    long long plane;              // floats per plane
+    int K, n0;
     // gather
     int nsmp;
     const long long* smp_idx;     // base node index inside a wavefield buffer, -1 = not owned
@@ -57,7 +63,13 @@ point_step_kernel(const __grid_constant__ PointParams p, int nb_inj) {
         for (int e = e0; e < e1; ++e) s = fmaf(p.ent_w[e], p.inj_row[p.ent_point[e]], s);
         const long long cu = p.cell_u[i], cc = p.cell_c[i];
         const float add = s * p.r[cc];
-        p.target[cu] = __ldcg(p.target + cu) + add;
+        const float v = __ldcg(p.target + cu) + add;
+        p.target[cu] = v;
+        if (p.peer_lo || p.peer_hi) {
+            const long long zb = cu / p.plane;   // buffer plane: owned plane z sits at z + K
+            if (p.peer_lo && zb < 2 * p.K) p.peer_lo[cu - (long long)p.K * p.plane] = v;
+            if (p.peer_hi && zb >= p.n0) p.peer_hi[cu - (long long)p.n0 * p.plane] = v;
+        }
         if (p.snap) p.snap[cc] = __ldcg(p.snap + cc) + add;
         if (p.usave)
             p.grad[cc] = fmaf(-__ldcg(p.usave + cc) * p.inv_dt2, add, __ldcg(p.grad + cc));

@@ -24,15 +24,18 @@ struct StepVariant {
     size_t smem;
     const void* func;
     cudaError_t (*launch)(const StepMaps&, const StepParams&, dim3, cudaStream_t);
+    // the same kernel with the fused halo push (default shapes only, else null)
+    const void* func_push = nullptr;
+    cudaError_t (*launch_push)(const StepMaps&, const StepParams&, dim3, cudaStream_t) = nullptr;
 };
 
 std::vector<StepVariant>& step_variant_registry();
 
-template <int K, int TXV, int TY, int NST, bool SEP>
+template <int K, int TXV, int TY, int NST, bool SEP, bool PUSH = false>
 cudaError_t launch_step(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
     using S = StepShape<K, TXV, TY, NST, SEP>;
-    return launch_pdl(&acoustic_step_kernel<K, TXV, TY, NST, SEP>, grid, S::NTHREADS, S::SMEM, st,
-                      tm, p);
+    return launch_pdl(&acoustic_step_kernel<K, TXV, TY, NST, SEP, PUSH>, grid, S::NTHREADS, S::SMEM,
+                      st, tm, p);
 }
 
 template <int K, int TXV, int TY, int NST, bool SEP>
@@ -45,15 +48,20 @@ void register_step() {
         v.nthreads = S::NTHREADS; v.smem = S::SMEM;
         v.func = reinterpret_cast<const void*>(&acoustic_step_kernel<K, TXV, TY, NST, SEP>);
         v.launch = &launch_step<K, TXV, TY, NST, SEP>;
+        if constexpr (K <= 4 && TXV == 16 && TY == 16 && NST == K + 3) {   // the default shape
+            v.func_push = reinterpret_cast<const void*>(
+                &acoustic_step_kernel<K, TXV, TY, NST, SEP, true>);
+            v.launch_push = &launch_step<K, TXV, TY, NST, SEP, true>;
+        }
         step_variant_registry().push_back(v);
     }
 }
 
-template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROT>
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROT, bool PUSH = false>
 cudaError_t launch_dual(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
     using S = DualShape<K, TXV, TY, NS, SEP>;
-    return launch_pdl(&acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT>, grid, S::NTHREADS,
-                      S::SMEM, st, tm, p);
+    return launch_pdl(&acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT, PUSH>, grid,
+                      S::NTHREADS, S::SMEM, st, tm, p);
 }
 
 template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROT = false>
@@ -67,6 +75,11 @@ void register_dual() {
         v.func = reinterpret_cast<const void*>(
             &acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT>);
         v.launch = &launch_dual<K, TXV, TY, NS, SEP, MINB, ROT>;
+        if constexpr (K >= 5 && TXV == 16 && TY == 16 && NS == 4 && !ROT) {   // the default shape
+            v.func_push = reinterpret_cast<const void*>(
+                &acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, ROT, true>);
+            v.launch_push = &launch_dual<K, TXV, TY, NS, SEP, MINB, ROT, true>;
+        }
         step_variant_registry().push_back(v);
     }
 }

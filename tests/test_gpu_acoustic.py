@@ -256,7 +256,7 @@ def test_unstable_dt_and_nan_guard():
 
 
 def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_forward=False,
-               fused=False):
+               fused=False, pushed=False):
     """N plans on one device stepping in lockstep with device-to-device ghost copies:
     the single-GPU emulation of the multi-GPU slab protocol.  Returns the summed sampled
     traces, the assembled last level and (gradient) the assembled grad."""
@@ -264,6 +264,9 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
     op = capi.OP_FORWARD if op is None else op
     backward = op != capi.OP_FORWARD
     plans = [make_plan(model, geom, order, slab=(cuts[i], cuts[i + 1])) for i in range(len(cuts) - 1)]
+    if pushed:   # fused halo push: boundary planes go straight into the neighbours' ghosts
+        for i, p in enumerate(plans):
+            p.link_peers(plans[i - 1] if i > 0 else None, plans[i + 1] if i + 1 < len(plans) else None)
 
     def sweep(o, traces_cloud, traces, se):
         for p in plans:
@@ -271,6 +274,16 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
             p.step_begin(o, se)
         ts = range(geom.nt - 2, 0, -1) if o != capi.OP_FORWARD else range(1, geom.nt - 1)
         for t in ts:
+            if pushed:   # no copies and no host synchronisation: events order the slabs
+                for p in plans:
+                    p.step_slab_boundary(o, t)
+                    p.step_slab_interior(o, t)
+                for i, p in enumerate(plans):
+                    if i > 0:
+                        p.peer_wait(plans[i - 1])
+                    if i + 1 < len(plans):
+                        p.peer_wait(plans[i + 1])
+                continue
             for p in plans:
                 if fused:   # the two native half-step calls of slabs.PlanEngine
                     p.step_slab_boundary(o, t)
@@ -310,6 +323,34 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
             p._chk(capi.lib.sfb_get_gradient(p.h, C.byref(capi._view(grad))))
         p.close()
     return rec, u, grad
+
+
+def test_fused_halo_push_matches_single_domain_bitwise():
+    """sfb_link_peers: the boundary kernels store their planes (and the point kernel its
+    injected nodes) directly into the neighbours' ghost planes; slabs are ordered by events
+    only.  Forward, adjoint and gradient equal the single-domain run bit for bit."""
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([48, 30, 34], 10.0, 8, 8, 50)
+    rng = np.random.default_rng(9)
+    data = rng.standard_normal((geom.nt, geom.n_rec)) * np.hanning(geom.nt)[:, None]
+    plan = make_plan(model, geom, 8)
+    rec1, _ = plan.forward(geom.src)
+    u1 = plan.wavefield(geom.nt - 1)
+    srca1, _ = plan.adjoint(data)
+    v1 = plan.wavefield(0)
+    plan.forward(geom.src, save_every=2)
+    g1, _ = plan.gradient(data)
+    plan.close()
+    n0 = model.N[0]
+    src_plane = int(geom.src_base[0][0])
+    cuts = [0, 20, src_plane + 1, n0]          # the source cell straddles a cut
+    rec3, u3, _ = _run_slabs(model, geom, 8, cuts, pushed=True)
+    assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
+    srca3, v3, _ = _run_slabs(model, geom, 8, cuts, op=capi.OP_ADJOINT, inj=data, pushed=True)
+    assert np.array_equal(srca3, srca1) and np.array_equal(v3, v1)
+    _, _, g3 = _run_slabs(model, geom, 8, cuts, op=capi.OP_GRADIENT, save_every=2, inj=data,
+                          prior_forward=True, pushed=True)
+    assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
 
 
 @pytest.mark.parametrize("fused", [False, True])

@@ -55,9 +55,20 @@ def parts(t):
 
 a = timed(whole)
 b = timed(parts)
+# the same protocol with the fused halo push: neighbours on the same device stand in for the
+# peers (their ghost planes receive this slab's boundary planes as they are computed)
+def neighbour(lo, hi):
+    q = capi.Plan(N, [h] * 3, order, dt, nt, 0, (lo, hi))
+    q.set_model(m, damp, vmax)
+    return q
+below, above = neighbour(0, n0_slab), neighbour(2 * n0_slab, 3 * n0_slab)
+plan.link_peers(below, above)
+c = timed(parts)
+plan.link_peers(None, None)
+below.close(); above.close()
 K = order // 2
 print(json.dumps({"slab": [n0_slab, n, n], "order": order, "tile": plan.get_tile(),
                   "whole_ms": a * 1e3, "parts_ms": b * 1e3, "whole_gpts": pts / a / 1e9,
-                  "parts_gpts": pts / b / 1e9, "protocol_efficiency": a / b,
+                  "parts_gpts": pts / b / 1e9, "protocol_efficiency": a / b, "pushed_ms": c * 1e3, "pushed_efficiency": a / c,
                   "halo_mb_per_neighbour": K * n * n * 4 / 1e6}))
 plan.close()
