@@ -104,6 +104,16 @@ ExecutionReport run_wave(WaveOp& w, Backend backend = Backend::Auto, int nthread
 ExecutionReport run_gradient(GradientOp& g, Backend backend = Backend::Auto,
                              int nthreads = 1);
 
+// extension: run a forward or adjoint operator on a slab decomposition of the
+// grid along axis 0 driven by this one process -- one slab per entry of `devices` (CUDA
+// ordinals; an ordinal may repeat).  The slabs are linked with sfb_link_peers: each boundary
+// half-step stores its planes straight into the neighbours' ghost planes (peer stores over
+// NVLink) while the interior updates, and events order the slabs; there is no copy and no
+// collective.  Fills w.smp's traces and the two live levels of w.wavefield exactly as
+// run_wave does (the result is bit-identical to the single-device run).
+ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model,
+                               const AcquisitionGeometry& geom, const std::vector<int>& devices);
+
 // proj/include/sf/seismic_ops.hpp:61, proj/src/seismic_ops.cpp:149-160
 double objective(const SparseFunction& pred, const std::vector<double>& observed);
 

@@ -14,7 +14,10 @@ int device();
 // One sfb_plan plus what is bound to it.
 class Engine {
 public:
-    Engine(const SeismicModel& model, const AcquisitionGeometry& geom, int space_order) {
+    // slab_lo < slab_hi: own only those planes of axis 0 (one slab of a decomposed run);
+    // dev < 0: the calling thread's device
+    Engine(const SeismicModel& model, const AcquisitionGeometry& geom, int space_order,
+           long slab_lo = 0, long slab_hi = 0, int dev = -1) {
         const Grid& g = *model.grid();
         sfb_plan_desc d{};
         d.ndim = g.ndim();
@@ -25,7 +28,9 @@ public:
         d.space_order = space_order;
         d.dt = geom.dt();
         d.nt = geom.nt();
-        d.device = device();
+        d.device = dev >= 0 ? dev : device();
+        d.slab_lo = slab_lo;
+        d.slab_hi = slab_hi;
         int rc = sfb_plan_create(&d, &plan_);
         if (rc != SFB_OK) raise_status(rc, sfb_last_error(nullptr));
         try {

@@ -4,6 +4,7 @@
 // run_window (proj/src/seismic_ops.cpp:44-54) is handed to sfb_forward / sfb_adjoint /
 // sfb_gradient here.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <mutex>
 #include <thread>
@@ -238,6 +239,77 @@ ExecutionReport run_wave(WaveOp& w, Backend, int) {
         }
     }
     return to_report(rep);
+}
+
+// SURVEY.md 8e through the operator interface: one process, one plan per slab, fused halo push
+ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model,
+                               const AcquisitionGeometry& geom, const std::vector<int>& devices) {
+    if (w.tti) throw CapabilityError("run_wave_slabs: acoustic operators only");
+    if (devices.empty()) throw ParameterError("run_wave_slabs: empty device list");
+    if (model.grid()->ndim() != 3) throw CapabilityError("run_wave_slabs: 3-D grids only");
+    const long n0 = model.grid()->shape()[0];
+    const long K = w.space_order / 2, nslab = long(devices.size());
+    if (n0 / nslab < 2 * K)
+        throw ParameterError("run_wave_slabs: slabs thinner than two halo widths");
+    const int op = w.adjoint ? SFB_OP_ADJOINT : SFB_OP_FORWARD;
+    const int inj_cloud = w.adjoint ? SFB_CLOUD_REC : SFB_CLOUD_SRC;
+    const int smp_cloud = w.adjoint ? SFB_CLOUD_SRC : SFB_CLOUD_REC;
+    std::vector<std::unique_ptr<Engine>> eng;
+    long lo = 0;
+    for (long i = 0; i < nslab; ++i) {   // balanced contiguous split (slabs.split_slabs)
+        const long hi = lo + n0 / nslab + (i < n0 % nslab ? 1 : 0);
+        eng.emplace_back(new Engine(model, geom, w.space_order, lo, hi, devices[std::size_t(i)]));
+        lo = hi;
+    }
+    for (long i = 0; i < nslab; ++i) {
+        Engine& e = *eng[std::size_t(i)];
+        e.check(sfb_upload_traces(e.plan(), inj_cloud, w.inj->traces().data()));
+        e.check(sfb_link_peers(e.plan(), i > 0 ? eng[std::size_t(i - 1)]->plan() : nullptr,
+                               i + 1 < nslab ? eng[std::size_t(i + 1)]->plan() : nullptr));
+        e.check(sfb_step_begin(e.plan(), op, 0));
+    }
+    for (auto& e : eng) e->check(sfb_stream_sync(e->plan()));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long s = 0; s < w.nt - 2; ++s) {
+        const long t = w.adjoint ? w.nt - 2 - s : 1 + s;
+        for (auto& e : eng) {
+            e->check(sfb_step_slab_boundary(e->plan(), op, t));
+            e->check(sfb_step_slab_interior(e->plan(), op, t));
+        }
+        for (long i = 0; i < nslab; ++i) {
+            Engine& e = *eng[std::size_t(i)];
+            if (i > 0) e.check(sfb_peer_wait(e.plan(), eng[std::size_t(i - 1)]->plan()));
+            if (i + 1 < nslab) e.check(sfb_peer_wait(e.plan(), eng[std::size_t(i + 1)]->plan()));
+        }
+    }
+    for (auto& e : eng) e->check(sfb_step_end(e->plan(), op));
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    // sampled traces: every point is sampled by the slab that owns its base plane, the
+    // others hold zeros, so the record is the sum; wavefield: each slab writes its planes
+    std::vector<double>& out = w.smp->traces();
+    std::fill(out.begin(), out.end(), 0.0);
+    std::vector<double> part(out.size());
+    w.wavefield->zero();
+    for (auto& e : eng) {
+        e->check(sfb_download_traces(e->plan(), smp_cloud, part.data()));
+        for (std::size_t i = 0; i < out.size(); ++i) out[i] += part[i];
+        if (w.nt >= 3) {
+            TimeFunction& u = *w.wavefield;
+            const long a = w.adjoint ? 0 : w.nt - 1, b = w.adjoint ? 1 : w.nt - 2;
+            for (long lvl : {a, b}) {
+                sfb_field_mview mv = Engine::mview(u, u.time_buffered() ? lvl % u.time_slots() : lvl);
+                e->check(sfb_get_wavefield(e->plan(), 0, lvl, &mv));
+            }
+        }
+    }
+    ExecutionReport rep;
+    const long steps = std::max(0L, w.nt - 2);
+    double pts = 1;
+    for (long e : model.grid()->shape()) pts *= double(e);
+    rep.seconds = sec;
+    rep.steps = steps;
+    rep.gpts_per_s = sec > 0 ? pts * double(steps) / sec / 1e9 : 0.0;
+    return rep;
 }
 
 // proj/src/seismic_ops.cpp:143-147

@@ -133,6 +133,41 @@ def test_fwi_gradient_checkpointed_equals_full_history():
         H.fwi_gradient(m, g, observed, 8, save_every=2, checkpoint_every=4)
 
 
+def test_run_wave_slabs_equals_run_wave():
+    """run_wave_slabs: the slab decomposition through the operator interface, one process,
+    linked plans with the fused halo push (three slabs on the one device here).  Forward and
+    adjoint equal the single-plan run bit for bit."""
+    n, h = 40, 10.0
+    vel = np.full((n, 28, 30), 1.5)
+    vel[..., 15:] = 2.5
+    m = H.SeismicModel([n, 28, 30], [h] * 3, [0.0] * 3, vel.ravel(), 6, 8)
+    L0, L1 = (n - 1) * h, 27 * h
+    rec = np.array([[L0 * i / 39.0, 0.5 * L1, 4.5 * h] for i in range(40)])
+    g = H.AcquisitionGeometry(m, [0.5 * L0 + 0.37 * h, 0.5 * L1 + 0.37 * h, 2.13 * h], rec.ravel(),
+                              0.0, 60.0, 0.8 * m.critical_dt(), 0.02)
+    fwd = H.forward_operator(m, g, 8)
+    H.run_wave(fwd)
+    rec1 = g.rec.traces.copy()
+    u1 = fwd.wavefield.array().copy()
+    assert np.abs(rec1).max() > 0
+    fwd3 = H.forward_operator(m, g, 8)
+    g.rec.traces[:] = 0.0
+    rep = H.run_wave_slabs(fwd3, m, g, [0, 0, 0])
+    assert rep.steps == g.nt - 2
+    assert np.array_equal(g.rec.traces, rec1)
+    assert np.array_equal(fwd3.wavefield.array(), u1)
+    # adjoint: receiver traces in, source-position traces out
+    g.rec.traces[:] = rec1
+    adj = H.adjoint_operator(m, g, 8)
+    H.run_wave(adj)
+    srca1 = adj.smp.traces.copy()
+    adj3 = H.adjoint_operator(m, g, 8)
+    H.run_wave_slabs(adj3, m, g, [0, 0])
+    assert np.abs(srca1).max() > 0 and np.array_equal(adj3.smp.traces, srca1)
+    with pytest.raises(H.ParameterError):
+        H.run_wave_slabs(fwd3, m, g, [0] * 8)      # 6.5-plane slabs < 2 K
+
+
 def test_gradient_operator_needs_saved_history():  # seismic_ops.cpp:113-114
     m = constant_model(21, 10.0, 1.5, 6)
     g = H.AcquisitionGeometry(m, [100.0, 20.0], [40.0, 40.0], 0.0, 60.0, 0.8 * m.critical_dt(), 0.01)
