@@ -353,6 +353,24 @@ def test_fused_halo_push_matches_single_domain_bitwise():
     assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
 
 
+def test_link_peers_checks_the_neighbours():
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([48, 30, 34], 10.0, 8, 8, 10)
+    n0 = model.N[0]
+    a = make_plan(model, geom, 8, slab=(0, 20))
+    b = make_plan(model, geom, 8, slab=(20, 41))
+    c = make_plan(model, geom, 8, slab=(41, n0))
+    b.link_peers(a, c)
+    with pytest.raises(capi.SfbError) as e:      # c is not the slab below b
+        b.link_peers(c, a)
+    assert e.value.code == capi.ERR_PARAMETER
+    with pytest.raises(capi.SfbError):           # a does not touch c
+        a.link_peers(None, c)
+    b.link_peers(None, None)                      # unlink
+    for p in (a, b, c):
+        p.close()
+
+
 @pytest.mark.parametrize("fused", [False, True])
 def test_slab_decomposition_matches_single_domain_bitwise(fused):
     model, geom = make_problem([48, 30, 34], 10.0, 8, 8, 60)
