@@ -215,6 +215,17 @@ SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, v
  * operators; lo / hi are the plans of the slabs below / above, or NULL at an outer face. */
 SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi);
 SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour);
+/* The same between processes (one per GPU): sfb_peer_export fills a blob of
+ * SFB_PEER_BLOB_BYTES (CUDA IPC handles of the plan's wavefield buffers and of its step
+ * counter) that the caller ships to the neighbouring ranks by any means;
+ * sfb_link_peers_ipc maps the neighbours' blobs (NULL at an outer face).  Every boundary
+ * half-step then ends by writing the plan's step counter with a stream memory operation,
+ * and sfb_peer_wait_ipc makes both streams of the plan wait, on the device, until the
+ * neighbours' counters have reached its own: no host-side handshake per step. */
+#define SFB_PEER_BLOB_BYTES 256
+SFB_API int sfb_peer_export(sfb_plan* plan, void* blob);
+SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* hi_blob);
+SFB_API int sfb_peer_wait_ipc(sfb_plan* plan);
 
 /* ---- TTI slab stepping.  One step of a slab is: sfb_tti_step_rot(part) (pass 1: g,
  * b g and L(p) on the owned planes; needs the ghost planes of p and r), the

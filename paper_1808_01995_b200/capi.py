@@ -46,7 +46,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune",
 ]
@@ -83,6 +83,10 @@ lib.sfb_tti_step_update.argtypes = [C.c_void_p, C.c_int64, C.c_int]
 lib.sfb_tti_halo_blocks.argtypes = lib.sfb_halo_blocks.argtypes
 lib.sfb_link_peers.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 lib.sfb_peer_wait.argtypes = [C.c_void_p, C.c_void_p]
+lib.sfb_peer_export.argtypes = [C.c_void_p, C.c_void_p]
+lib.sfb_link_peers_ipc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+lib.sfb_peer_wait_ipc.argtypes = [C.c_void_p]
+PEER_BLOB_BYTES = 256
 lib.sfb_stream_sync.argtypes = [C.c_void_p]
 lib.sfb_streams.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
 lib.sfb_set_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -324,6 +328,17 @@ class Plan:
 
     def link_peers(self, lo=None, hi=None):
         self._chk(lib.sfb_link_peers(self.h, lo.h if lo else None, hi.h if hi else None))
+
+    def peer_export(self):
+        blob = C.create_string_buffer(PEER_BLOB_BYTES)
+        self._chk(lib.sfb_peer_export(self.h, blob))
+        return blob.raw
+
+    def link_peers_ipc(self, lo_blob=None, hi_blob=None):
+        self._chk(lib.sfb_link_peers_ipc(self.h, lo_blob, hi_blob))
+
+    def peer_wait_ipc(self):
+        self._chk(lib.sfb_peer_wait_ipc(self.h))
 
     def peer_wait(self, neighbour):
         self._chk(lib.sfb_peer_wait(self.h, neighbour.h))

@@ -22,6 +22,38 @@ std::vector<TtiVariant>& tti_variant_registry() {
 
 using namespace sfb;
 
+namespace {
+
+// stream memory operations of the driver API (no link-time libcuda dependency)
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValueFn stream_value_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+        throw Failure(SFB_ERR_CAPABILITY, std::string("driver lacks ") + name);
+    return reinterpret_cast<StreamValueFn>(p);
+}
+
+struct PeerBlob {   // what sfb_peer_export writes into the caller's SFB_PEER_BLOB_BYTES
+    cudaIpcMemHandle_t u[2];
+    cudaIpcMemHandle_t flag;
+    int64_t z_lo, z_hi, n1, n2, pitch, plane, K;
+};
+static_assert(sizeof(PeerBlob) <= SFB_PEER_BLOB_BYTES, "peer blob");
+
+void close_ipc(Plan& P) {
+    for (int side = 0; side < 2; ++side) {
+        for (int b = 0; b < 2; ++b)
+            if (P.ipc_u[side][b]) cudaIpcCloseMemHandle(P.ipc_u[side][b]);
+        if (P.ipc_flag[side]) cudaIpcCloseMemHandle(P.ipc_flag[side]);
+        P.ipc_u[side][0] = P.ipc_u[side][1] = P.ipc_flag[side] = nullptr;
+    }
+}
+
+}  // namespace
+
+
 extern "C" {
 
 SFB_API int sfb_abi_version(void) { return SFB_ABI_VERSION; }
@@ -216,6 +248,7 @@ SFB_API int sfb_plan_destroy(sfb_plan* plan) {
     if (plan->ev_main) cudaEventDestroy(plan->ev_main);
     if (plan->ev_bnd) cudaEventDestroy(plan->ev_bnd);
     if (plan->ev_push) cudaEventDestroy(plan->ev_push);
+    close_ipc(*plan);
     if (plan->ev_t0) cudaEventDestroy(plan->ev_t0);
     if (plan->ev_t1) cudaEventDestroy(plan->ev_t1);
     delete plan;
@@ -599,8 +632,18 @@ SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t) {
             step_compute(*plan, op, t, SFB_PART_HIGH);
         }
         step_points(*plan, op, t, SFB_PART_LOW);
-        if (plan->peer_lo[0] || plan->peer_hi[0])   // linked: the push of this step ends here
+        if (plan->peer_lo[0] || plan->peer_hi[0]) {   // linked: the push of this step ends here
             SFB_CUDA(cudaEventRecord(plan->ev_push, plan->s_bnd));
+            if (plan->ipc_flag[0] || plan->ipc_flag[1]) {   // neighbours in other processes
+                static StreamValueFn write_value = stream_value_fn("cuStreamWriteValue32");
+                CUresult rc = write_value(plan->s_bnd,
+                                          reinterpret_cast<CUdeviceptr>(plan->push_flag.p),
+                                          ++plan->push_count, 0);
+                if (rc != CUDA_SUCCESS)
+                    throw Failure(SFB_ERR_CUDA, "cuStreamWriteValue32 failed with code " +
+                                                    std::to_string(int(rc)));
+            }
+        }
     });
 }
 
@@ -639,6 +682,88 @@ SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi) {
                 cudaError_t e = cudaDeviceEnablePeerAccess(q->device, 0);
                 if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SFB_CUDA(e);
                 (void)cudaGetLastError();
+            }
+        }
+    });
+}
+
+SFB_API int sfb_peer_export(sfb_plan* plan, void* blob) {
+    if (!plan || !blob) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        if (!P.push_flag.p) P.push_flag.alloc(256, true);
+        PeerBlob pb{};
+        for (int b = 0; b < 2; ++b) SFB_CUDA(cudaIpcGetMemHandle(&pb.u[b], P.u[b].p));
+        SFB_CUDA(cudaIpcGetMemHandle(&pb.flag, P.push_flag.p));
+        pb.z_lo = P.z_lo;
+        pb.z_hi = P.z_hi;
+        pb.n1 = P.N[1];
+        pb.n2 = P.N[2];
+        pb.pitch = P.pitch;
+        pb.plane = P.plane;
+        pb.K = P.K;
+        std::memset(blob, 0, SFB_PEER_BLOB_BYTES);
+        std::memcpy(blob, &pb, sizeof pb);
+    });
+}
+
+SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* hi_blob) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        close_ipc(P);
+        for (int b = 0; b < 2; ++b) P.peer_lo[b] = P.peer_hi[b] = nullptr;
+        if (!lo_blob && !hi_blob) return;
+        if (!P.variant->launch_push) {
+            select_variant(P, 0, 0, 0);
+            require(P.variant->launch_push != nullptr, SFB_ERR_CAPABILITY,
+                    "link_peers_ipc: no halo-push kernel for this order");
+        }
+        if (!P.push_flag.p) P.push_flag.alloc(256, true);
+        const void* blobs[2] = {lo_blob, hi_blob};
+        for (int side = 0; side < 2; ++side) {
+            if (!blobs[side]) continue;
+            PeerBlob pb;
+            std::memcpy(&pb, blobs[side], sizeof pb);
+            require(pb.K == P.K && pb.n1 == P.N[1] && pb.n2 == P.N[2] && pb.pitch == P.pitch &&
+                        pb.plane == P.plane &&
+                        (side == 0 ? pb.z_hi == P.z_lo : pb.z_lo == P.z_hi),
+                    SFB_ERR_PARAMETER, "link_peers_ipc: the blob is not the neighbouring slab");
+            for (int b = 0; b < 2; ++b)
+                SFB_CUDA(cudaIpcOpenMemHandle(&P.ipc_u[side][b], pb.u[b],
+                                              cudaIpcMemLazyEnablePeerAccess));
+            SFB_CUDA(cudaIpcOpenMemHandle(&P.ipc_flag[side], pb.flag, cudaIpcMemLazyEnablePeerAccess));
+            const long long n0q = pb.z_hi - pb.z_lo;
+            for (int b = 0; b < 2; ++b) {
+                float* base = static_cast<float*>(P.ipc_u[side][b]);
+                if (side == 0)
+                    P.peer_lo[b] = base + (n0q + pb.K) * pb.plane;   // its high ghost planes
+                else
+                    P.peer_hi[b] = base;                              // its low ghost planes
+            }
+        }
+        P.push_count = 0;
+        SFB_CUDA(cudaMemsetAsync(P.push_flag.p, 0, 256, P.s_main));
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    });
+}
+
+SFB_API int sfb_peer_wait_ipc(sfb_plan* plan) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        static StreamValueFn wait_value = stream_value_fn("cuStreamWaitValue32");
+        // every slab has made the same number of boundary half-steps when its neighbours
+        // may go on: wait until theirs have reached this plan's own count
+        for (int side = 0; side < 2; ++side) {
+            if (!P.ipc_flag[side]) continue;
+            const CUdeviceptr f = reinterpret_cast<CUdeviceptr>(P.ipc_flag[side]);
+            for (cudaStream_t st : {P.s_main, P.s_bnd}) {
+                CUresult rc = wait_value(st, f, P.push_count, CU_STREAM_WAIT_VALUE_GEQ);
+                if (rc != CUDA_SUCCESS)
+                    throw Failure(SFB_ERR_CUDA, "cuStreamWaitValue32 failed with code " +
+                                                    std::to_string(int(rc)));
+                if (P.s_bnd == P.s_main) break;
             }
         }
     });

@@ -143,6 +143,13 @@ struct Plan {
     float* peer_lo[2] = {nullptr, nullptr};
     float* peer_hi[2] = {nullptr, nullptr};
     cudaEvent_t ev_push = nullptr;
+    // neighbours in other processes (sfb_peer_export / sfb_link_peers_ipc): their buffers are
+    // mapped through CUDA IPC, and the boundary half-steps are counted in a device word per
+    // plan that the neighbours' streams wait on (stream memory operations: no host handshake)
+    DevBuf push_flag;                    // [0]: boundary half-steps completed since linking
+    unsigned push_count = 0;
+    void* ipc_u[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [lo/hi][parity], opened
+    void* ipc_flag[2] = {nullptr, nullptr};                         // [lo/hi], opened
     bool main_pending = false, bnd_pending = false;
 
     DevBuf u[2], r, damp, dz, dy, dx, grad, snaps, flag;

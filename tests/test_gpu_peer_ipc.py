@@ -1,0 +1,66 @@
+"""The fused halo push between PROCESSES (CUDA IPC + stream memory operations): two ranks,
+each with its own CUDA context and one slab plan -- both on cuda:0 here, which CUDA IPC
+allows -- reproduce the single-domain forward run bit for bit.  torch.distributed (gloo) only
+carries the IPC blobs and the final gather."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests.common import make_plan, make_problem
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
+
+SHAPE, ORDER, NSTEPS = [44, 30, 34], 8, 40
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from paper_1808_01995_b200 import capi, slabs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    model, geom = make_problem(SHAPE, 10.0, 8, ORDER, NSTEPS)
+    bounds = slabs.split_slabs(model.N[0], world, ORDER // 2)
+    plan = make_plan(model, geom, ORDER, slab=bounds[rank])
+    plan.upload_traces(capi.CLOUD_SRC, geom.src)
+    drv = slabs.PeerPushDriver(plan, capi.OP_FORWARD, rank, world)
+    plan.step_begin(capi.OP_FORWARD)
+    dist.barrier()   # nobody pushes into a neighbour that is still zeroing its fields
+    drv.run(1, geom.nt - 1)
+    plan.step_end(capi.OP_FORWARD)
+    rec = torch.from_numpy(plan.download_traces(capi.CLOUD_REC))
+    u = np.zeros(model.N)
+    plan.wavefield(geom.nt - 1, out=u)
+    u = torch.from_numpy(u)
+    dist.all_reduce(rec)
+    dist.all_reduce(u)
+    dist.barrier()   # keep every mapping alive until all ranks are done
+    if rank == 0:
+        np.save(out + "_rec.npy", rec.numpy())
+        np.save(out + "_u.npy", u.numpy())
+    plan.close()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_push_between_processes_matches_single_domain(tmp_path, world):
+    import torch.multiprocessing as mp
+    model, geom = make_problem(SHAPE, 10.0, 8, ORDER, NSTEPS)
+    plan = make_plan(model, geom, ORDER)
+    rec1, _ = plan.forward(geom.src)
+    u1 = plan.wavefield(geom.nt - 1)
+    plan.close()
+    out = str(tmp_path / "ipc")
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert np.abs(rec1).max() > 0
+    assert np.array_equal(np.load(out + "_rec.npy"), rec1)
+    assert np.array_equal(np.load(out + "_u.npy"), u1)
