@@ -211,6 +211,24 @@ dim3 row_grid(const Plan& P, long long rows) {
 void download_field(Plan& P, const float* dev, const sfb_field_mview* out) {
     DevBuf tmp;
     const long long rows = (long long)P.n0 * P.N[1];
+    // a dense host array (numpy, a halo-free Function): move fp32 over the bus through the
+    // pinned halves and widen on host threads -- half the PCIe bytes of the general path
+    long long hs[3] = {0, 0, 0};
+    for (int a = 0; a < P.ndim; ++a) hs[3 - P.ndim + a] = out->stride[a];
+    const bool dense = (P.N[2] == 1 || hs[2] == 1) && (P.N[1] == 1 || hs[1] == P.N[2]) &&
+                       (P.N[0] == 1 || hs[0] == P.N[1] * P.N[2]);
+    if (dense) {
+        const float* src = dev;
+        if (P.pitch != P.N[2]) {
+            tmp.alloc(size_t(rows) * P.N[2] * 4, false);
+            pack_f32_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(dev, tmp.as<float>(), rows,
+                                                                   int(P.N[2]), P.pitch);
+            SFB_CUDA(cudaGetLastError());
+            src = tmp.as<float>();
+        }
+        download_f32(P, src, out->ptr + P.z_lo * hs[0], rows * P.N[2]);
+        return;
+    }
     tmp.alloc(size_t(rows) * P.N[2] * 8, false);
     convert_f32_pitched_f64<<<row_grid(P, rows), 256, 0, P.s_main>>>(dev, tmp.as<double>(), rows,
                                                                    int(P.N[2]), P.pitch);

@@ -117,6 +117,15 @@ static __global__ void convert_f32_pitched_f64(const float* __restrict__ src, do
         dst[row * n2 + x] = (double)src[row * pitch + x];
 }
 
+// fp32 pitched rows -> fp32 compact rows
+static __global__ void pack_f32_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                       long long rows, int n2, int pitch) {
+    const long long row = blockIdx.y * (long long)gridDim.z + blockIdx.z;
+    if (row >= rows) return;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n2; x += gridDim.x * blockDim.x)
+        dst[row * n2 + x] = src[row * pitch + x];
+}
+
 static __global__ void convert_f64_f32_flat(const double* __restrict__ src, float* __restrict__ dst,
                                      long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
