@@ -389,7 +389,8 @@ def ours(args):
         "config": workload_config(1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "acoustic_step_kernel", "kernel_ms": kern_s * 1e3,
+                     "kernel": ("acoustic_step_dual_kernel" if tile["stages"] < 0
+                                else "acoustic_step_kernel"), "kernel_ms": kern_s * 1e3,
                      "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts,
                      "tile": tile},
         "cpu_baseline": cpu,
