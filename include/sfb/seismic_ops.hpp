@@ -113,6 +113,10 @@ ExecutionReport run_gradient(GradientOp& g, Backend backend = Backend::Auto,
 // run_wave does (the result is bit-identical to the single-device run).
 ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model,
                                const AcquisitionGeometry& geom, const std::vector<int>& devices);
+// the TTI pair on slabs: two neighbour exchanges per step (g between the passes, the new p
+// and r levels after the update) as device-to-device copies between the plans
+ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model, const TtiModel& tti,
+                               const AcquisitionGeometry& geom, const std::vector<int>& devices);
 
 // proj/include/sf/seismic_ops.hpp:61, proj/src/seismic_ops.cpp:149-160
 double objective(const SparseFunction& pred, const std::vector<double>& observed);

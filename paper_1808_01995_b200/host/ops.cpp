@@ -312,6 +312,83 @@ ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model,
     return rep;
 }
 
+ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model, const TtiModel& tti,
+                               const AcquisitionGeometry& geom, const std::vector<int>& devices) {
+    if (!w.tti) throw ParameterError("run_wave_slabs: not a TTI operator");
+    if (devices.empty()) throw ParameterError("run_wave_slabs: empty device list");
+    if (model.grid()->ndim() != 3) throw CapabilityError("run_wave_slabs: 3-D grids only");
+    const long n0 = model.grid()->shape()[0];
+    const long K = w.space_order / 2, nslab = long(devices.size());
+    if (n0 / nslab < 2 * K)
+        throw ParameterError("run_wave_slabs: slabs thinner than two halo widths");
+    const int op = SFB_OP_TTI_FORWARD;
+    std::vector<std::unique_ptr<Engine>> eng;
+    long lo = 0;
+    sfb_field_view ev = Engine::view(*tti.epsilon), dv = Engine::view(*tti.delta),
+                   tv = Engine::view(*tti.theta), pv = Engine::view(*tti.phi);
+    for (long i = 0; i < nslab; ++i) {
+        const long hi = lo + n0 / nslab + (i < n0 % nslab ? 1 : 0);
+        eng.emplace_back(new Engine(model, geom, w.space_order, lo, hi, devices[std::size_t(i)]));
+        Engine& e = *eng.back();
+        e.check(sfb_set_model_tti(e.plan(), &ev, &dv, &tv, &pv));
+        e.check(sfb_upload_traces(e.plan(), SFB_CLOUD_SRC, w.inj->traces().data()));
+        e.check(sfb_step_begin(e.plan(), op, 0));
+        lo = hi;
+    }
+    auto sync_all = [&] {
+        for (auto& e : eng) e->check(sfb_stream_sync(e->plan()));
+    };
+    // ghost planes of `which` between every pair of neighbouring slabs
+    auto exchange = [&](int which, long t) {
+        sync_all();
+        for (long i = 0; i + 1 < nslab; ++i) {
+            Engine &a = *eng[std::size_t(i)], &b = *eng[std::size_t(i + 1)];
+            void *a_slo, *a_shi, *a_rlo, *a_rhi, *b_slo, *b_shi, *b_rlo, *b_rhi;
+            int64_t n = 0;
+            a.check(sfb_tti_halo_blocks(a.plan(), which, t, &a_slo, &a_shi, &a_rlo, &a_rhi, &n));
+            b.check(sfb_tti_halo_blocks(b.plan(), which, t, &b_slo, &b_shi, &b_rlo, &b_rhi, &n));
+            b.check(sfb_copy_halo(b.plan(), b_rlo, a_shi, n));
+            a.check(sfb_copy_halo(a.plan(), a_rhi, b_slo, n));
+        }
+        sync_all();
+    };
+    sync_all();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long t = 1; t < w.nt - 1; ++t) {
+        for (auto& e : eng) e->check(sfb_tti_step_rot(e->plan(), t, SFB_PART_ALL));
+        exchange(SFB_TTI_HALO_G_P, t);
+        exchange(SFB_TTI_HALO_G_R, t);
+        for (auto& e : eng) e->check(sfb_tti_step_update(e->plan(), t, SFB_PART_ALL));
+        exchange(SFB_TTI_HALO_P, t);
+        exchange(SFB_TTI_HALO_R, t);
+    }
+    for (auto& e : eng) e->check(sfb_step_end(e->plan(), op));
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<double>& out = w.smp->traces();
+    std::fill(out.begin(), out.end(), 0.0);
+    std::vector<double> part(out.size());
+    w.wavefield->zero();
+    w.wavefield_r->zero();
+    for (auto& e : eng) {
+        e->check(sfb_download_traces(e->plan(), SFB_CLOUD_REC, part.data()));
+        for (std::size_t i = 0; i < out.size(); ++i) out[i] += part[i];
+        if (w.nt >= 3)
+            for (int field = 0; field < 2; ++field)
+                for (long lvl : {w.nt - 1, w.nt - 2}) {
+                    TimeFunction& f = field ? *w.wavefield_r : *w.wavefield;
+                    sfb_field_mview mv = Engine::mview(f, lvl % f.time_slots());
+                    e->check(sfb_get_wavefield(e->plan(), field, lvl, &mv));
+                }
+    }
+    ExecutionReport rep;
+    double pts = 1;
+    for (long e : model.grid()->shape()) pts *= double(e);
+    rep.seconds = sec;
+    rep.steps = std::max(0L, w.nt - 2);
+    rep.gpts_per_s = sec > 0 ? pts * double(rep.steps) / sec / 1e9 : 0.0;
+    return rep;
+}
+
 // proj/src/seismic_ops.cpp:143-147
 ExecutionReport run_gradient(GradientOp& g, Backend, int) {
     if (!g.engine) throw BindingError("run_gradient: operator was not built");

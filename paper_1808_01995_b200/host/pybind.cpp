@@ -195,8 +195,16 @@ PYBIND11_MODULE(_sfb_host, m) {
           py::arg("space_order"), py::arg("save") = false, py::arg("tiles") = std::vector<long>{});
     m.def("adjoint_operator", &adjoint_operator);
     m.def("gradient_operator", &gradient_operator);
-    m.def("run_wave_slabs", &run_wave_slabs, py::arg("op"), py::arg("model"), py::arg("geom"),
-          py::arg("devices"), py::call_guard<py::gil_scoped_release>());
+    m.def("run_wave_slabs",
+          py::overload_cast<WaveOp&, const SeismicModel&, const AcquisitionGeometry&,
+                            const std::vector<int>&>(&run_wave_slabs),
+          py::arg("op"), py::arg("model"), py::arg("geom"), py::arg("devices"),
+          py::call_guard<py::gil_scoped_release>());
+    m.def("run_wave_slabs_tti",
+          py::overload_cast<WaveOp&, const SeismicModel&, const TtiModel&,
+                            const AcquisitionGeometry&, const std::vector<int>&>(&run_wave_slabs),
+          py::arg("op"), py::arg("model"), py::arg("tti"), py::arg("geom"), py::arg("devices"),
+          py::call_guard<py::gil_scoped_release>());
     m.def("run_wave", &run_wave, py::arg("op"), py::arg("backend") = Backend::Auto,
           py::arg("nthreads") = 1, py::call_guard<py::gil_scoped_release>());
     m.def("run_gradient", &run_gradient, py::arg("op"), py::arg("backend") = Backend::Auto,

@@ -53,8 +53,16 @@ def parts(t):
     plan.step_slab_boundary(F, t)
     plan.step_slab_interior(F, t)
 
+def only_boundary(t):
+    plan.step_slab_boundary(F, t)
+
+def only_interior(t):
+    plan.step_slab_interior(F, t)
+
 a = timed(whole)
 b = timed(parts)
+bnd_only = timed(only_boundary)
+int_only = timed(only_interior)
 # the same protocol with the fused halo push: neighbours on the same device stand in for the
 # peers (their ghost planes receive this slab's boundary planes as they are computed)
 def neighbour(lo, hi):
@@ -69,6 +77,6 @@ below.close(); above.close()
 K = order // 2
 print(json.dumps({"slab": [n0_slab, n, n], "order": order, "tile": plan.get_tile(),
                   "whole_ms": a * 1e3, "parts_ms": b * 1e3, "whole_gpts": pts / a / 1e9,
-                  "parts_gpts": pts / b / 1e9, "protocol_efficiency": a / b, "pushed_ms": c * 1e3, "pushed_efficiency": a / c,
+                  "parts_gpts": pts / b / 1e9, "protocol_efficiency": a / b, "boundary_alone_ms": bnd_only * 1e3, "interior_alone_ms": int_only * 1e3, "pushed_ms": c * 1e3, "pushed_efficiency": a / c,
                   "halo_mb_per_neighbour": K * n * n * 4 / 1e6}))
 plan.close()
