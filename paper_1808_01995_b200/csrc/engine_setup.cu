@@ -77,9 +77,11 @@ void select_variant(Plan& P, int txv, int ty, int nst, int dual) {
         if (txv > 0 && (v.TXV != txv || v.TY != ty || (nst > 0 && v.NST != nst))) continue;
         if (txv <= 0) {
             // default shape (measured on B200, tools/probe_tiles.py): the ring kernel up to
-            // order 8, the dual-stream kernel (4 stages) above, 64 x 16 tiles
+            // order 8, the dual-stream kernel (4 stages) above; 64 x 16 tiles, 64 x 14 from
+            // order 14 up
             const bool want_dual = P.K >= 5;
-            if (v.dual != want_dual || v.rotate || v.TXV != 16 || v.TY != 16) continue;
+            const int want_ty = P.K >= 7 ? 14 : 16;
+            if (v.dual != want_dual || v.rotate || v.TXV != 16 || v.TY != want_ty) continue;
             if (v.NST != (want_dual ? 4 : P.K + 3)) continue;
         }
         if (!best) best = &v;
