@@ -325,15 +325,18 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
     return rec, u, grad
 
 
-def test_fused_halo_push_matches_single_domain_bitwise():
+@pytest.mark.parametrize("order,shape,nslab", [(8, [48, 30, 34], 3), (16, [64, 30, 34], 2),
+                                               (12, [64, 30, 34], 2)])
+def test_fused_halo_push_matches_single_domain_bitwise(order, shape, nslab):
     """sfb_link_peers: the boundary kernels store their planes (and the point kernel its
     injected nodes) directly into the neighbours' ghost planes; slabs are ordered by events
-    only.  Forward, adjoint and gradient equal the single-domain run bit for bit."""
+    only.  Forward, adjoint and gradient equal the single-domain run bit for bit (ring
+    kernel at order 8, dual-stream kernels with 16- and 14-row tiles above)."""
     from paper_1808_01995_b200 import capi
-    model, geom = make_problem([48, 30, 34], 10.0, 8, 8, 50)
+    model, geom = make_problem(shape, 10.0, 8, order, 50)
     rng = np.random.default_rng(9)
     data = rng.standard_normal((geom.nt, geom.n_rec)) * np.hanning(geom.nt)[:, None]
-    plan = make_plan(model, geom, 8)
+    plan = make_plan(model, geom, order)
     rec1, _ = plan.forward(geom.src)
     u1 = plan.wavefield(geom.nt - 1)
     srca1, _ = plan.adjoint(data)
@@ -343,12 +346,12 @@ def test_fused_halo_push_matches_single_domain_bitwise():
     plan.close()
     n0 = model.N[0]
     src_plane = int(geom.src_base[0][0])
-    cuts = [0, 20, src_plane + 1, n0]          # the source cell straddles a cut
-    rec3, u3, _ = _run_slabs(model, geom, 8, cuts, pushed=True)
+    cuts = [0, 20, src_plane + 1, n0] if nslab == 3 else [0, src_plane + 1, n0]   # source on a cut
+    rec3, u3, _ = _run_slabs(model, geom, order, cuts, pushed=True)
     assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
-    srca3, v3, _ = _run_slabs(model, geom, 8, cuts, op=capi.OP_ADJOINT, inj=data, pushed=True)
+    srca3, v3, _ = _run_slabs(model, geom, order, cuts, op=capi.OP_ADJOINT, inj=data, pushed=True)
     assert np.array_equal(srca3, srca1) and np.array_equal(v3, v1)
-    _, _, g3 = _run_slabs(model, geom, 8, cuts, op=capi.OP_GRADIENT, save_every=2, inj=data,
+    _, _, g3 = _run_slabs(model, geom, order, cuts, op=capi.OP_GRADIENT, save_every=2, inj=data,
                           prior_forward=True, pushed=True)
     assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
 
