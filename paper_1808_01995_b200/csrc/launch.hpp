@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <utility>
 
 namespace sfb {
@@ -22,7 +23,9 @@ cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, int threads, size_t
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    // SFB_NO_PDL=1 launches with plain stream order (validation: results must not change)
+    static const bool plain = std::getenv("SFB_NO_PDL") != nullptr;
+    cfg.numAttrs = plain ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -21,6 +21,7 @@ rw = np.zeros((rb.shape[0], 8)); rw[:, 0] = 0.7; rw[:, 4] = 0.3
 sb = np.array([[n // 2, n // 2, 41]], dtype=np.int64)
 sw = np.full((1, 8), 0.125)
 out = []
+dump = os.environ.get("SOAK_DUMP")   # save the order-8 traces, to compare runs across launch modes
 for order, tile in ((8, None), (8, (16, 16, -103)), (8, (16, 16, -3)), (12, None), (16, None), (4, None)):
     dt = capi.critical_dt([h] * 3, vmax, order)
     nt = steps + 2
@@ -37,6 +38,8 @@ for order, tile in ((8, None), (8, (16, 16, -103)), (8, (16, 16, -3)), (12, None
         rec, _ = plan.forward(src, save_every=8)
         recs.append(rec); lv.append(plan.wavefield(nt - 1))
     res["forward_equal"] = bool(np.array_equal(recs[0], recs[1]) and np.array_equal(lv[0], lv[1]))
+    if dump and tile is None:
+        np.save(f"{dump}_rec_so{order}.npy", recs[0].astype(np.float32))
     res["finite"] = bool(np.isfinite(lv[0]).all()); res["absmax"] = float(np.abs(lv[0]).max())
     resid = np.random.default_rng(3).standard_normal(rec.shape) * np.hanning(nt)[:, None]
     gs = [plan.gradient(resid)[0] for _ in range(2)]
