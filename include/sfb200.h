@@ -221,7 +221,10 @@ SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour);
  * sfb_link_peers_ipc maps the neighbours' blobs (NULL at an outer face).  Every boundary
  * half-step then ends by writing the plan's step counter with a stream memory operation,
  * and sfb_peer_wait_ipc makes both streams of the plan wait, on the device, until the
- * neighbours' counters have reached its own: no host-side handshake per step. */
+ * neighbours' counters have reached its own: no host-side handshake per step.  All linked
+ * plans must make the same sequence of boundary half-steps, link before any of them steps,
+ * and stay alive until every rank has synchronised its last step (their streams read this
+ * plan's counter). */
 #define SFB_PEER_BLOB_BYTES 256
 SFB_API int sfb_peer_export(sfb_plan* plan, void* blob);
 SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* hi_blob);
