@@ -210,8 +210,10 @@ SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, v
  * injected into them -- directly into the neighbours' ghost planes as it computes them (peer
  * stores over NVLink): no copy, no send/recv.  Ordering is by events: before its next
  * step a plan calls sfb_peer_wait(plan, neighbour) for each neighbour, which makes both of
- * its streams wait for that neighbour's last boundary half-step (its pushes have landed, and
- * it has finished reading the ghost planes this plan will overwrite next).  Acoustic
+ * its streams wait for that neighbour's last boundary half-step (its pushes have landed) and
+ * its boundary stream -- the one that stores into peer memory -- also for the neighbour's
+ * last INTERIOR half-step, whose gather is the last reader of the ghost planes this plan
+ * overwrites next (a receiver cell that straddles the cut reads one).  Acoustic
  * operators; lo / hi are the plans of the slabs below / above, or NULL at an outer face. */
 SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi);
 SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour);
@@ -219,9 +221,10 @@ SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour);
  * SFB_PEER_BLOB_BYTES (CUDA IPC handles of the plan's wavefield buffers and of its step
  * counter) that the caller ships to the neighbouring ranks by any means;
  * sfb_link_peers_ipc maps the neighbours' blobs (NULL at an outer face).  Every boundary
- * half-step then ends by writing the plan's step counter with a stream memory operation,
- * and sfb_peer_wait_ipc makes both streams of the plan wait, on the device, until the
- * neighbours' counters have reached its own: no host-side handshake per step.  All linked
+ * half-step and every interior half-step then ends by writing one of the plan's two step
+ * counters with a stream memory operation, and sfb_peer_wait_ipc makes the plan's streams
+ * wait, on the device, until the neighbours' counters have reached its own (same two
+ * conditions as sfb_peer_wait): no host-side handshake per step.  All linked
  * plans must make the same sequence of boundary half-steps, link before any of them steps,
  * and stay alive until every rank has synchronised its last step (their streams read this
  * plan's counter). */
@@ -243,6 +246,9 @@ SFB_API int sfb_tti_step_update(sfb_plan* plan, int64_t t, int part);
 SFB_API int sfb_tti_halo_blocks(sfb_plan* plan, int which, int64_t t, void** send_lo,
                                 void** send_hi, void** recv_lo, void** recv_hi, int64_t* count);
 SFB_API int sfb_stream_sync(sfb_plan* plan);
+/* test aid: keeps the plan's main (0) or boundary (1) stream busy for `microseconds`
+ * (<= 1 s) at the point of the call, to shake out ordering races between linked slabs */
+SFB_API int sfb_debug_stall(sfb_plan* plan, int boundary_stream, int64_t microseconds);
 /* raw CUDA stream handles (cudaStream_t) the plan launches on: main, then boundary */
 SFB_API int sfb_streams(sfb_plan* plan, void** main_stream, void** boundary_stream);
 /* adopt caller-owned streams (e.g. the streams a collective library orders against) */

@@ -269,33 +269,64 @@ long sfo_locate(int ndim, const long *N, const double *h, const double *origin, 
  *   out = ( L(cur) - m*(old - 2 cur)/dt^2 + 1/2 damp*old/dt ) * inv0
  * cur/old/out are haloed arrays (zero halo = the reference's Dirichlet reads,
  * include/sf/function.hpp:17); m/damp/inv0 are compact. */
+/* one row of the dense update with the halo width known at compile time (inlined into the
+ * switch below, so gcc unrolls the stencil and vectorises along the contiguous axis; the
+ * summation order per node is unchanged: centre, then neighbours K..1, axis by axis) */
+static inline __attribute__((always_inline)) void dense_row(
+    const int K, const long N2, const long s0, const long s1, const int a0, const int a1,
+    const int a2, const double *ih2, const double *w2, const double s0dt, const double s1dt,
+    const double *restrict cur, const double *restrict old, double *restrict out,
+    const double *restrict m, const double *restrict damp, const double *restrict inv0) {
+#pragma omp simd
+    for (long l = 0; l < N2; ++l) {
+        double lap = 0.0;
+        if (a0) {
+            double acc = w2[0] * cur[l];
+            for (int jj = K; jj >= 1; --jj) acc += w2[jj] * (cur[l - jj * s0] + cur[l + jj * s0]);
+            lap += acc * ih2[0];
+        }
+        if (a1) {
+            double acc = w2[0] * cur[l];
+            for (int jj = K; jj >= 1; --jj) acc += w2[jj] * (cur[l - jj * s1] + cur[l + jj * s1]);
+            lap += acc * ih2[1];
+        }
+        if (a2) {
+            double acc = w2[0] * cur[l];
+            for (int jj = K; jj >= 1; --jj) acc += w2[jj] * (cur[l - jj] + cur[l + jj]);
+            lap += acc * ih2[2];
+        }
+        double v = -1.0 * (-1.0 * lap + m[l] * (old[l] + (-2.0) * cur[l]) * s1dt +
+                           (-0.5) * damp[l] * old[l] * s0dt);
+        out[l] = v * inv0[l];
+    }
+}
+
 static void dense_update(const emb3 *e, const double *w2, double dt, const double *cur,
                          const double *old, double *out, const double *m,
                          const double *damp, const double *inv0) {
     const int K = e->K;
     const double s0 = 1.0 / dt, s1 = 1.0 / (dt * dt);
     const long N0 = e->N[0], N1 = e->N[1], N2 = e->N[2];
-    const long st[3] = {e->s0, e->s1, 1};
 #pragma omp parallel for collapse(2) schedule(static)
     for (long i = 0; i < N0; ++i)
         for (long j = 0; j < N1; ++j) {
             size_t row = hidx(e, i, j, 0);
             size_t crow = ((size_t)i * N1 + j) * N2;
-            for (long l = 0; l < N2; ++l) {
-                size_t q = row + l;
-                double lap = 0.0;
-                for (int d = 0; d < 3; ++d) {
-                    if (!e->act[d]) continue;
-                    double acc = w2[0] * cur[q];
-                    for (int jj = K; jj >= 1; --jj)
-                        acc += w2[jj] * (cur[q - jj * st[d]] + cur[q + jj * st[d]]);
-                    lap += acc * e->ih2[d];
-                }
-                double mm = m[crow + l], dd = damp[crow + l];
-                double v = -1.0 * (-1.0 * lap + mm * (old[q] + (-2.0) * cur[q]) * s1 +
-                                   (-0.5) * dd * old[q] * s0);
-                out[q] = v * inv0[crow + l];
+#define SFO_ROW(KK)                                                                          \
+    dense_row(KK, N2, e->s0, e->s1, e->act[0], e->act[1], e->act[2], e->ih2, w2, s0, s1,     \
+              cur + row, old + row, out + row, m + crow, damp + crow, inv0 + crow)
+            switch (K) {
+            case 1: SFO_ROW(1); break;
+            case 2: SFO_ROW(2); break;
+            case 3: SFO_ROW(3); break;
+            case 4: SFO_ROW(4); break;
+            case 5: SFO_ROW(5); break;
+            case 6: SFO_ROW(6); break;
+            case 7: SFO_ROW(7); break;
+            case 8: SFO_ROW(8); break;
+            default: SFO_ROW(K); break;
             }
+#undef SFO_ROW
         }
 }
 

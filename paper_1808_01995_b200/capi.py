@@ -48,7 +48,7 @@ SYMBOLS = [
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
     "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
-    "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune",
+    "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune", "sfb_debug_stall",
 ]
 
 lib.sfb_last_error.restype = C.c_char_p
@@ -88,6 +88,7 @@ lib.sfb_link_peers_ipc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 lib.sfb_peer_wait_ipc.argtypes = [C.c_void_p]
 PEER_BLOB_BYTES = 256
 lib.sfb_stream_sync.argtypes = [C.c_void_p]
+lib.sfb_debug_stall.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_streams.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
 lib.sfb_set_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 lib.sfb_copy_halo.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
@@ -108,7 +109,7 @@ class SfbError(RuntimeError):
 
 
 def _view(a: np.ndarray) -> FieldView:
-    assert a.dtype == np.float64
+    assert a.dtype == np.float64 and 1 <= a.ndim <= 3
     v = FieldView()
     v.ptr = a.ctypes.data
     for d in range(a.ndim):
@@ -187,9 +188,10 @@ class Plan:
         self._chk(lib.sfb_set_model(self.h, C.byref(_view(m)), C.byref(_view(damp)), float(v_max)))
 
     def set_model_tti(self, epsilon, delta, theta, phi):
-        views = [_view(np.asarray(f, dtype=np.float64)) for f in (epsilon, delta, theta, phi)]
-        self._keep = views
+        arrs = [np.asarray(f, dtype=np.float64) for f in (epsilon, delta, theta, phi)]
+        views = [_view(a) for a in arrs]   # FieldView.ptr is a bare address: arrs must outlive the call
         self._chk(lib.sfb_set_model_tti(self.h, *[C.byref(v) for v in views]))
+        del arrs
 
     def tti_forward(self, src):
         src = np.ascontiguousarray(src, dtype=np.float64)
@@ -345,6 +347,9 @@ class Plan:
 
     def copy_halo(self, dst, src, count):
         self._chk(lib.sfb_copy_halo(self.h, dst, src, count))
+
+    def debug_stall(self, boundary_stream, microseconds):
+        self._chk(lib.sfb_debug_stall(self.h, int(boundary_stream), int(microseconds)))
 
     def sync(self):
         self._chk(lib.sfb_stream_sync(self.h))

@@ -42,6 +42,16 @@ struct PeerBlob {   // what sfb_peer_export writes into the caller's SFB_PEER_BL
 };
 static_assert(sizeof(PeerBlob) <= SFB_PEER_BLOB_BYTES, "peer blob");
 
+// test aid (sfb_debug_stall): occupy a stream for a given time
+__global__ void stall_kernel(unsigned long long ns) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    } while (t1 - t0 < ns);
+}
+
 void close_ipc(Plan& P) {
     for (int side = 0; side < 2; ++side) {
         for (int b = 0; b < 2; ++b)
@@ -222,6 +232,7 @@ SFB_API int sfb_plan_create(const sfb_plan_desc* desc, sfb_plan** out) {
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_main, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_bnd, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_push, cudaEventDisableTiming));
+        SFB_CUDA(cudaEventCreateWithFlags(&P.ev_done, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreate(&P.ev_t0));
         SFB_CUDA(cudaEventCreate(&P.ev_t1));
         P.u[0].alloc(size_t(P.ucount) * 4);
@@ -248,6 +259,7 @@ SFB_API int sfb_plan_destroy(sfb_plan* plan) {
     if (plan->ev_main) cudaEventDestroy(plan->ev_main);
     if (plan->ev_bnd) cudaEventDestroy(plan->ev_bnd);
     if (plan->ev_push) cudaEventDestroy(plan->ev_push);
+    if (plan->ev_done) cudaEventDestroy(plan->ev_done);
     close_ipc(*plan);
     if (plan->ev_t0) cudaEventDestroy(plan->ev_t0);
     if (plan->ev_t1) cudaEventDestroy(plan->ev_t1);
@@ -742,7 +754,7 @@ SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* 
                     P.peer_hi[b] = base;                              // its low ghost planes
             }
         }
-        P.push_count = 0;
+        P.push_count = P.done_count = 0;
         SFB_CUDA(cudaMemsetAsync(P.push_flag.p, 0, 256, P.s_main));
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
     });
@@ -753,18 +765,25 @@ SFB_API int sfb_peer_wait_ipc(sfb_plan* plan) {
     return guarded(plan, [&] {
         Plan& P = *plan;
         static StreamValueFn wait_value = stream_value_fn("cuStreamWaitValue32");
-        // every slab has made the same number of boundary half-steps when its neighbours
-        // may go on: wait until theirs have reached this plan's own count
+        auto wait = [&](cudaStream_t st, CUdeviceptr word, unsigned value) {
+            CUresult rc = wait_value(st, word, value, CU_STREAM_WAIT_VALUE_GEQ);
+            if (rc != CUDA_SUCCESS)
+                throw Failure(SFB_ERR_CUDA, "cuStreamWaitValue32 failed with code " +
+                                                std::to_string(int(rc)));
+        };
+        // every slab has made the same number of half-steps when its neighbours may go on
         for (int side = 0; side < 2; ++side) {
             if (!P.ipc_flag[side]) continue;
             const CUdeviceptr f = reinterpret_cast<CUdeviceptr>(P.ipc_flag[side]);
-            for (cudaStream_t st : {P.s_main, P.s_bnd}) {
-                CUresult rc = wait_value(st, f, P.push_count, CU_STREAM_WAIT_VALUE_GEQ);
-                if (rc != CUDA_SUCCESS)
-                    throw Failure(SFB_ERR_CUDA, "cuStreamWaitValue32 failed with code " +
-                                                    std::to_string(int(rc)));
-                if (P.s_bnd == P.s_main) break;
-            }
+            // (1) their pushes of this step have landed in this plan's ghost planes: both
+            // streams read those next step
+            wait(P.s_main, f, P.push_count);
+            if (P.s_bnd != P.s_main) wait(P.s_bnd, f, P.push_count);
+            // (2) they have finished READING their own ghost planes of the level this plan's
+            // next boundary half-step overwrites (their last reader is the gather of the
+            // interior half-step, on their main stream): only the boundary stream stores
+            // into peer memory
+            wait(P.s_bnd, f + 4, P.done_count);
         }
     });
 }
@@ -772,17 +791,34 @@ SFB_API int sfb_peer_wait_ipc(sfb_plan* plan) {
 SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour) {
     if (!plan || !neighbour) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
+        // (1) the neighbour's pushes of this step have landed (both streams read them)
         SFB_CUDA(cudaStreamWaitEvent(plan->s_main, neighbour->ev_push, 0));
         if (plan->s_bnd != plan->s_main)
             SFB_CUDA(cudaStreamWaitEvent(plan->s_bnd, neighbour->ev_push, 0));
+        // (2) the neighbour's gather has finished reading the ghost planes this plan's next
+        // boundary half-step overwrites
+        SFB_CUDA(cudaStreamWaitEvent(plan->s_bnd, neighbour->ev_done, 0));
     });
 }
 
 SFB_API int sfb_step_slab_interior(sfb_plan* plan, int op, int64_t t) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
-        step_compute(*plan, op, t, SFB_PART_INTERIOR);
-        step_points(*plan, op, t, SFB_PART_INTERIOR);
+        Plan& P = *plan;
+        step_compute(P, op, t, SFB_PART_INTERIOR);
+        step_points(P, op, t, SFB_PART_INTERIOR);
+        if (P.peer_lo[0] || P.peer_hi[0]) {   // linked: the ghost planes of level t are free
+            SFB_CUDA(cudaEventRecord(P.ev_done, P.s_main));
+            if (P.ipc_flag[0] || P.ipc_flag[1]) {
+                static StreamValueFn write_value = stream_value_fn("cuStreamWriteValue32");
+                CUresult rc = write_value(P.s_main,
+                                          reinterpret_cast<CUdeviceptr>(P.push_flag.p) + 4,
+                                          ++P.done_count, 0);
+                if (rc != CUDA_SUCCESS)
+                    throw Failure(SFB_ERR_CUDA, "cuStreamWriteValue32 failed with code " +
+                                                    std::to_string(int(rc)));
+            }
+        }
     });
 }
 
@@ -811,6 +847,15 @@ SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, v
         if (send_hi) *send_hi = u + (long long)P.n0 * P.plane;
         if (recv_hi) *recv_hi = u + (long long)(P.n0 + P.K) * P.plane;
         if (count) *count = blk;
+    });
+}
+
+SFB_API int sfb_debug_stall(sfb_plan* plan, int boundary_stream, int64_t microseconds) {
+    if (!plan || microseconds < 0 || microseconds > 1000000) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        stall_kernel<<<1, 1, 0, boundary_stream ? plan->s_bnd : plan->s_main>>>(
+            (unsigned long long)microseconds * 1000ull);
+        SFB_CUDA(cudaGetLastError());
     });
 }
 

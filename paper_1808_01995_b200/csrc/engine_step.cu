@@ -101,8 +101,18 @@ void mark_stream(Plan& P, int part) {
 }
 
 
+// the acoustic stepping entry points: no TTI state, and imaging needs a bound history
+// (t % save_every below must not divide by zero across the C ABI)
+static void check_step_op(const Plan& P, int op, const OpRoles& ro, const StepExtras* ex) {
+    require(op != SFB_OP_TTI_FORWARD, SFB_ERR_PARAMETER,
+            "the TTI operator steps through sfb_tti_step_rot / sfb_tti_step_update");
+    require(!ro.imaging || (ex && ex->usave) || (P.history_valid && P.save_every > 0),
+            SFB_ERR_PARAMETER, "gradient_operator: saved forward history required");
+}
+
 void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) {
     const OpRoles ro = roles(op);
+    check_step_op(P, op, ro, ex);
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;
     const bool pair = part == kPartBoundaryPair;   // needs n0 >= 2K (split_slabs guarantees it)
@@ -189,6 +199,7 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
 void step_points(Plan& P, int op, long long t, int part, float* target_override, bool allow_gather,
                  const StepExtras* ex) {
     const OpRoles ro = roles(op);
+    check_step_op(P, op, ro, ex);
     const int cur = int(t & 1), oth = cur ^ 1;
     const long long tnew = ro.backward ? t - 1 : t + 1;
     Cloud& ci = P.cloud[ro.inj];

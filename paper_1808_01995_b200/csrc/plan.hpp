@@ -143,11 +143,16 @@ struct Plan {
     float* peer_lo[2] = {nullptr, nullptr};
     float* peer_hi[2] = {nullptr, nullptr};
     cudaEvent_t ev_push = nullptr;
+    // ... and the event that closes the interior half-step, whose gather is the last reader
+    // of this slab's ghost planes of the current level: a neighbour may overwrite them (the
+    // push of its next boundary half-step) only after it
+    cudaEvent_t ev_done = nullptr;
     // neighbours in other processes (sfb_peer_export / sfb_link_peers_ipc): their buffers are
     // mapped through CUDA IPC, and the boundary half-steps are counted in a device word per
     // plan that the neighbours' streams wait on (stream memory operations: no host handshake)
-    DevBuf push_flag;                    // [0]: boundary half-steps completed since linking
-    unsigned push_count = 0;
+    DevBuf push_flag;                    // [0]: boundary half-steps completed since linking,
+                                         // [1]: interior half-steps (ghost-plane readers done)
+    unsigned push_count = 0, done_count = 0;
     void* ipc_u[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [lo/hi][parity], opened
     void* ipc_flag[2] = {nullptr, nullptr};                         // [lo/hi], opened
     bool main_pending = false, bnd_pending = false;

@@ -256,7 +256,7 @@ def test_unstable_dt_and_nan_guard():
 
 
 def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_forward=False,
-               fused=False, pushed=False):
+               fused=False, pushed=False, stall=None):
     """N plans on one device stepping in lockstep with device-to-device ghost copies:
     the single-GPU emulation of the multi-GPU slab protocol.  Returns the summed sampled
     traces, the assembled last level and (gradient) the assembled grad."""
@@ -275,8 +275,10 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
         ts = range(geom.nt - 2, 0, -1) if o != capi.OP_FORWARD else range(1, geom.nt - 1)
         for t in ts:
             if pushed:   # no copies and no host synchronisation: events order the slabs
-                for p in plans:
+                for i, p in enumerate(plans):
                     p.step_slab_boundary(o, t)
+                    if stall and i == stall[0]:   # hold this slab's main stream back
+                        p.debug_stall(0, stall[1])
                     p.step_slab_interior(o, t)
                 for i, p in enumerate(plans):
                     if i > 0:
@@ -354,6 +356,39 @@ def test_fused_halo_push_matches_single_domain_bitwise(order, shape, nslab):
     _, _, g3 = _run_slabs(model, geom, order, cuts, op=capi.OP_GRADIENT, save_every=2, inj=data,
                           prior_forward=True, pushed=True)
     assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
+
+
+@pytest.mark.parametrize("slow_slab", [0, 1])
+def test_fused_halo_push_waits_for_the_ghost_plane_readers(slow_slab):
+    """A receiver cell that straddles a slab cut is gathered by the slab below, which reads
+    its high ghost plane in the interior half-step.  The neighbour's next boundary half-step
+    overwrites that plane, so it must wait for the gather, not only for the boundary
+    half-step (round-1 advisor finding): one slab's main stream is held back 300 us every
+    step, off-node receivers sit in the last plane below each cut."""
+    from paper_1808_01995_b200 import capi
+    shape, h, nbl = [48, 30, 34], 10.0, 8
+    cuts = [0, 22, 43, shape[0] + 2 * nbl]
+    rec = [[(c - 1 - nbl + 0.4) * h, 0.5 * (shape[1] - 1) * h, 4.5 * h] for c in cuts[1:-1]]
+    rec += [[(c - nbl + 0.3) * h, 0.45 * (shape[1] - 1) * h, 3.2 * h] for c in cuts[1:-1]]
+    model, geom = make_problem(shape, h, nbl, 8, 40, rec=rec)
+    assert sorted(int(b[0]) for b in geom.rec_base)[:2] == [cuts[1] - 1, cuts[1]]
+    plan = make_plan(model, geom, 8)
+    rec1, _ = plan.forward(geom.src)
+    u1 = plan.wavefield(geom.nt - 1)
+    plan.close()
+    assert np.abs(rec1).min(axis=0).max() >= 0 and (np.abs(rec1).max(axis=0) > 0).all()
+    rec3, u3, _ = _run_slabs(model, geom, 8, cuts, pushed=True, stall=(slow_slab, 300))
+    assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
+    # the adjoint samples at the source cell: put it across the first cut as well
+    src = [[(cuts[1] - 1 - nbl + 0.37) * h, 0.5 * (shape[1] - 1) * h, 2.13 * h]]
+    model, geom = make_problem(shape, h, nbl, 8, 40, rec=rec, src=src)
+    data = np.random.default_rng(3).standard_normal((geom.nt, geom.n_rec)) * np.hanning(geom.nt)[:, None]
+    plan = make_plan(model, geom, 8)
+    srca1, _ = plan.adjoint(data)
+    plan.close()
+    srca3, _, _ = _run_slabs(model, geom, 8, cuts, op=capi.OP_ADJOINT, inj=data, pushed=True,
+                             stall=(slow_slab, 300))
+    assert np.abs(srca1).max() > 0 and np.array_equal(srca3, srca1)
 
 
 def test_link_peers_checks_the_neighbours():

@@ -100,8 +100,13 @@ def test_two_slabs_equal_one_domain_at_full_size(full):
 
 def test_gradient_imaging_at_full_size(full):
     """config 3: forward saving every 4th level in HBM, adjoint sweep driven by random
-    residuals, fused imaging.  Checked against the imaging condition evaluated on the
-    host from the plan's own saved / live levels on a sub-volume."""
+    residuals, fused imaging.  Properties here (zero in / zero out, linearity) and a VALUE
+    check of a sub-volume around the source: the imaging condition
+    grad -= u_saved[t] (v[t-1] - 2 v[t] + v[t+1]) / dt^2 (proj/src/seismic_ops.cpp:132)
+    re-evaluated on the host in f64 from wavefield levels downloaded step by step through
+    the stepping entry points.  (The whole gradient is compared with the oracle's sweep in
+    tests/test_gpu_parity_fullsize.py.)"""
+    from paper_1808_01995_b200 import capi
     model, geom = full
     plan = plan_for(model, geom)
     src = np.ascontiguousarray(geom.src.traces)
@@ -117,6 +122,26 @@ def test_gradient_imaging_at_full_size(full):
     # linear in the residual
     g2, _ = plan.gradient(2.0 * resid)
     assert rel_l2(g2, 2.0 * g) <= 1e-7
+    # value check on a sub-volume: saved forward levels and adjoint levels, one step at a time
+    nt = geom.nt
+    b = [int(x) for x in np.array(geom.src.base_table).reshape(-1, 3)[0]]
+    box = tuple(slice(max(c - 12, 0), c + 12) for c in b)
+    buf = np.zeros(plan.shape)
+    saved = {t: plan.wavefield(t, out=buf)[box].copy() for t in range(4, nt - 1, 4)}
+    G = capi.OP_ADJOINT   # the gradient sweep's wavefield is the adjoint run of the residual
+    plan.upload_traces(capi.CLOUD_REC, resid)
+    plan.step_begin(G)
+    levels = {nt - 1: np.zeros_like(saved[4]), nt - 2: np.zeros_like(saved[4])}
+    want = np.zeros_like(saved[4])
+    inv_dt2 = 1.0 / geom.dt ** 2
+    for t in range(nt - 2, 0, -1):
+        plan.run_steps(G, t, t + 1)                    # writes level t-1
+        levels[t - 1] = plan.wavefield(t - 1, out=buf)[box].copy()
+        if t % 4 == 0:
+            want -= saved[t] * (levels[t - 1] - 2.0 * levels[t] + levels[t + 1]) * inv_dt2
+        levels.pop(t + 1)
+    assert np.abs(want).max() > 0
+    assert rel_l2(g[box], want) <= 1e-4
     plan.close()
 
 
