@@ -631,7 +631,11 @@ SFB_API int sfb_step_compute(sfb_plan* plan, int op, int64_t t, int part) {
 
 SFB_API int sfb_step_points(sfb_plan* plan, int op, int64_t t, int part) {
     if (!plan) return SFB_ERR_PARAMETER;
-    return guarded(plan, [&] { step_points(*plan, op, t, part); });
+    return guarded(plan, [&] {
+        require(op != SFB_OP_TTI_FORWARD, SFB_ERR_PARAMETER,
+                "the TTI operator steps through sfb_tti_step_rot / sfb_tti_step_update");
+        step_points(*plan, op, t, part);
+    });
 }
 
 SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t) {

@@ -103,15 +103,16 @@ void mark_stream(Plan& P, int part) {
 
 // the acoustic stepping entry points: no TTI state, and imaging needs a bound history
 // (t % save_every below must not divide by zero across the C ABI)
-static void check_step_op(const Plan& P, int op, const OpRoles& ro, const StepExtras* ex) {
-    require(op != SFB_OP_TTI_FORWARD, SFB_ERR_PARAMETER,
-            "the TTI operator steps through sfb_tti_step_rot / sfb_tti_step_update");
+static void check_step_op(const Plan& P, int, const OpRoles& ro, const StepExtras* ex) {
     require(!ro.imaging || (ex && ex->usave) || (P.history_valid && P.save_every > 0),
             SFB_ERR_PARAMETER, "gradient_operator: saved forward history required");
 }
 
 void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) {
     const OpRoles ro = roles(op);
+    // the TTI pair has its own update launches (engine_tti.cu); only its point work comes here
+    require(op != SFB_OP_TTI_FORWARD, SFB_ERR_PARAMETER,
+            "the TTI operator steps through sfb_tti_step_rot / sfb_tti_step_update");
     check_step_op(P, op, ro, ex);
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;

@@ -118,13 +118,15 @@ std::shared_ptr<TimeFunction> TimeFunction::create(std::string name,
 std::shared_ptr<SparseFunction> SparseFunction::create(std::string name,
                                                        std::shared_ptr<const Grid> grid,
                                                        std::vector<double> coords, long nt) {
-    if (!grid) throw ParameterError("sparse function needs a grid");
-    if (nt < 1) throw ParameterError("sparse function needs nt >= 1");
-    const std::size_t nd = std::size_t(grid->ndim());
-    if (coords.empty() || coords.size() % nd != 0)
-        throw ParameterError("coordinate list size must be a multiple of grid rank");
-    return std::shared_ptr<SparseFunction>(
+    if (!grid) throw ParameterError("point cloud '" + name + "': no grid given");
+    const std::size_t rank = std::size_t(grid->ndim());
+    if (coords.empty() || coords.size() % rank)
+        throw ParameterError("point cloud '" + name + "': " + std::to_string(coords.size()) +
+                             " coordinates do not form points of rank " + std::to_string(rank));
+    if (nt < 1) throw ParameterError("point cloud '" + name + "': traces need at least one sample");
+    std::shared_ptr<SparseFunction> cloud(
         new SparseFunction(std::move(name), std::move(grid), std::move(coords), nt));
+    return cloud;
 }
 
 SparseFunction::SparseFunction(std::string name, std::shared_ptr<const Grid> grid,

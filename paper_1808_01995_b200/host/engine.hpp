@@ -31,6 +31,7 @@ public:
         d.device = dev >= 0 ? dev : device();
         d.slab_lo = slab_lo;
         d.slab_hi = slab_hi;
+        desc_ = d;
         int rc = sfb_plan_create(&d, &plan_);
         if (rc != SFB_OK) raise_status(rc, sfb_last_error(nullptr));
         try {
@@ -48,6 +49,29 @@ public:
     Engine& operator=(const Engine&) = delete;
 
     sfb_plan* plan() const { return plan_; }
+
+    // ---- reuse across shots and iterations (the fwi driver) -------------------------------
+    // a plan is tied to the grid, the order and the time axis; the model fields and the two
+    // point clouds can be replaced on a live plan
+    bool fits(const SeismicModel& model, const AcquisitionGeometry& geom, int space_order) const {
+        const Grid& g = *model.grid();
+        if (g.ndim() != desc_.ndim || space_order != desc_.space_order) return false;
+        if (geom.nt() != desc_.nt || geom.dt() != desc_.dt) return false;
+        for (int a = 0; a < desc_.ndim; ++a)
+            if (g.shape()[std::size_t(a)] != desc_.shape[a] ||
+                g.spacing()[std::size_t(a)] != desc_.spacing[a])
+                return false;
+        return true;
+    }
+    void rebind_model(const SeismicModel& model) {
+        sfb_field_view mv = view(*model.m()), dv = view(*model.damp());
+        check(sfb_set_model(plan_, &mv, &dv, model.v_max()));
+    }
+    void rebind_geometry(const AcquisitionGeometry& geom) {
+        bind_cloud(SFB_CLOUD_SRC, *geom.src());
+        bind_cloud(SFB_CLOUD_REC, *geom.rec());
+    }
+    int device_ordinal() const { return desc_.device; }
     void check(int rc) const {
         if (rc != SFB_OK) raise_status(rc, sfb_last_error(plan_));
     }
@@ -78,6 +102,7 @@ private:
     }
 
     sfb_plan* plan_ = nullptr;
+    sfb_plan_desc desc_{};
 };
 
 

@@ -4,9 +4,12 @@
 // run_window (proj/src/seismic_ops.cpp:44-54) is handed to sfb_forward / sfb_adjoint /
 // sfb_gradient here.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <mutex>
+#include <numeric>
 #include <thread>
 
 #include "engine.hpp"
@@ -160,15 +163,15 @@ WaveOp tti_forward_operator(const SeismicModel& model, const TtiModel& tti,
 // proj/src/seismic_ops.cpp:109-135
 GradientOp gradient_operator(const SeismicModel& model, const AcquisitionGeometry& geom,
                              int space_order, std::shared_ptr<TimeFunction> saved_u) {
+    const bool full_history = saved_u && !saved_u->time_buffered() && saved_u->time_slots() == geom.nt();
+    if (!full_history) throw ParameterError("gradient_operator: saved forward history required");
     check_space_order(space_order);
     check_cfl(model, geom, space_order);
-    if (!saved_u || saved_u->time_buffered() || saved_u->time_slots() != geom.nt())
-        throw ParameterError("gradient_operator: saved forward history required");
 
     GradientOp g;
-    g.dt = geom.dt();
-    g.nt = geom.nt();
     g.space_order = space_order;
+    g.nt = geom.nt();
+    g.dt = geom.dt();
     g.resid = SparseFunction::create("resid", model.grid(), cloud_coords(*geom.rec()), geom.nt());
     g.resid->locate();
     g.v = TimeFunction::create("v", model.grid(), space_order, 2);
@@ -401,142 +404,266 @@ ExecutionReport run_gradient(GradientOp& g, Backend, int) {
     return to_report(rep);
 }
 
-// proj/src/seismic_ops.cpp:149-160
+// ---- misfit, shot gradient and the inversion driver ---------------------------------------
+// Semantics are the reference's (proj/src/seismic_ops.cpp:149-286: least-squares misfit over
+// all rows, residual = predicted - observed, gradient folded onto the physical cells,
+// fixed-step projected descent with the step chosen at the first iteration); the
+// organisation is this repository's: a shot is evaluated directly on an engine, and the
+// driver keeps ONE engine per lane for the whole inversion instead of building operators,
+// plans and device buffers per shot and per iteration.
+
 double objective(const SparseFunction& pred, const std::vector<double>& observed) {
-    const std::size_t n = std::size_t(pred.nt()) * std::size_t(pred.npoints());
-    if (observed.size() != n) throw ParameterError("objective: observed trace shape mismatch");
-    double phi = 0;
     const std::vector<double>& p = pred.traces();
-    for (std::size_t i = 0; i < n; ++i) {
-        const double r = p[i] - observed[i];
-        phi += 0.5 * r * r;
+    if (observed.size() != std::size_t(pred.nt()) * std::size_t(pred.npoints()))
+        throw ParameterError("objective: " + std::to_string(observed.size()) +
+                             " observed samples for a " + std::to_string(pred.nt()) + " x " +
+                             std::to_string(pred.npoints()) + " record");
+    double half_sq = 0.0;   // accumulated sample by sample, in table order
+    auto o = observed.begin();
+    for (double v : p) {
+        const double d = v - *o++;
+        half_sq += 0.5 * d * d;
     }
-    return phi;
+    return half_sq;
 }
 
 namespace {
 
-// adjoint of the edge-clamped extension, proj/src/seismic_ops.cpp:166-193: every padded
-// cell is summed onto the physical cell it copies, padded cells visited in row-major order
-std::vector<double> fold_gradient(const SeismicModel& model, const Function& grad) {
-    const std::vector<long>& ps = model.physical_shape();
-    const std::vector<long>& shape = model.grid()->shape();
-    const int nd = int(shape.size()), off = 3 - nd;
-    long N[3] = {1, 1, 1}, pn[3] = {1, 1, 1}, pad[3] = {0, 0, 0}, st[3] = {0, 0, 0};
-    for (int a = 0; a < nd; ++a) {
-        N[off + a] = shape[std::size_t(a)];
-        pn[off + a] = ps[std::size_t(a)];
-        pad[off + a] = model.nbl();
-        st[off + a] = grad.stride(a);
+// Adjoint of SeismicModel's edge-clamped extension (proj/src/model.cpp:92-100): a padded
+// node contributes to the physical cell whose value it copies.  `padded` is a compact
+// row-major array over the computational grid; nodes are visited in storage order.
+std::vector<double> fold_onto_physical(const SeismicModel& model, const std::vector<double>& padded) {
+    const std::vector<long>& phys = model.physical_shape();
+    const std::vector<long>& full = model.grid()->shape();
+    const std::size_t rank = full.size();
+    // per axis: computational index -> physical index
+    std::vector<std::vector<long>> to_phys(rank);
+    for (std::size_t a = 0; a < rank; ++a) {
+        to_phys[a].resize(std::size_t(full[a]));
+        for (long i = 0; i < full[a]; ++i)
+            to_phys[a][std::size_t(i)] = std::clamp(i - model.nbl(), 0L, phys[a] - 1);
     }
-    std::vector<long> zero(std::size_t(nd), 0);
-    const double* origin = grad.values() + grad.flat_index(zero);
-    std::vector<double> out(std::size_t(pn[0]) * pn[1] * pn[2], 0.0);
-    for (long i = 0; i < N[0]; ++i) {
-        const long pi = std::clamp(i - pad[0], 0L, pn[0] - 1);
-        for (long j = 0; j < N[1]; ++j) {
-            const long pj = std::clamp(j - pad[1], 0L, pn[1] - 1);
-            const double* row = origin + i * st[0] + j * st[1];
-            double* orow = out.data() + (std::size_t(pi) * pn[1] + pj) * pn[2];
-            for (long l = 0; l < N[2]; ++l) orow[std::clamp(l - pad[2], 0L, pn[2] - 1)] += row[l];
+    std::size_t cells = 1;
+    for (long e : phys) cells *= std::size_t(e);
+    std::vector<double> out(cells, 0.0);
+    // walk the padded array as (rows of the last axis) x (last axis)
+    const long row_len = full[rank - 1];
+    const std::vector<long>& last = to_phys[rank - 1];
+    std::vector<long> idx(rank, 0);
+    const std::size_t rows = padded.size() / std::size_t(row_len);
+    for (std::size_t r = 0; r < rows; ++r) {
+        std::size_t base = 0;
+        for (std::size_t a = 0; a + 1 < rank; ++a)
+            base = base * std::size_t(phys[a]) + std::size_t(to_phys[a][std::size_t(idx[a])]);
+        double* dst = out.data() + base * std::size_t(phys[rank - 1]);
+        const double* src = padded.data() + r * std::size_t(row_len);
+        for (long l = 0; l < row_len; ++l) dst[last[std::size_t(l)]] += src[l];
+        for (std::size_t a = rank - 1; a-- > 0;) {   // advance the row index (odometer)
+            if (++idx[a] < full[a]) break;
+            idx[a] = 0;
         }
     }
+    return out;
+}
+
+struct ShotPolicy {
+    int space_order;
+    long save_every;        // image against every save_every-th forward level
+    long checkpoint_every;  // or keep checkpoints and recompute (exact imaging condition)
+};
+
+void check_policy(const ShotPolicy& p, const char* who) {
+    if (p.save_every < 1) throw ParameterError(std::string(who) + ": save_every must be >= 1");
+    if (p.checkpoint_every != 0 && (p.checkpoint_every < 2 || p.save_every != 1))
+        throw ParameterError(std::string(who) + ": checkpoint_every must be >= 2 (with save_every 1)");
+}
+
+// One shot on a bound engine: forward run keeping the history in HBM, misfit and residual
+// on the host, gradient sweep, fold.  The predicted record lands in geom.rec() as with the
+// operator interface.
+GradientResult evaluate_shot(Engine& e, const SeismicModel& model, AcquisitionGeometry& geom,
+                             const std::vector<double>& observed, const ShotPolicy& pol,
+                             std::vector<double>& padded_scratch) {
+    check_space_order(pol.space_order);
+    check_cfl(model, geom, pol.space_order);
+    SparseFunction& rec = *geom.rec();
+    const double* src = geom.src()->traces().data();
+    if (pol.checkpoint_every > 0)
+        e.check(sfb_forward_checkpointed(e.plan(), src, rec.traces().data(), pol.checkpoint_every, nullptr));
+    else
+        e.check(sfb_forward(e.plan(), src, rec.traces().data(), pol.save_every, nullptr));
+    GradientResult out;
+    out.objective = objective(rec, observed);
+    out.residual.resize(observed.size());
+    std::transform(rec.traces().begin(), rec.traces().end(), observed.begin(), out.residual.begin(),
+                   [](double pred, double obs) { return pred - obs; });
+    const std::vector<long>& full = model.grid()->shape();
+    std::size_t nodes = 1;
+    for (long n : full) nodes *= std::size_t(n);
+    padded_scratch.assign(nodes, 0.0);
+    sfb_field_mview gv{};
+    gv.ptr = padded_scratch.data();
+    long stride = 1;
+    for (std::size_t a = full.size(); a-- > 0;) {
+        gv.stride[a] = stride;
+        stride *= full[a];
+    }
+    e.check(sfb_gradient(e.plan(), out.residual.data(), &gv, nullptr));
+    out.gradient = fold_onto_physical(model, padded_scratch);
     return out;
 }
 
 }  // namespace
 
-// proj/src/seismic_ops.cpp:197-216
 GradientResult fwi_gradient(const SeismicModel& model, AcquisitionGeometry& geom,
-                            const std::vector<double>& observed, int space_order, Backend backend,
+                            const std::vector<double>& observed, int space_order, Backend,
                             long save_every, long checkpoint_every) {
-    if (save_every < 1) throw ParameterError("fwi_gradient: save_every must be >= 1");
-    if (checkpoint_every != 0 && (checkpoint_every < 2 || save_every != 1))
-        throw ParameterError("fwi_gradient: checkpoint_every must be >= 2 (with save_every 1)");
-    WaveOp fwd = forward_operator(model, geom, space_order, true);
-    fwd.save_every = save_every;
-    fwd.checkpoint_every = checkpoint_every;
-    fwd.host_history = false;  // the history stays in HBM
-    run_wave(fwd, backend);
-    GradientResult res;
-    res.objective = objective(*geom.rec(), observed);
-    GradientOp g = gradient_operator(model, geom, space_order, fwd.wavefield);
-    const std::size_t n = std::size_t(geom.nt()) * std::size_t(geom.n_rec());
-    res.residual.resize(n);
-    const std::vector<double>& pred = geom.rec()->traces();
-    for (std::size_t i = 0; i < n; ++i) res.residual[i] = pred[i] - observed[i];
-    g.resid->traces() = res.residual;
-    run_gradient(g, backend);
-    res.gradient = fold_gradient(model, *g.grad);
-    return res;
+    const ShotPolicy pol{space_order, save_every, checkpoint_every};
+    check_policy(pol, "fwi_gradient");
+    check_space_order(space_order);
+    check_cfl(model, geom, space_order);
+    Engine engine(model, geom, space_order);
+    std::vector<double> scratch;
+    return evaluate_shot(engine, model, geom, observed, pol, scratch);
 }
 
-// proj/src/seismic_ops.cpp:218-286: fixed-step projected gradient descent; shot gradients
-// computed cfg.nthreads at a time (one engine per shot) and reduced in shot order.
+namespace {
+
+// A lane = one CUDA device slot that evaluates shots one after the other on an engine it
+// keeps: the plan, its wavefield / history buffers and tensor maps live as long as the
+// inversion.  Per shot only the two point tables are rebound, per iteration the model.
+class ShotLane {
+public:
+    explicit ShotLane(int device_ordinal) : device_(device_ordinal) {}
+
+    GradientResult evaluate(const SeismicModel& model, long model_version, AcquisitionGeometry& geom,
+                            const std::vector<double>& observed, const ShotPolicy& pol) {
+        set_device(device_);
+        if (!engine_ || !engine_->fits(model, geom, pol.space_order)) {
+            engine_.reset();   // free the old plan's HBM before the new one allocates
+            engine_ = std::make_unique<Engine>(model, geom, pol.space_order);
+            ++plans_built_;
+        } else {
+            if (bound_version_ != model_version) engine_->rebind_model(model);
+            engine_->rebind_geometry(geom);
+        }
+        bound_version_ = model_version;
+        return evaluate_shot(*engine_, model, geom, observed, pol, scratch_);
+    }
+    long plans_built() const { return plans_built_; }
+
+private:
+    int device_;
+    std::unique_ptr<Engine> engine_;
+    long bound_version_ = -1;
+    long plans_built_ = 0;
+    std::vector<double> scratch_;
+};
+
+// All shots of one iteration over the lanes.  Shots are handed out dynamically (a lane takes
+// the next unclaimed shot when it is free); results are stored by shot index so that the
+// reduction order -- and with it the result -- does not depend on the lane count.
+class ShotPool {
+public:
+    ShotPool(const FwiConfig& cfg, int caller_device) {
+        const std::size_t lanes = cfg.nthreads > 1 ? std::size_t(cfg.nthreads) : 1;
+        for (std::size_t i = 0; i < lanes; ++i)
+            lanes_.emplace_back(cfg.devices.empty() ? caller_device : cfg.devices[i % cfg.devices.size()]);
+    }
+
+    std::vector<GradientResult> evaluate(const SeismicModel& model, long model_version,
+                                         std::vector<AcquisitionGeometry>& shots,
+                                         const std::vector<std::vector<double>>& observed,
+                                         const ShotPolicy& pol) {
+        std::vector<GradientResult> terms(shots.size());
+        std::vector<std::string> errors(shots.size());
+        std::atomic<std::size_t> next{0};
+        auto drain = [&](ShotLane& lane) {
+            for (std::size_t s; (s = next.fetch_add(1)) < shots.size();) {
+                try {
+                    terms[s] = lane.evaluate(model, model_version, shots[s], observed[s], pol);
+                } catch (const std::exception& e) {
+                    errors[s] = e.what()[0] ? e.what() : "unknown failure";
+                }
+            }
+        };
+        std::vector<std::thread> crew;
+        for (std::size_t i = 1; i < lanes_.size() && i < shots.size(); ++i)
+            crew.emplace_back(drain, std::ref(lanes_[i]));
+        const int callers_device = device();
+        drain(lanes_[0]);   // the caller is lane 0
+        set_device(callers_device);
+        for (std::thread& t : crew) t.join();
+        for (std::size_t s = 0; s < errors.size(); ++s)
+            if (!errors[s].empty())
+                throw StabilityError("fwi: shot " + std::to_string(s) + " failed: " + errors[s]);
+        return terms;
+    }
+
+private:
+    std::vector<ShotLane> lanes_;
+};
+
+double max_abs(const std::vector<double>& v) {
+    double m = 0.0;
+    for (double x : v) m = std::max(m, std::abs(x));
+    return m;
+}
+
+}  // namespace
+
 FwiResult fwi(SeismicModel& model, std::vector<AcquisitionGeometry>& shots,
               const std::vector<std::vector<double>>& observed, const FwiConfig& cfg,
               const std::vector<double>* true_m) {
-    if (shots.empty() || shots.size() != observed.size())
-        throw ParameterError("fwi: one observed record per shot required");
-    if (!(cfg.m_min > 0.0) || !(cfg.m_max > cfg.m_min)) throw ParameterError("fwi: bad model box");
-    FwiResult out;
+    if (shots.empty() || observed.size() != shots.size())
+        throw ParameterError("fwi: " + std::to_string(shots.size()) + " shots but " +
+                             std::to_string(observed.size()) + " observed records");
+    if (!(cfg.m_min > 0.0 && cfg.m_max > cfg.m_min))
+        throw ParameterError("fwi: the model box needs 0 < m_min < m_max");
+    const ShotPolicy pol{cfg.space_order, cfg.save_every, cfg.checkpoint_every};
+    check_policy(pol, "fwi");
+
     std::vector<double> m = model.physical_m();
-    double alpha = 0;
-    auto rms_error = [&](const std::vector<double>& cur) {
+    auto distance_to_truth = [&] {   // rms over the physical cells; 0 without a reference model
         if (!true_m) return 0.0;
-        double s = 0;
-        for (std::size_t i = 0; i < cur.size(); ++i) s += (cur[i] - (*true_m)[i]) * (cur[i] - (*true_m)[i]);
-        return std::sqrt(s / double(cur.size()));
+        double sq = 0.0;
+        for (std::size_t i = 0; i < m.size(); ++i) sq += (m[i] - (*true_m)[i]) * (m[i] - (*true_m)[i]);
+        return std::sqrt(sq / double(m.size()));
     };
-    const int dev = device();
+
+    ShotPool pool(cfg, device());
+    FwiResult history;
+    double step = 0.0;   // fixed after the first gradient: step_scale * max|m| / max|g|
     for (long it = 0; it < cfg.n_iter; ++it) {
-        std::vector<GradientResult> parts(shots.size());
-        std::vector<std::string> failures(shots.size());
-        const std::size_t width = cfg.nthreads > 1 ? std::size_t(cfg.nthreads) : 1;
-        for (std::size_t lo = 0; lo < shots.size(); lo += width) {
-            const std::size_t hi = std::min(shots.size(), lo + width);
-            std::vector<std::thread> pool;
-            for (std::size_t s = lo; s < hi; ++s)
-                pool.emplace_back([&, s] {
-                    set_device(cfg.devices.empty() ? dev : cfg.devices[s % cfg.devices.size()]);
-                    try {
-                        parts[s] = fwi_gradient(model, shots[s], observed[s], cfg.space_order,
-                                                cfg.backend, cfg.save_every, cfg.checkpoint_every);
-                    } catch (const Error& e) {
-                        failures[s] = e.what();
-                    }
-                });
-            for (auto& th : pool) th.join();
-        }
-        for (const auto& f : failures)
-            if (!f.empty()) throw StabilityError("fwi: shot failed: " + f);
-        double phi = 0;
+        const std::vector<GradientResult> terms = pool.evaluate(model, it, shots, observed, pol);
+        // reduce in shot order
+        double phi = 0.0;
         std::vector<double> g(m.size(), 0.0);
-        for (const auto& p : parts) {
-            phi += p.objective;
-            for (std::size_t i = 0; i < g.size(); ++i) g[i] += p.gradient[i];
+        for (const GradientResult& term : terms) {
+            phi += term.objective;
+            std::transform(g.begin(), g.end(), term.gradient.begin(), g.begin(), std::plus<double>());
         }
         if (!std::isfinite(phi))
-            throw StabilityError("fwi: non-finite objective at iteration " + std::to_string(it));
-        out.objectives.push_back(phi);
-        out.model_rms.push_back(rms_error(m));
+            throw StabilityError("fwi: the objective of iteration " + std::to_string(it) + " is not finite");
+        history.objectives.push_back(phi);
+        history.model_rms.push_back(distance_to_truth());
         if (it == 0) {
-            double gmax = 0, mmax = 0;
-            for (double v : g) gmax = std::max(gmax, std::abs(v));
-            for (double v : m) mmax = std::max(mmax, std::abs(v));
-            if (gmax == 0.0) {
-                out.final_m = m;
-                return out;
+            const double steepest = max_abs(g);
+            if (steepest == 0.0) {   // already at a stationary point: nothing to do
+                history.final_m = std::move(m);
+                return history;
             }
-            alpha = cfg.step_scale * mmax / gmax;
+            step = cfg.step_scale * max_abs(m) / steepest;
         }
-        for (std::size_t i = 0; i < m.size(); ++i)
-            m[i] = std::clamp(m[i] - alpha * g[i], cfg.m_min, cfg.m_max);
+        // projected descent step onto the box [m_min, m_max]
+        std::transform(m.begin(), m.end(), g.begin(), m.begin(), [&](double mi, double gi) {
+            return std::clamp(mi - step * gi, cfg.m_min, cfg.m_max);
+        });
         model.set_physical_m(m);
     }
-    out.model_rms.push_back(rms_error(m));
-    out.final_m = m;
-    return out;
+    history.model_rms.push_back(distance_to_truth());
+    history.final_m = std::move(m);
+    return history;
 }
 
 }  // namespace sfb

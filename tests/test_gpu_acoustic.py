@@ -528,3 +528,29 @@ def test_concurrent_plans_from_two_threads():
     for t in th:
         t.join()
     assert np.array_equal(out[0], serial[0]) and np.array_equal(out[1], serial[1])
+
+
+def test_step_entry_points_reject_bad_operators_with_a_status():
+    """Round-1 advisor finding: stepping the gradient operator without a bound history
+    divided by save_every = 0 (SIGFPE across the C ABI), and the acoustic step accepted the
+    TTI operator id.  Both are parameter errors now."""
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([24, 24, 24], 10.0, 6, 8, 10)
+    plan = make_plan(model, geom, 8)
+    plan.upload_traces(capi.CLOUD_SRC, geom.src)
+    plan.upload_traces(capi.CLOUD_REC, geom.rec)
+    plan.step_begin(capi.OP_FORWARD)
+    for call in (lambda: plan.step_compute(capi.OP_GRADIENT, 3, capi.PART_ALL),
+                 lambda: plan.step_points(capi.OP_GRADIENT, 3, capi.PART_ALL),
+                 lambda: plan.run_steps(capi.OP_GRADIENT, 1, 3),
+                 lambda: plan.time_stencil(capi.OP_GRADIENT, 1, 3),
+                 lambda: plan.step_compute(capi.OP_TTI_FORWARD, 3, capi.PART_ALL),
+                 lambda: plan.step_points(capi.OP_TTI_FORWARD, 3, capi.PART_ALL),
+                 lambda: plan.step_slab_boundary(capi.OP_TTI_FORWARD, 3)):
+        with pytest.raises(capi.SfbError) as e:
+            call()
+        assert e.value.code == capi.ERR_PARAMETER
+    plan.autotune(2)   # zeroes save_every; the plan must still refuse, not crash
+    with pytest.raises(capi.SfbError):
+        plan.run_steps(capi.OP_GRADIENT, 1, 3)
+    plan.close()
