@@ -1,26 +1,34 @@
 #!/usr/bin/env python
-"""bench.py -- headline benchmark of the wave-propagator path.
+"""bench.py -- benchmark of the wave-propagator path (BASELINE.json metric: GPts/s per operator
+at 1/2/4/8 B200 and the fraction of the HBM roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2|3|4|5] [--op forward|adjoint|gradient|tti] [--scaling strong|weak]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
 
-Metric (BASELINE.json): GPts/s = padded grid points x time steps / seconds of the stepping
-loop, acoustic forward operator.  A "step" is one time step of the propagator (dense
-update + source scatter + receiver gather).  Workload at every N: BASELINE.json configs[1]
-(512^3 physical + 40-node layer = 592^3, space order 8, 512x512 receivers, one off-node
-Ricker source, seeded smoothed-noise velocity); at N > 1 the same grid is cut into N slabs
-along the slowest axis (strong scaling, as configs[1] asks) and ghost planes travel over
-NCCL send/recv each step.
+GPts/s = computed (padded) grid nodes x time steps / seconds of the stepping loop.  A "step" is
+one time step of the operator: dense update + point scatter + point gather (+ imaging for the
+gradient sweep; two launches for the TTI pair).
 
-One JSON line on stdout (rank 0).  `value` is timed with CUDA events on the plan's own
-stream with all inputs resident in HBM; `e2e` is the same metric through the C-ABI call
-sfb_forward with host buffers (source traces H2D, receiver traces D2H inside the timed
-region); `roofline` is the dense-update kernel alone; `cpu_baseline` is the f64 oracle on
-the host cores.  `--impl reference` times the CPU implementation (oracle/_ref when the
-reference's own sources were compiled here, else the oracle port).  At N = 1 the line also
-carries `other_operators`: device-timed GPts/s of the adjoint, the gradient sweep and the TTI
-forward operator on the same grid (extras, not the contract metric; --no-other-ops skips them),
-and `value_runs`: three timed windows of exactly K steps each, of which `value` is the median.
+Workloads (--config is BASELINE.json's 1-based numbering; default 2 = configs[1], the
+configuration the metric is quoted on):
+  2  acoustic forward, 592^3 computed nodes, order 8, 1 source, 512 x 512 receivers
+  3  acoustic FWI gradient sweep on the two-layer medium, 592^3, order 8, every 4th level saved
+  4  TTI forward, 592^3, order 12, seeded smooth Thomsen fields (delta clipped to epsilon:
+     the builder's pseudo-acoustic system is ill-posed otherwise)
+  5  large-domain acoustic forward, order 16, 8 off-node sources, 1024 x 1024 receivers; weak
+     scaling (default): 1024 x 1024 x (128 N) physical nodes, slab axis first
+At N > 1 the grid is cut into N slabs along the slowest axis; ghost planes are pushed into the
+neighbours' memory by the boundary kernels (CUDA IPC) with NCCL send/recv as the fallback
+(SFB_HALO=nccl forces it); the TTI pair exchanges over NCCL.
+
+One JSON line on stdout (rank 0).  `value`: device-timed (CUDA events on the plan's stream,
+max over ranks), inputs resident in HBM.  `e2e`: the same metric through the C-ABI with HOST
+buffers, host<->device copies inside the timed region.  `roofline`: the dominant kernel alone
+(N = 1) against MEASURED_PEAKS.json.  `cpu_baseline` / `--impl reference`: the reference's own
+CPU engine (oracle/_ref) or the oracle port on the host cores, bounded sample.  The default
+N = 1 line also carries `operators`: adjoint, gradient sweep and TTI forward on the same
+grid, each with its own roofline and e2e (--no-other-ops skips them).
 """
 from __future__ import annotations
 
@@ -38,12 +46,42 @@ if ROOT not in sys.path:
 
 import numpy as np  # noqa: E402
 
-BYTES_PER_POINT = 20.0   # u[t], u[t-1], u[t+1], m, damp, one touch each
-N_PHYS, ORDER, NBL, H = 512, 8, 40, 12.5
+NBL, H = 40, 12.5
+CONFIGS = {
+    2: dict(key="configs[1]", op="forward", order=8, n=512, scaling="strong"),
+    3: dict(key="configs[2]", op="gradient", order=8, n=512, scaling="strong"),
+    4: dict(key="configs[3]", op="tti", order=12, n=512, scaling="strong"),
+    5: dict(key="configs[4]", op="forward", order=16, n=1024, scaling="weak", per_rank=128),
+}
+# contract bytes per node-step and what the kernels really have to move
+CONTRACT_BYTES = {"forward": 20.0, "adjoint": 20.0, "gradient": 28.0, "tti": 48.0}
+METRIC = {"forward": "acoustic_forward_gpts_per_s", "adjoint": "acoustic_adjoint_gpts_per_s",
+          "gradient": "acoustic_gradient_gpts_per_s", "tti": "tti_forward_gpts_per_s"}
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def actual_bytes(op, sep, images_every=1):
+    """Bytes a node-step must move with this build's data layout: the separable-damping kernel
+    rebuilds damp from three 1-D profiles (16 B instead of 20); the gradient sweep adds the
+    grad read-modify-write and the snapshot read on imaging steps only; the TTI pair streams
+    a, b, c for theta, phi."""
+    base = 16.0 if sep else 20.0
+    if op == "gradient":
+        return base + 12.0 / max(images_every, 1)
+    if op == "tti":
+        return 48.0 if sep else 52.0
+    return base
 
 
 # ---- clocks ---------------------------------------------------------------------------
@@ -95,110 +133,325 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---- workload -------------------------------------------------------------------------
+# ---- workloads ------------------------------------------------------------------------
 
-def build_workload(nsteps_total):
-    """configs[1] through the C++ host layer (SeismicModel / AcquisitionGeometry)."""
-    from paper_1808_01995_b200 import _sfb_host as Hst
-    from paper_1808_01995_b200 import synthetic as syn
-    cfg = syn.config(2, N_PHYS)
-    t0 = time.time()
-    vel = cfg["velocity"]()
-    log(f"[bench] velocity {vel.shape} in {time.time() - t0:.1f}s "
-        f"[{vel.min():.3f}, {vel.max():.3f}]")
-    t0 = time.time()
-    model = Hst.SeismicModel(cfg["shape"], [H] * 3, [0.0] * 3, vel, NBL, ORDER)
-    del vel
-    dt, tn = syn.time_axis(model.critical_dt(ORDER), nsteps_total)
-    geom = Hst.AcquisitionGeometry(model, np.asarray(cfg["src"]).ravel(), cfg["rec"].ravel(),
-                                   0.0, tn, dt, cfg["f0"])
-    assert geom.nt == nsteps_total + 2, (geom.nt, nsteps_total)
-    log(f"[bench] model + geometry in {time.time() - t0:.1f}s: N={model.grid.shape} dt={dt:.6f} "
-        f"nt={geom.nt} n_rec={geom.n_rec}")
-    return cfg, model, geom
+def grid_of(config, world, scaling):
+    """computed (padded) extents and physical extents of a configuration at `world` GPUs"""
+    c = CONFIGS[config]
+    if config == 5 and scaling == "weak":
+        phys = [c["per_rank"] * world, c["n"], c["n"]]
+    else:
+        phys = [c["n"]] * 3
+    return [p + 2 * NBL for p in phys], phys
 
 
-def make_plan(model, geom, device=0, slab=None):
+def workload_config(config, op, world, scaling, extra=None):
+    c = CONFIGS[config]
+    N, phys = grid_of(config, world, scaling)
+    what = {
+        2: "acoustic forward, 1 off-node 15 Hz Ricker source, 512x512 receivers at 25 m, seeded "
+           "smoothed-noise velocity (sigma 8) in [1.5,4.5] km/s",
+        3: "acoustic FWI gradient sweep (forward history every 4th level in HBM, residual traces at "
+           "512x512 receivers, imaging fused into the sweep), two-layer medium 1.5/2.5 km/s",
+        4: "TTI forward (rotated first-derivative pairs, coupled p/r), seeded smooth fields: v in "
+           "[1.5,4.5], epsilon in [0,0.3], delta in [0,0.2] clipped to delta <= epsilon (deviation "
+           "from BASELINE: the builder's system is ill-posed for epsilon < delta), theta, phi in "
+           "[0,pi/4]; 1 source, 512x512 receivers",
+        5: "large-domain acoustic forward, 8 seeded off-node sources, 1024x1024 receivers at 25 m, "
+           "seeded smoothed-noise velocity in [1.5,4.5] km/s generated per slab",
+    }[config]
+    if op != c["op"]:
+        what = f"{op} operator on the grid and medium of: " + what
+    cfg = {"workload": f"BASELINE.json {c['key']}: {what}; {phys[0]}x{phys[1]}x{phys[2]} physical + "
+                       f"{NBL}-node absorbing layer = {N[0]}x{N[1]}x{N[2]} computed nodes, space order "
+                       f"{c['order']}, fp32",
+           "grid": N, "space_order": c["order"], "operator": op,
+           "decomposition": f"{world} slab(s) along the slowest axis",
+           "l2": f"every field ({np.prod(N) * 4 / world / 1e9:.2f} GB per GPU) is larger than the "
+                 "126 MB L2: no flush needed"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+class Workload:
+    """One configuration's host-side inputs for one rank."""
+
+    def __init__(self, config, op, nsteps, rank=0, world=1, scaling="strong"):
+        from paper_1808_01995_b200 import capi, slabs
+        from paper_1808_01995_b200 import synthetic as syn
+        self.config, self.op, self.rank, self.world = config, op, rank, world
+        c = CONFIGS[config]
+        self.order = c["order"]
+        self.N, self.phys = grid_of(config, world, scaling)
+        self.bounds = slabs.split_slabs(self.N[0], world, self.order // 2)
+        self.slab = self.bounds[rank] if world > 1 else None
+        self.tti = None
+        t0 = time.time()
+        if config == 5:
+            self._build_slab_local(nsteps, syn, capi)
+        else:
+            self._build_global(nsteps, syn)
+        log(f"[bench] rank {rank}: workload {config} built in {time.time() - t0:.1f}s: N={self.N} "
+            f"dt={self.dt:.6f} nt={self.nt} n_src={self.src_base.shape[0]} n_rec={self.rec_base.shape[0]}")
+
+    def _build_global(self, nsteps, syn):
+        from paper_1808_01995_b200 import _sfb_host as Hst
+        cfg = syn.config(self.config, CONFIGS[self.config]["n"])
+        self.vel_phys = cfg["velocity"]()
+        model = Hst.SeismicModel(cfg["shape"], [H] * 3, [0.0] * 3, self.vel_phys, NBL, self.order)
+        crit = model.critical_dt(self.order)
+        if self.op == "tti":
+            eps, delta, theta, phi = cfg["tti"]() if "tti" in cfg else syn.tti_fields(cfg["shape"])
+            self.tti = [syn.extend(f, NBL) for f in (eps, delta, theta, phi)]
+            crit = 0.9 * crit / np.sqrt(1.0 + 2.0 * float(eps.max()))
+        dt, tn = syn.time_axis(crit, nsteps)
+        # the geometry checks dt against the acoustic limit only; the TTI limit is smaller
+        geom = Hst.AcquisitionGeometry(model, np.asarray(cfg["src"]).ravel(), cfg["rec"].ravel(),
+                                       0.0, tn, dt, cfg["f0"])
+        assert geom.nt == nsteps + 2, (geom.nt, nsteps)
+        self.model, self.geom = model, geom
+        self.dt, self.nt, self.v_max = dt, geom.nt, model.v_max
+        self.src_base = np.array(geom.src.base_table).reshape(-1, 3)
+        self.src_w = np.array(geom.src.weight_table).reshape(-1, 8)
+        self.rec_base = np.array(geom.rec.base_table).reshape(-1, 3)
+        self.rec_w = np.array(geom.rec.weight_table).reshape(-1, 8)
+        self.src = np.ascontiguousarray(geom.src.traces)
+        self.m = lambda: model.m.array()
+        self.damp = lambda: model.damp.array()
+
+    def _build_slab_local(self, nsteps, syn, capi):
+        """configs[4]: no rank holds a global field (1104^3 in f64 is 10.8 GB per field)."""
+        from paper_1808_01995_b200 import _sfb_host as Hst
+        self.v_max = 4.5
+        self.dt = capi.critical_dt([H] * 3, self.v_max, self.order)
+        self.nt = nsteps + 2
+        lo, hi = self.slab if self.slab else (0, self.N[0])
+        self._m, self._damp = syn.slab_model(
+            self.phys, NBL, [H] * 3, lo, hi,
+            lambda a, b: syn.smooth_slab(self.phys, a, b, syn.SEED + 6, 8.0, 1.5, 4.5), self.v_max)
+        ext = [H * (p - 1) for p in self.phys]
+        src = np.random.default_rng(syn.SEED + 7).uniform([0, 0, 0], ext, size=(8, 3))
+        n = CONFIGS[5]["n"]
+        ii, jj = np.meshgrid(np.linspace(0.0, ext[0], n), np.arange(n) * H, indexing="ij")
+        rec = np.stack([ii.ravel(), jj.ravel(), np.full(ii.size, 25.0)], axis=1)
+        org = [-NBL * H] * 3
+        self.src_base, self.src_w = capi.locate(self.N, [H] * 3, org, src)
+        self.rec_base, self.rec_w = capi.locate(self.N, [H] * 3, org, rec)
+        wavelet = np.asarray(Hst.ricker(0.015, 0.0, self.dt, self.nt))
+        self.src = np.repeat(wavelet[:, None], 8, axis=1).copy()
+        self.m = self.damp = None
+
+    def make_plan(self, device, dense_damping=False):
+        from paper_1808_01995_b200 import capi
+        plan = capi.Plan(self.N, [H] * 3, self.order, self.dt, self.nt, device, self.slab,
+                         dense_damping=dense_damping)
+        if self.m is None:
+            plan.set_model_slab(self._m, self._damp, self.v_max)
+        else:
+            plan.set_model(self.m(), self.damp(), self.v_max)
+        plan.set_points(capi.CLOUD_SRC, self.src_base, self.src_w)
+        plan.set_points(capi.CLOUD_REC, self.rec_base, self.rec_w)
+        if self.tti is not None:
+            plan.set_model_tti(*self.tti)
+        return plan
+
+    def residual_traces(self):
+        """configs[2]: N(0,1) noise per receiver convolved in time with the 15 Hz Ricker"""
+        from paper_1808_01995_b200 import _sfb_host as Hst
+        from paper_1808_01995_b200 import synthetic as syn
+        n_rec = self.rec_base.shape[0]
+        spec = np.fft.rfft(np.asarray(Hst.ricker(0.015, 0.0, self.dt, self.nt)))[:, None]
+        rng = np.random.default_rng(syn.SEED + 10)
+        out = np.empty((self.nt, n_rec))
+        for lo in range(0, n_rec, 65536):
+            xi = rng.standard_normal((self.nt, min(65536, n_rec - lo)))
+            out[:, lo:lo + xi.shape[1]] = np.fft.irfft(np.fft.rfft(xi, axis=0) * spec, n=self.nt, axis=0)
+        out[[0, self.nt - 1]] = 0.0
+        return out
+
+
+# ---- one operator on one GPU ------------------------------------------------------------
+
+def op_ids(op):
     from paper_1808_01995_b200 import capi
-    plan = capi.Plan(model.grid.shape, model.grid.spacing, ORDER, geom.dt, geom.nt, device, slab)
-    plan.set_model(model.m.array(), model.damp.array(), model.v_max)
-    nd = 3
-    plan.set_points(capi.CLOUD_SRC, np.array(geom.src.base_table).reshape(-1, nd),
-                    np.array(geom.src.weight_table).reshape(-1, 8))
-    plan.set_points(capi.CLOUD_REC, np.array(geom.rec.base_table).reshape(-1, nd),
-                    np.array(geom.rec.weight_table).reshape(-1, 8))
-    return plan
+    return {"forward": capi.OP_FORWARD, "adjoint": capi.OP_ADJOINT, "gradient": capi.OP_GRADIENT,
+            "tti": capi.OP_TTI_FORWARD}[op]
 
 
-def other_operators(plan, geom, rec, model, device):
-    """Device-timed throughput of the other operators of the path on the same grid (not part
-    of the contract's metric; reported so that every operator has a number from this box):
-    adjoint and FWI-gradient sweep at order 8 on the bench plan, TTI forward at order 12
-    (config 4's size) on its own plan with cheap analytic Thomsen fields."""
-    from paper_1808_01995_b200 import capi
-    out = {"unit": "GPts/s", "grid": list(model.grid.shape)}
+def windows(plan, op, nt, W, K, runs=3, stencil_only=False):
+    """`runs` windows of exactly K steps, each after W untimed warm-up steps from a zeroed
+    state; device-timed by the engine (CUDA events on the plan's stream).  Sorted by time."""
+    import torch
+    oid = op_ids(op)
+    fn = plan.time_stencil if stencil_only else plan.run_steps
+    out = []
+    for _ in range(runs):
+        plan.step_begin(oid)
+        if op in ("adjoint", "gradient"):      # descending: window [a, b) runs t = b-1 .. a
+            top = nt - 1
+            plan.run_steps(oid, top - W, top)
+            out.append(fn(oid, top - W - K, top - W))
+        else:
+            plan.run_steps(oid, 1, 1 + W)
+            out.append(fn(oid, 1 + W, 1 + W + K))
+        torch.cuda.synchronize()
+    return sorted(out, key=lambda r: r.seconds)
+
+
+def roofline_of(op, pts, kernel_s, sep, images_every, tile, K_half, clocks, traffic=None):
+    """`achieved` uses the bytes this build's kernels must move per node-step (see
+    actual_bytes); the SURVEY.md 8(d) contract figure is carried beside it."""
+    peak, kind = peaks()
+    b = actual_bytes(op, sep, images_every)
+    cb = CONTRACT_BYTES[op]
+    r = {"bound": "hbm", "achieved": b * pts / kernel_s / 1e9, "peak": peak, "unit": "GB/s",
+         "frac": b * pts / kernel_s / 1e9 / peak, "peak_kind": kind,
+         "basis_bytes_per_point": b, "algorithmic_bytes_per_launch": b * pts,
+         "contract_bytes_per_point": cb, "achieved_contract": cb * pts / kernel_s / 1e9,
+         "frac_contract": cb * pts / kernel_s / 1e9 / peak,
+         "basis": ("bytes the kernel must move with this build's layout (separable damping "
+                   "rebuilt from 1-D profiles: 16 B; the SURVEY.md 8(d) contract figure of "
+                   f"{cb:.0f} B is in *_contract)"),
+         "kernel_ms": kernel_s * 1e3, "tile": tile}
+    if op == "tti":
+        r["kernel"] = "tti_rot_kernel + tti_div_update_kernel (two launches per step)"
+        flops = 57.0 * K_half + 29.0          # reference accounting, engine_tti.cu
+        sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        r["fp32"] = {"flops_per_point": flops, "achieved_tflops": flops * pts / kernel_s / 1e12,
+                     "peak_tflops": fp32_peak, "frac": flops * pts / kernel_s / 1e12 / fp32_peak}
+    else:
+        r["kernel"] = "acoustic_step_dual_kernel" if tile.get("stages", 0) < 0 else "acoustic_step_kernel"
+    if op == "gradient":
+        r["images_every"] = images_every
+    tr = traffic if traffic is not None else static_traffic(op, sep)
+    r.update(tr)
+    return r
+
+
+def static_traffic(op, sep):
+    """DRAM bytes per launch from the committed ncu --set full capture of the same kernel
+    (profiles/r02_traffic.json, written by tools/ncu_summary.py); cannot be measured inside
+    an unprofiled run."""
+    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    key = {"forward": "acoustic_sep" if sep else "acoustic_dense", "adjoint": "acoustic_sep" if sep else "acoustic_dense",
+           "gradient": "gradient", "tti": "tti"}[op]
     try:
-        plan.upload_traces(capi.CLOUD_REC, rec)
-        out["adjoint_so8"] = plan.run_resident(capi.OP_ADJOINT).gpts_per_s
-        se = max(4, -(-geom.nt // 100))
-        f = plan.run_resident(capi.OP_FORWARD, se)
-        g = plan.run_resident(capi.OP_GRADIENT)
-        out["forward_saving_so8"] = f.gpts_per_s
-        out["gradient_sweep_so8"] = g.gpts_per_s
-        out["gradient_images_every"] = se
-        out["gradient_roofline_28B"] = peaks()[0] / 28.0
-    except Exception as e:  # never lose the contract line over an extra
-        out["error_acoustic"] = repr(e)
-    try:
-        N = list(model.grid.shape)
-        steps = 20
-        lin = [np.linspace(0.0, 1.0, n) for n in N]
-        ones = np.ones(N)
-        eps = 0.3 * lin[0][:, None, None] * ones
-        delta = 0.2 * lin[1][None, :, None] * lin[0][:, None, None] * ones
-        theta = (np.pi / 4) * lin[2][None, None, :] * ones
-        phi = (np.pi / 4) * lin[1][None, :, None] * ones
-        dt = 0.9 * capi.critical_dt(list(model.grid.spacing), model.v_max, 12) / np.sqrt(1.6)
-        tp = capi.Plan(N, model.grid.spacing, 12, dt, steps + 2, device)
-        tp.set_model(model.m.array(), model.damp.array(), model.v_max)
-        tp.set_model_tti(eps, delta, theta, phi)
-        del eps, delta, theta, phi, ones
-        tp.set_points(capi.CLOUD_SRC, np.array(geom.src.base_table).reshape(-1, 3),
-                      np.array(geom.src.weight_table).reshape(-1, 8))
-        tp.set_points(capi.CLOUD_REC, np.array(geom.rec.base_table).reshape(-1, 3),
-                      np.array(geom.rec.weight_table).reshape(-1, 8))
-        tp.upload_traces(capi.CLOUD_SRC, np.sin(np.arange(steps + 2) * 0.1).reshape(-1, 1))
-        tp.run_resident(capi.OP_TTI_FORWARD)
-        r = tp.run_resident(capi.OP_TTI_FORWARD)
-        out["tti_forward_so12"] = r.gpts_per_s
-        out["tti_roofline_48B"] = peaks()[0] / 48.0
-        out["tti_tflops"] = r.gflops / 1e3
-        tp.close()
-    except Exception as e:
-        out["error_tti"] = repr(e)
-    return out
-
-
-def peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+        with open(path) as f:
+            d = json.load(f)
+        return {"traffic": d[key]["dram_bytes_per_launch"],
+                "traffic_source": f"static: {d[key]['source']} (ncu --set full, dram__bytes_read.sum + "
+                                  "dram__bytes_write.sum per launch)"}
     except Exception:
-        return 6650.0, "fallback"
+        return {"traffic": None, "traffic_source": "no ncu capture committed for this kernel"}
 
 
-# ---- CPU arm ----------------------------------------------------------------------------
+def measure_op(wl, op, K, W, device, want_e2e=True):
+    """value / roofline / e2e of one operator on one GPU; returns a dict (no `metric` keys)."""
+    import torch
+    from paper_1808_01995_b200 import capi
+    pts = float(np.prod(wl.N))
+    plan = wl.make_plan(device)
+    tile = plan.autotune() if op != "tti" else {}
+    sep = bool(plan.get_tile()["sep"])
+    images_every = 1
+    plan.upload_traces(capi.CLOUD_SRC, wl.src)
+    data = None
+    if op in ("adjoint", "gradient"):
+        data = wl.residual_traces()
+        plan.upload_traces(capi.CLOUD_REC, data)
+    if op == "gradient":
+        images_every = 4                       # configs[2]: every 4th level saved in HBM
+        plan.run_resident(capi.OP_FORWARD, images_every)
+    with ClockSampler(device) as clk:
+        ws = windows(plan, op, wl.nt, W, K)
+        st = windows(plan, op, wl.nt, W, K, runs=1, stencil_only=True)[0]
+    clocks = clk.summary()
+    rep = ws[len(ws) // 2]
+    res = {"value": pts * K / rep.seconds / 1e9, "unit": "GPts/s", "ms_per_step": rep.seconds / K * 1e3,
+           "value_runs": [pts * K / r.seconds / 1e9 for r in ws], "gpu_launches": int(rep.kernel_launches),
+           "clocks": clocks,
+           "roofline": roofline_of(op, pts, st.seconds / st.steps, sep, images_every,
+                                   plan.get_tile() if op != "tti" else {}, wl.order // 2, clocks)}
+    if want_e2e:
+        # the C-ABI call with HOST buffers over exactly K steps: a plan with nt = K + 2
+        plan.close()
+        wk = wl_with_steps(wl, K)
+        p2 = wk.make_plan(device)
+        if tile:
+            p2.set_tile(tile["txv"], tile["ty"], tile["stages"], 0)
+        n_src, n_rec = wk.src_base.shape[0], wk.rec_base.shape[0]
+        if op == "forward":
+            rec = np.empty((wk.nt, n_rec))
+            call = lambda: p2.forward(wk.src, out=rec)[0]          # noqa: E731
+            h2d, d2h = n_src * 8, n_rec * 8
+        elif op == "tti":
+            call = lambda: p2.tti_forward(wk.src)[0]               # noqa: E731
+            h2d, d2h = n_src * 8, n_rec * 8
+        elif op == "adjoint":
+            d2 = wk.residual_traces()
+            call = lambda: p2.adjoint(d2)[0]                       # noqa: E731
+            h2d, d2h = n_rec * 8, n_src * 8
+        else:
+            d2 = wk.residual_traces()
+            p2.forward(wk.src, save_every=images_every)            # the history the sweep images against
+            call = lambda: p2.gradient(d2)[0]                      # noqa: E731
+            h2d, d2h = n_rec * 8, int(pts * 8 / K)                 # grad (f64, padded grid) comes back once
+        call()                                                     # warm-up: allocations, first touch
+        t0 = time.perf_counter()
+        out = call()
+        sec = time.perf_counter() - t0
+        assert np.isfinite(out).all()
+        if wl.config != 5:    # configs[4]'s random sources may sit far from the receiver plane
+            assert float(np.abs(out).max()) > 0.0
+        res["e2e"] = {"value": pts * K / sec / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": int(h2d),
+                      "d2h_bytes_per_step": int(d2h), "seconds": sec,
+                      "call": {"forward": "sfb_forward", "adjoint": "sfb_adjoint",
+                               "gradient": "sfb_gradient (history of a prior sfb_forward resident)",
+                               "tti": "sfb_tti_forward"}[op]}
+        p2.close()
+    else:
+        plan.close()
+    torch.cuda.synchronize()
+    return res
 
-def cpu_run(model_shape, vmax_dt, steps, threads=None):
-    """Oracle (f64 port of the reference's loop nest, all host threads) on the same 592^3
-    order-8 dense update; returns (GPts/s, threads, seconds)."""
+
+def wl_with_steps(wl, nsteps):
+    """the same configuration over `nsteps` steps: only the time axis shrinks (the Ricker
+    source table of a shorter run is a prefix of the longer one's)"""
+    if wl.nt == nsteps + 2:
+        return wl
+    assert nsteps + 2 <= wl.nt
+    w2 = object.__new__(Workload)
+    w2.__dict__.update(wl.__dict__)
+    w2.nt = nsteps + 2
+    w2.src = np.ascontiguousarray(wl.src[: w2.nt])
+    return w2
+
+
+def cheap_tti_fields(N):
+    """analytic Thomsen fields for the TTI extra of the default line (the seeded config-4 fields
+    take a minute of host filtering; --op tti / --config 4 uses them)"""
+    lin = [np.linspace(0.0, 1.0, n) for n in N]
+    ones = np.ones(N)
+    eps = 0.3 * lin[0][:, None, None] * ones
+    delta = 0.2 * lin[1][None, :, None] * lin[0][:, None, None] * ones
+    theta = (np.pi / 4) * lin[2][None, None, :] * ones
+    phi = (np.pi / 4) * lin[1][None, :, None] * ones
+    return [eps, delta, theta, phi]
+
+
+# ---- CPU legs ---------------------------------------------------------------------------
+
+def oracle_dense(N, order, dt, steps, threads=None):
+    """f64 oracle port (oracle/sf_oracle.c, OpenMP) on the dense update of an N grid."""
     from oracle import oracle as o
     if threads:
         o.set_num_threads(threads)
-    N = model_shape
     rng = np.random.default_rng(7)
 
-    class M:  # minimal stand-in carrying what dense_steps reads
+    class M:
         pass
     m = M()
     m.ndim, m.N, m.spacing = 3, list(N), [H] * 3
@@ -209,213 +462,356 @@ def cpu_run(model_shape, vmax_dt, steps, threads=None):
     cur = rng.standard_normal(N) * 1e-3
     old = cur.copy()
     t0 = time.time()
-    o.dense_steps(m, ORDER, vmax_dt, steps, cur, old)
+    o.dense_steps(m, order, dt, steps, cur, old)
     sec = time.time() - t0
     return float(np.prod(N)) * steps / sec / 1e9, o.num_threads(), sec
 
 
-def reference_cpu(n, steps):
-    """The reference's OWN engines (oracle/_ref: its unmodified sources compiled in place) on
-    the bare order-8 acoustic update of an n^3 grid -- the recipe of its `bench`
-    (proj/src/verify.cpp:338-376).  Tries its default engine (emitted C, serial) and its
-    threaded interpreter with every host thread, returns the faster."""
+def reference_inputs(config, planes, vel=None):
+    """configs[1] / configs[4] inputs cut to `planes` physical planes along the slowest axis
+    (the whole workload when planes = the configuration's extent)"""
+    from paper_1808_01995_b200 import synthetic as syn
+    c = CONFIGS[config]
+    n = c["n"]
+    shape = [planes, n, n]
+    ext0 = H * (planes - 1)
+    if config == 5:
+        if vel is None:
+            vel = syn.smooth_slab([n, n, n], 0, planes, syn.SEED + 6, 8.0, 1.5, 4.5)
+        src = np.random.default_rng(syn.SEED + 7).uniform([0, 0, 0], [ext0, H * (n - 1), H * (n - 1)], size=(8, 3))
+        ii, jj = np.meshgrid(np.linspace(0.0, ext0, n), np.arange(n) * H, indexing="ij")
+        rec = np.stack([ii.ravel(), jj.ravel(), np.full(ii.size, 25.0)], axis=1)
+    else:
+        cfg = syn.config(2, n)
+        if vel is None:
+            vel = cfg["velocity"]()
+        vel = vel[:planes]
+        src = np.asarray(cfg["src"], dtype=float).copy()
+        src[:, 0] = np.minimum(src[:, 0], 0.5 * ext0 + H / 4)
+        rec = cfg["rec"][cfg["rec"][:, 0] <= ext0]
+    return shape, np.ascontiguousarray(vel), src, rec
+
+
+def reference_forward(config, inputs, nsteps, threads):
+    """The reference's OWN forward_operator + run_wave (proj/src/seismic_ops.cpp:58-82,137-141)
+    through oracle/_ref, threaded interpreter engine; returns (seconds of its stepping loop,
+    computed nodes)."""
+    from oracle import oracle as o
     from oracle import ref
-    cores = os.cpu_count() or 1
-    best = None
-    trials = [("interpreter", ref.INTERPRETER, cores)]
-    if ref.emit_available():
-        trials.insert(0, ("emitted-C (cc -O2, serial: proj/src/emit.cpp:282-283)", ref.EMITTED, 1))
-    for name, be, thr in trials:
-        sec, _ = ref.dense_bench(n, ORDER, steps, be, thr)
-        g = float(n) ** 3 * steps / sec / 1e9
-        if best is None or g > best[0]:
-            best = (g, thr, sec, name)
-    return best
+    shape, vel, src, rec = inputs
+    order = CONFIGS[config]["order"]
+    w = o.second_derivative_weights(order)
+    sum_abs = float(abs(w[0]) + 2 * np.abs(w[1:]).sum())
+    dt = H / 4.5 / np.sqrt(3 * sum_abs / 2.0) * (1.0 - 1e-9)          # critical dt at v_max <= 4.5
+    p = ref.Problem(shape, [H] * 3, [0.0] * 3, vel, NBL, order, order, src, rec,
+                    0.0, (nsteps + 1.5) * dt, dt, 0.015)
+    out = p.forward(backend=ref.INTERPRETER, nthreads=threads, levels=False)
+    assert out["nt"] == nsteps + 2, (out["nt"], nsteps)
+    return out["seconds"], float(np.prod([x + 2 * NBL for x in shape]))
 
 
 def reference_arm(args):
-    """`--impl reference`: the CPU implementation of the path on this box's host cores."""
+    """`--impl reference`: the reference's CPU implementation of the path on this box's host
+    cores -- its own forward_operator through oracle/_ref when that was built (kind
+    "reference"), else the oracle port (kind "port") -- W warm-up steps, then K timed steps,
+    on a sample of the workload bounded to about 150 s of CPU work."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = N_PHYS + 2 * NBL
+    config, op = args.config, args.op
+    K, W = args.steps, max(args.warmup, 1)
+    cores = os.cpu_count() or 1
+    c = CONFIGS[config]
+    order, n1 = c["order"], c["n"] + 2 * NBL
+    N, phys = grid_of(config, args.gpus, args.scaling)
+    budget = 150.0
     from oracle import ref
-    from paper_1808_01995_b200 import capi
-    if ref.available():
+    if op == "forward" and config in (2, 5) and ref.available():
         kind = "reference"
-        g1, thr, s1, name = reference_cpu(n, 1)          # calibration (also warms the C cache)
-        k = max(1, min(args.steps, int(20.0 / max(s1, 1e-3))))
-        gpts, cores, sec, name = reference_cpu(n, k)
-        sample = (f"{k} dense time steps of the full 592^3 order-8 grid on the reference's own "
-                  f"engine ({name}, {cores} thread(s)), f64")
-        w = 1
+        s1, pts1 = reference_forward(config, reference_inputs(config, 48), 2, cores)
+        rate = pts1 * 2 / s1                                          # node-steps per second
+        total = int(min(N[0], budget * rate / (K + W) / (n1 * n1), 4.0e8 / (n1 * n1)))
+        planes = max(48, min(phys[0], total - 2 * NBL))
+        inputs = reference_inputs(config, planes)
+        reference_forward(config, inputs, W, cores)                   # W untimed warm-up steps
+        sec, pts = reference_forward(config, inputs, K, cores)
+        gpts = pts * K / sec / 1e9
+        sample = (f"the reference's own forward_operator + run_wave (threaded interpreter engine, "
+                  f"{cores} threads, f64) on {c['key']}'s inputs"
+                  + ("" if planes == phys[0] else f", {planes} of {phys[0]} physical planes along the "
+                     "slowest axis (bounded sample)")
+                  + f": {K} time steps incl. source injection and receiver sampling, order {order}")
     else:
         kind = "port"
-        dt = capi.critical_dt([H] * 3, 4.5, ORDER)
-        gpts, cores, sec = cpu_run([n] * 3, dt, 1)
-        k = max(1, min(args.steps, int(25.0 / max(sec, 1e-3))))
-        w = 1
-        gpts, cores, sec = cpu_run([n] * 3, dt, k)
-        sample = (f"{k} dense time steps of the full 592^3 order-8 grid (f64 oracle port, "
-                  f"OpenMP, {cores} threads)")
+        from paper_1808_01995_b200 import capi
+        dt = capi.critical_dt([H] * 3, 4.5, order)
+        g, cores, s = oracle_dense([64, n1, n1], order, dt, 1)
+        rate = 64.0 * n1 * n1 / s
+        planes = int(max(64, min(N[0], budget * rate / (K + W) / (n1 * n1), 4.0e8 / (n1 * n1))))
+        oracle_dense([planes, n1, n1], order, dt, W)
+        gpts, cores, sec = oracle_dense([planes, n1, n1], order, dt, K)
+        why = {"forward": "", "adjoint": "; the adjoint and gradient sweeps run this same dense update",
+               "gradient": "; the adjoint and gradient sweeps run this same dense update",
+               "tti": "; the reference has no TTI operator: the acoustic update at the same order stands in"}[op]
+        sample = (f"{K} dense time steps of a {planes}x{n1}x{n1} grid, order {order}, f64 oracle port "
+                  f"(oracle/sf_oracle.c, OpenMP, {cores} threads){why}")
     line = {
-        "impl": "reference", "metric": "acoustic_forward_gpts_per_s", "value": gpts,
-        "unit": "GPts/s", "n_gpus": args.gpus, "steps": k, "warmup": w,
-        "ms_per_step": sec / k * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.gpus),
-        "cpu_baseline": {"value": gpts, "unit": "GPts/s", "cores": cores, "kind": kind,
-                         "sample": sample},
+        "impl": "reference", "metric": METRIC[op], "value": gpts, "unit": "GPts/s",
+        "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": sec / K * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(config, op, args.gpus, args.scaling),
+        "cpu_baseline": {"value": gpts, "unit": "GPts/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": gpts, "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(n_gpus):
-    return {"workload": "BASELINE.json configs[1]: acoustic forward, 512^3 physical + 40-node "
-                        "absorbing layer (592^3 computed), space order 8, fp32, 1 Ricker source, "
-                        "512x512 receivers, seeded smoothed-noise velocity in [1.5,4.5] km/s",
-            "grid": [N_PHYS + 2 * NBL] * 3, "space_order": ORDER,
-            "decomposition": f"{n_gpus} slab(s) along the slowest axis",
-            "l2": "every field (0.83 GB) is larger than the 126 MB L2: no flush needed"}
+def cpu_baseline_leg(config, vel=None):
+    """bounded CPU sample beside the GPU line (rank 0): the reference's own engine when
+    oracle/_ref exists, with the oracle port's figure quoted in the sample text"""
+    from paper_1808_01995_b200 import capi
+    c = CONFIGS[config]
+    order, n1 = c["order"], c["n"] + 2 * NBL
+    dt = capi.critical_dt([H] * 3, 4.5, order)
+    planes, nst = (336, 10) if config != 5 else (96, 10)
+    oracle_dense([planes, n1, n1], order, dt, 1)            # first touch of the oracle's buffers
+    g, cores, s = oracle_dense([planes, n1, n1], order, dt, nst)
+    cpu = {"value": g, "unit": "GPts/s", "cores": cores, "kind": "port",
+           "sample": f"{nst} dense time steps of a {planes}x{n1}x{n1} grid (order {order}), f64 oracle port "
+                     f"(oracle/sf_oracle.c, gcc -O3 -fopenmp), {s:.1f} s"}
+    from oracle import ref
+    if ref.available() and config in (2, 5):
+        threads = os.cpu_count() or 1
+        pl, rst = (256, 8) if config != 5 else (64, 8)
+        sec, pts = reference_forward(config, reference_inputs(config, pl, vel), rst, threads)
+        cpu = {"value": pts * rst / sec / 1e9, "unit": "GPts/s", "cores": threads, "kind": "reference",
+               "sample": f"{rst} time steps of the reference's own forward_operator (threaded interpreter, "
+                         f"f64) on {c['key']}'s inputs, {pl} of {c['n']} physical planes along the slowest "
+                         f"axis, {sec:.1f} s; the OpenMP oracle port reaches {g:.3f} GPts/s on {cores} threads"}
+    return cpu
 
 
-# ---- our arm -----------------------------------------------------------------------------
+# ---- our arm, one GPU -------------------------------------------------------------------
+
+def single_gpu(args):
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    K, W = args.steps, max(args.warmup, 3)
+    config, op = args.config, args.op
+    wl = Workload(config, op, W + K, scaling=args.scaling)
+    main = measure_op(wl, op, K, W, local)
+    line = {"metric": METRIC[op], "value": main["value"], "unit": "GPts/s", "n_gpus": 1, "steps": K,
+            "warmup": W, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(config, op, 1, args.scaling),
+            "roofline": main["roofline"], "cpu_baseline": None, "e2e": main["e2e"],
+            "gpu_launches": main["gpu_launches"], "clocks": main["clocks"],
+            "value_runs": main["value_runs"]}
+    if op == "forward" and config == 2 and not args.no_other_ops:
+        # the dense-damping build of the same kernel really streams the contract's 20 B
+        try:
+            from paper_1808_01995_b200 import capi
+            pd = wl.make_plan(local, dense_damping=True)
+            pd.autotune()
+            pd.upload_traces(capi.CLOUD_SRC, wl.src)
+            st = windows(pd, "forward", wl.nt, W, K, runs=1, stencil_only=True)[0]
+            pts = float(np.prod(wl.N))
+            ks = st.seconds / st.steps
+            line["roofline"]["dense_damping_build"] = {
+                "kernel_ms": ks * 1e3, "bytes_per_point": 20.0, "achieved": 20.0 * pts / ks / 1e9,
+                "frac": 20.0 * pts / ks / 1e9 / peaks()[0], "tile": pd.get_tile()}
+            pd.close()
+        except Exception as e:
+            line["roofline"]["dense_damping_build"] = {"error": repr(e)}
+        ops = {}
+        for other in ("adjoint", "gradient"):
+            try:
+                ops[other] = measure_op(wl, other, K, W, local)
+            except Exception as e:  # never lose the contract line over an extra
+                ops[other] = {"error": repr(e)}
+        try:
+            wt = object.__new__(Workload)
+            wt.__dict__.update(wl.__dict__)
+            wt.config, wt.op, wt.order = 2, "tti", 12
+            wt.tti = cheap_tti_fields(wl.N)
+            from paper_1808_01995_b200 import capi
+            wt.dt = 0.9 * capi.critical_dt([H] * 3, wl.v_max, 12) / np.sqrt(1.6)
+            wt.src = np.sin(np.arange(wl.nt) * 0.1).reshape(-1, 1) * np.ones((1, wl.src.shape[1]))
+            ops["tti"] = measure_op(wt, "tti", K, W, local, want_e2e=False)
+            ops["tti"]["note"] = ("order 12 on the 592^3 grid with analytic Thomsen fields; "
+                                  "`--config 4` runs BASELINE.json configs[3] with its seeded fields")
+        except Exception as e:
+            ops["tti"] = {"error": repr(e)}
+        line["operators"] = ops
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_leg(config, getattr(wl, "vel_phys", None))
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm, N GPUs ----------------------------------------------------------------------
+
+class SlabJob:
+    """bench_core job over one capi.Plan on one GPU."""
+
+    def __init__(self, wl, plan, op, device, rank, world):
+        import torch
+        from paper_1808_01995_b200 import capi, slabs
+        self.torch, self.capi, self.wl, self.plan, self.op = torch, capi, wl, plan, op
+        self.oid = op_ids(op)
+        lo, hi = wl.bounds[rank]
+        self.points_owned = float(hi - lo) * wl.N[1] * wl.N[2]
+        self.halo = "none (one GPU)"
+        ex = slabs.HaloExchanger(rank, world)
+        if op == "tti":
+            self.eng = slabs.TtiPlanEngine(plan, device)
+            self._loop = lambda a, b: slabs.tti_step_loop(self.eng, ex, a, b)     # noqa: E731
+            if world > 1:
+                self.halo = "nccl send/recv (two exchanges per step: g, then p and r)"
+        else:
+            self.eng = slabs.PlanEngine(plan, self.oid, device)
+            self._loop = lambda a, b: slabs.step_loop(self.eng, ex, a, b)         # noqa: E731
+            if world > 1:
+                self.halo = "nccl send/recv"
+                if os.environ.get("SFB_HALO", "push") == "push":
+                    try:
+                        drv = slabs.PeerPushDriver(plan, self.oid, rank, world)
+                        self._loop = drv.run
+                        self.halo = "fused peer push (CUDA IPC stores from the boundary kernels)"
+                    except RuntimeError as e:
+                        if rank == 0:
+                            log(f"[bench] {e}; falling back to NCCL send/recv")
+        self.e0 = torch.cuda.Event(enable_timing=True)
+        self.e1 = torch.cuda.Event(enable_timing=True)
+
+    def begin(self):
+        self.plan.step_begin(self.oid)
+
+    def loop(self, a, b):
+        self._loop(a, b)
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def start(self):
+        e = self.eng
+        e.s_main.wait_stream(e.s_bnd)
+        with self.torch.cuda.stream(e.s_main):
+            self.e0.record()
+        e.s_bnd.wait_stream(e.s_main)
+
+    def stop(self):
+        e = self.eng
+        e.s_main.wait_stream(e.s_bnd)
+        with self.torch.cuda.stream(e.s_main):
+            self.e1.record()
+        self.torch.cuda.synchronize()
+        return self.e0.elapsed_time(self.e1) * 1e-3
+
+    def launches(self):
+        return self.plan.launch_count()
+
+    def upload(self):
+        self.plan.upload_traces(self.capi.CLOUD_SRC, self.wl.src)
+        return float(self.wl.src.nbytes)
+
+    def download(self):
+        rec = self.plan.download_traces(self.capi.CLOUD_REC)
+        self.rec = rec
+        return float(rec.nbytes)
+
+
+def multi_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1808_01995_b200 import capi, slabs
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    # NCCL prints its banner (and, with NCCL_DEBUG=INFO, its communicator lines) on stdout;
+    # the contract is ONE JSON line there, so stdout is parked on stderr until the line is ready
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29577")
+    os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator lines -> stderr
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if world > 1 or os.environ.get("SFB_BENCH_INIT_PG"):
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device(f"cuda:{local}"))
+    K, W = args.steps, max(args.warmup, 3)
+    config, op = args.config, args.op
+    wl = Workload(config, op, W + K, rank, world, args.scaling)
+    plan = wl.make_plan(local)
+    tile = plan.autotune() if op != "tti" else {}
+    sep = bool(plan.get_tile()["sep"])
+    plan.upload_traces(capi.CLOUD_SRC, wl.src)
+    job = SlabJob(wl, plan, op, local, rank, world)
+    comm = slabs.Comm(rank, world, torch.device(f"cuda:{local}"))
+    with ClockSampler(local) as clk:
+        meas = slabs.bench_core(comm, job, K, W)
+    clocks = clk.summary()
+    plan.step_end(op_ids(op))
+    assert np.isfinite(job.rec).all()
+    log(f"[bench] rank {rank}: {meas['per_rank_ms_per_step'][rank]:.4f} ms/step on its slab "
+        f"{wl.bounds[rank]}, halo: {job.halo}")
+    halo_bytes = int(plan.halo_blocks(capi.OP_FORWARD, 1)["count"] * 4) * (4 if op == "tti" else 1)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline_leg(config)
+    sys.stdout.flush()
+    os.dup2(saved_stdout, 1)
+    os.close(saved_stdout)
+    if rank == 0:
+        peak, kind = peaks()
+        line = slabs.scaling_line(
+            meas, metric=METRIC[op], world=world, K=K, W=W, scaling=args.scaling,
+            config=workload_config(config, op, world, args.scaling, {"tile": tile or None}),
+            bytes_per_point=actual_bytes(op, sep), contract_bytes=CONTRACT_BYTES[op], peak=peak,
+            peak_kind=kind, halo=job.halo, halo_bytes=halo_bytes,
+            extra={"cpu_baseline": cpu, "clocks": clocks})
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if dist.is_initialized():
+        dist.barrier()
+        dist.destroy_process_group()
+
 
 def ours(args):
     import torch
     from paper_1808_01995_b200 import capi
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available() or capi.device_count() < 1:
         raise SystemExit("bench.py needs a CUDA device: there is no CPU fallback")
-    K, W = args.steps, max(args.warmup, 3)
     if world > 1 or os.environ.get("SFB_BENCH_FORCE_DIST"):
-        from paper_1808_01995_b200 import slabs
-        return slabs.bench_distributed(args, K, W, build_workload, workload_config,
-                                       BYTES_PER_POINT, peaks)
-    torch.cuda.set_device(local)
-    cfg, model, geom = build_workload(W + K)
-    N = model.grid.shape
-    pts = float(np.prod(N))
-    t0 = time.time()
-    plan = make_plan(model, geom, local)
-    tile = plan.autotune()   # as in the paper, timing starts after the tile-shape autotuning
-    log(f"[bench] plan + uploads in {time.time() - t0:.1f}s, tile {tile}")
-    src = geom.src.traces
-    plan.upload_traces(capi.CLOUD_SRC, src)
-
-    # --- value: K steps after W warm-up steps, inputs resident, device-timed ------------
-    F = capi.OP_FORWARD
-    plan.step_begin(F)
-    plan.run_steps(F, 1, 1 + W)
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        rep = plan.run_steps(F, 1 + W, 1 + W + K)
-        torch.cuda.synchronize()
-        # two more windows of exactly K steps each (SURVEY.md 8d: "median of >= 3"); the
-        # line's value is the median window, all three are listed in `value_runs`
-        windows = [rep]
-        for _ in range(2):
-            plan.step_begin(F)
-            plan.run_steps(F, 1, 1 + W)
-            windows.append(plan.run_steps(F, 1 + W, 1 + W + K))
-            torch.cuda.synchronize()
-        windows.sort(key=lambda r: r.seconds)
-        value_runs = [pts * K / r.seconds / 1e9 for r in windows]
-        rep = windows[1]
-        # --- roofline: the dense-update kernel alone over the same K steps ----------------
-        plan.step_begin(F)
-        plan.run_steps(F, 1, 1 + W)
-        st = plan.time_stencil(F, 1 + W, 1 + W + K)
-    clocks = clk.summary()
-    plan.step_end(F)
-    value = pts * K / rep.seconds / 1e9
-    kern_s = st.seconds / st.steps
-    peak, peak_kind = peaks()
-    achieved = BYTES_PER_POINT * pts / kern_s / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if os.path.exists(tf):
-        with open(tf) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-
-    # --- e2e: the C-ABI call with host buffers, K steps ---------------------------------
-    plan.close()
-    from paper_1808_01995_b200 import _sfb_host as Hst
-    from paper_1808_01995_b200 import synthetic as syn
-    dt, tn = syn.time_axis(model.critical_dt(ORDER), K)
-    geom2 = Hst.AcquisitionGeometry(model, np.asarray(cfg["src"]).ravel(), cfg["rec"].ravel(),
-                                    0.0, tn, dt, cfg["f0"])
-    plan2 = make_plan(model, geom2, local)
-    src2 = np.ascontiguousarray(geom2.src.traces)
-    # the caller owns the receiver table (as geom.rec()->traces() in the reference): one
-    # buffer, touched by the warm-up pass, filled again by the timed call
-    rec = np.empty((geom2.nt, geom2.n_rec))
-    plan2.forward(src2[:], out=rec)  # warm-up pass (allocations, first touch of every buffer)
-    t0 = time.perf_counter()
-    rec, rep2 = plan2.forward(src2, out=rec)
-    e2e_s = time.perf_counter() - t0
-    e2e = pts * K / e2e_s / 1e9
-    assert np.isfinite(rec).all() and float(np.abs(rec).max()) > 0.0
-    other = None
-    if not args.no_other_ops:
-        other = other_operators(plan2, geom2, rec, model, local)
-    plan2.close()
-
-    # --- CPU baseline on this box's host cores (bounded sample) -------------------------
-    cpu = None
-    if not args.no_cpu:
-        g1, cores, s1 = cpu_run(N, geom.dt, 1)
-        n = max(2, min(40, int(10.0 / max(s1, 1e-3))))
-        g, cores, s = cpu_run(N, geom.dt, n)
-        cpu = {"value": g, "unit": "GPts/s", "cores": cores, "kind": "port",
-               "sample": f"{n} dense time steps of the same 592^3 order-8 grid, f64 oracle "
-                         f"(oracle/sf_oracle.c, gcc -O3 -fopenmp), {s:.1f} s"}
-        from oracle import ref
-        if ref.available():
-            rg, rthr, rs, rname = reference_cpu(N[0], 2)
-            cpu = {"value": rg, "unit": "GPts/s", "cores": rthr, "kind": "reference",
-                   "sample": f"2 dense time steps of the same 592^3 order-8 grid on the "
-                             f"reference's own engine ({rname}), {rs:.1f} s; the OpenMP oracle "
-                             f"port reaches {g:.3f} GPts/s on {cores} threads"}
-
-    line = {
-        "metric": "acoustic_forward_gpts_per_s", "value": value, "unit": "GPts/s", "n_gpus": 1,
-        "steps": K, "warmup": W, "ms_per_step": rep.seconds / K * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(1),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": ("acoustic_step_dual_kernel" if tile["stages"] < 0
-                                else "acoustic_step_kernel"), "kernel_ms": kern_s * 1e3,
-                     "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts,
-                     "tile": tile},
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e, "unit": "GPts/s", "h2d_bytes_per_step": int(geom2.n_src * 8),
-                "d2h_bytes_per_step": int(geom2.n_rec * 8), "seconds": e2e_s,
-                "device_seconds": rep2.seconds},
-        "gpu_launches": int(rep.kernel_launches),
-        "clocks": clocks,
-        "value_runs": value_runs,
-    }
-    if other is not None:
-        line["other_operators"] = other
-    print(json.dumps(line), flush=True)
+        return multi_gpu(args)
+    return single_gpu(args)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json configuration, 1-based (default 2 = configs[1])")
+    ap.add_argument("--op", default=None, choices=["forward", "adjoint", "gradient", "tti"],
+                    help="operator (default: the configuration's own)")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"])
     ap.add_argument("--no-other-ops", action="store_true",
-                    help="skip the adjoint / gradient / TTI extras of the JSON line")
+                    help="skip the adjoint / gradient / TTI extras of the default line")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
+    args.op = args.op or CONFIGS[args.config]["op"]
+    args.scaling = args.scaling or CONFIGS[args.config]["scaling"]
+    if args.scaling == "weak" and args.config != 5:
+        raise SystemExit("weak scaling is defined for --config 5 only")
+    if (args.op == "tti") != (args.config == 4):
+        raise SystemExit("the TTI operator is --config 4, and --config 4 is the TTI operator")
     if args.impl == "reference":
         return reference_arm(args)
     return ours(args)

@@ -121,6 +121,12 @@ SFB_API int sfb_critical_dt(int ndim, const double* spacing, double v_max, int s
  * (proj/src/seismic_ops.cpp:15-22); pass 0 to skip the gate. */
 SFB_API int sfb_set_model(sfb_plan* plan, const sfb_field_view* m, const sfb_field_view* damp,
                   double v_max);
+/* the same for one slab of a decomposed run whose rank never holds the global fields: the
+ * views cover the plan's own planes [slab_lo, slab_hi) only (plane 0 of the view = global
+ * plane slab_lo).  Large weak-scaling runs (BASELINE.json configs[4]) build m and damp per
+ * rank. */
+SFB_API int sfb_set_model_slab(sfb_plan* plan, const sfb_field_view* m_slab,
+                               const sfb_field_view* damp_slab, double v_max);
 /* anisotropy fields of the TTI operator (no reference counterpart) */
 SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
                       const sfb_field_view* delta, const sfb_field_view* theta,
@@ -167,7 +173,8 @@ SFB_API int sfb_upload_traces(sfb_plan* plan, int cloud, const double* traces);
 SFB_API int sfb_download_traces(sfb_plan* plan, int cloud, double* traces);
 SFB_API int sfb_run_resident(sfb_plan* plan, int op, int64_t save_every, sfb_report* report);
 /* steps t in [t_from, t_to) of an operator begun with sfb_step_begin, without touching the
- * state first (descending for the backward operators); timed on the device */
+ * state first (descending for the backward operators; SFB_OP_TTI_FORWARD runs its two
+ * launches per step); timed on the device */
 SFB_API int sfb_run_steps(sfb_plan* plan, int op, int64_t t_from, int64_t t_to,
                           sfb_report* report);
 /* the same window with the dense update kernel alone (no scatter / gather launches):

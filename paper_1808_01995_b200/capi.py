@@ -42,7 +42,7 @@ class Report(C.Structure):
 # the header)
 SYMBOLS = [
     "sfb_abi_version", "sfb_last_error", "sfb_device_count", "sfb_plan_create",
-    "sfb_plan_destroy", "sfb_fd_weights", "sfb_critical_dt", "sfb_set_model",
+    "sfb_plan_destroy", "sfb_fd_weights", "sfb_critical_dt", "sfb_set_model", "sfb_set_model_slab",
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
@@ -56,6 +56,7 @@ lib.sfb_last_error.argtypes = [C.c_void_p]
 lib.sfb_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]
 lib.sfb_plan_destroy.argtypes = [C.c_void_p]
 lib.sfb_set_model.argtypes = [C.c_void_p, C.POINTER(FieldView), C.POINTER(FieldView), C.c_double]
+lib.sfb_set_model_slab.argtypes = lib.sfb_set_model.argtypes
 lib.sfb_set_model_tti.argtypes = [C.c_void_p] + [C.POINTER(FieldView)] * 4
 lib.sfb_tti_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Report)]
 lib.sfb_set_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
@@ -134,6 +135,28 @@ def critical_dt(spacing, v_max, order):
     return out.value
 
 
+def locate(shape, spacing, origin, coords):
+    """SparseFunction::locate on a padded grid (sfb_locate): base int64 [np][ndim], weights
+    f64 [np][2^ndim].  `origin` is the origin of the padded grid."""
+    nd = len(shape)
+    d = PlanDesc()
+    d.ndim = nd
+    for a in range(nd):
+        d.shape[a] = int(shape[a])
+        d.spacing[a] = float(spacing[a])
+    d.space_order = 2
+    d.dt, d.nt = 1.0, 3
+    org = np.asarray(origin, dtype=np.float64)
+    co = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, nd)
+    base = np.zeros((co.shape[0], nd), dtype=np.int64)
+    w = np.zeros((co.shape[0], 1 << nd))
+    rc = lib.sfb_locate(C.byref(d), org.ctypes.data, co.shape[0], co.ctypes.data,
+                        base.ctypes.data, w.ctypes.data)
+    if rc:
+        raise SfbError(rc, lib.sfb_last_error(None).decode())
+    return base, w
+
+
 def device_count():
     n = C.c_int()
     lib.sfb_device_count(C.byref(n))
@@ -186,6 +209,12 @@ class Plan:
         m = np.asarray(m, dtype=np.float64)
         damp = np.asarray(damp, dtype=np.float64)
         self._chk(lib.sfb_set_model(self.h, C.byref(_view(m)), C.byref(_view(damp)), float(v_max)))
+
+    def set_model_slab(self, m_slab, damp_slab, v_max=0.0):
+        """m and damp over the plan's own planes only (a rank of a decomposed run)."""
+        m = np.asarray(m_slab, dtype=np.float64)
+        damp = np.asarray(damp_slab, dtype=np.float64)
+        self._chk(lib.sfb_set_model_slab(self.h, C.byref(_view(m)), C.byref(_view(damp)), float(v_max)))
 
     def set_model_tti(self, epsilon, delta, theta, phi):
         arrs = [np.asarray(f, dtype=np.float64) for f in (epsilon, delta, theta, phi)]

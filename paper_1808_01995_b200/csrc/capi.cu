@@ -267,45 +267,66 @@ SFB_API int sfb_plan_destroy(sfb_plan* plan) {
     return SFB_OK;
 }
 
+namespace {
+
+// slab_local: the views cover the plan's own planes only (index 0 = global plane slab_lo);
+// they are rebased so that the global plane indices used below land inside them
+void bind_model(Plan& P, const sfb_field_view* m, const sfb_field_view* damp, double v_max,
+                bool slab_local) {
+    require(m && damp && m->ptr && damp->ptr, SFB_ERR_PARAMETER, "set_model: null field");
+    if (v_max > 0.0) {
+        // check_cfl, proj/src/seismic_ops.cpp:15-22
+        double crit = 0;
+        sfb_critical_dt(P.ndim, P.desc.spacing, v_max, P.desc.space_order, &crit);
+        if (P.desc.dt > crit * (1.0 + 1e-12))
+            throw Failure(SFB_ERR_STABILITY,
+                          "dt " + std::to_string(P.desc.dt) + " exceeds the stable limit " +
+                              std::to_string(crit) + " at order " +
+                              std::to_string(P.desc.space_order));
+    }
+    IntView mv = embed_view(P, m->ptr, m->stride), dv = embed_view(P, damp->ptr, damp->stride);
+    if (slab_local) {
+        mv.ptr -= P.z_lo * mv.s[0];
+        dv.ptr -= P.z_lo * dv.s[0];
+    }
+    P.v_max = v_max;
+    const long long rows = (long long)P.n0 * P.N[1];
+    DevBuf tmp;
+    P.r.alloc(size_t(P.ccount) * 4);
+    P.damp.alloc(size_t(P.ccount) * 4);
+    upload_f64(P, mv, tmp);
+    convert_r_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(
+        tmp.as<double>(), P.r.as<float>(), rows, int(P.N[2]), P.pitch, P.desc.dt * P.desc.dt);
+    SFB_CUDA(cudaGetLastError());
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    upload_f64(P, dv, tmp);
+    convert_f64_f32_pitched<<<row_grid(P, rows), 256, 0, P.s_main>>>(
+        tmp.as<double>(), P.damp.as<float>(), rows, int(P.N[2]), P.pitch);
+    SFB_CUDA(cudaGetLastError());
+    SFB_CUDA(cudaStreamSynchronize(P.s_main));
+    // reference plane of the profile extraction: the global centre plane when the whole
+    // field is visible (every slab of a decomposed run then derives bit-identical profiles),
+    // the slab's own centre plane otherwise
+    detect_separable_damping(P, dv, tmp, slab_local ? P.z_lo + P.n0 / 2 : P.N[0] / 2);
+    if (P.sep) P.damp.release();
+    select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST,
+                   int(P.variant->dual) + int(P.variant->rotate));
+    P.model_set = true;
+    P.history_valid = false;
+}
+
+}  // namespace
+
 SFB_API int sfb_set_model(sfb_plan* plan, const sfb_field_view* m, const sfb_field_view* damp,
                   double v_max) {
     if (!plan) return SFB_ERR_PARAMETER;
-    return guarded(plan, [&] {
-        Plan& P = *plan;
-        require(m && damp && m->ptr && damp->ptr, SFB_ERR_PARAMETER, "set_model: null field");
-        if (v_max > 0.0) {
-            // check_cfl, proj/src/seismic_ops.cpp:15-22
-            double crit = 0;
-            sfb_critical_dt(P.ndim, P.desc.spacing, v_max, P.desc.space_order, &crit);
-            if (P.desc.dt > crit * (1.0 + 1e-12))
-                throw Failure(SFB_ERR_STABILITY,
-                              "dt " + std::to_string(P.desc.dt) + " exceeds the stable limit " +
-                                  std::to_string(crit) + " at order " +
-                                  std::to_string(P.desc.space_order));
-        }
-        P.v_max = v_max;
-        const long long rows = (long long)P.n0 * P.N[1];
-        DevBuf tmp;
-        P.r.alloc(size_t(P.ccount) * 4);
-        P.damp.alloc(size_t(P.ccount) * 4);
-        upload_f64(P, embed_view(P, m->ptr, m->stride), tmp);
-        convert_r_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(
-            tmp.as<double>(), P.r.as<float>(), rows, int(P.N[2]), P.pitch,
-            P.desc.dt * P.desc.dt);
-        SFB_CUDA(cudaGetLastError());
-        SFB_CUDA(cudaStreamSynchronize(P.s_main));
-        upload_f64(P, embed_view(P, damp->ptr, damp->stride), tmp);
-        convert_f64_f32_pitched<<<row_grid(P, rows), 256, 0, P.s_main>>>(
-            tmp.as<double>(), P.damp.as<float>(), rows, int(P.N[2]), P.pitch);
-        SFB_CUDA(cudaGetLastError());
-        SFB_CUDA(cudaStreamSynchronize(P.s_main));
-        detect_separable_damping(P, embed_view(P, damp->ptr, damp->stride), tmp);
-        if (P.sep) P.damp.release();
-        select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST,
-                       int(P.variant->dual) + int(P.variant->rotate));
-        P.model_set = true;
-        P.history_valid = false;
-    });
+    return guarded(plan, [&] { bind_model(*plan, m, damp, v_max, false); });
+}
+
+SFB_API int sfb_set_model_slab(sfb_plan* plan, const sfb_field_view* m_slab,
+                               const sfb_field_view* damp_slab, double v_max) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] { bind_model(*plan, m_slab, damp_slab, v_max, true); });
 }
 
 SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,

@@ -64,7 +64,7 @@ void upload_f64(Plan& P, const IntView& v, DevBuf& tmp);
 void download_f64(Plan& P, const DevBuf& tmp, double* ptr, const int64_t* stride);
 dim3 row_grid(const Plan& P, long long rows);
 void download_field(Plan& P, const float* dev, const sfb_field_mview* out);
-void detect_separable_damping(Plan& P, const IntView& v, const DevBuf& damp_f64);
+void detect_separable_damping(Plan& P, const IntView& v, const DevBuf& damp_f64, long long ref_plane);
 void build_cloud(Plan& P, Cloud& c);
 constexpr size_t kStageBytes = 32u << 20;  // per half
 
@@ -182,7 +182,7 @@ void gradient_checkpointed(Plan& P, sfb_report* rep);
 void tti_make_maps(Plan& P);
 void tti_begin(Plan& P);
 void tti_rot(Plan& P, long long t, int part);
-void tti_update(Plan& P, long long t, int part);
+void tti_update(Plan& P, long long t, int part, bool with_points = true);
 void run_tti(Plan& P, sfb_report* rep, double* stream_out);
 
 }  // namespace sfb

@@ -260,11 +260,12 @@ __global__ void sep_check_kernel(const double* __restrict__ damp, const double* 
     atomicMax(maxabs, (unsigned long long)__double_as_longlong(mx));
 }
 
-void detect_separable_damping(Plan& P, const IntView& v, const DevBuf& damp_f64) {
+void detect_separable_damping(Plan& P, const IntView& v, const DevBuf& damp_f64, long long ref_plane) {
     P.sep = false;
     if (P.force_dense_damp) return;
-    // lines through the grid centre; the centre value is counted once (in px)
-    const long long c[3] = {P.N[0] / 2, P.N[1] / 2, P.N[2] / 2};
+    // lines through the reference node (grid centre by default); its value is counted once
+    // (in px).  Any reference node yields the same sums for a separable field.
+    const long long c[3] = {ref_plane, P.N[1] / 2, P.N[2] / 2};
     auto at = [&](long long i, long long j, long long l) {
         return v.ptr[i * v.s[0] + j * v.s[1] + l * v.s[2]];
     };

@@ -453,9 +453,20 @@ void run_window(Plan& P, int op, long long t_from, long long t_to, bool with_poi
     require(t_from >= 1 && t_to <= P.desc.nt - 1 && t_from <= t_to, SFB_ERR_PARAMETER,
             "run_steps: window outside [1, nt-1)");
     const long before = P.launches;
+    const bool tti = op == SFB_OP_TTI_FORWARD;
+    if (tti) {
+        require(P.tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
+        require(P.n0 == P.N[0], SFB_ERR_CAPABILITY, "TTI windows run one whole domain");
+        require(P.tti_chunk[0] > 0, SFB_ERR_PARAMETER, "call sfb_step_begin(SFB_OP_TTI_FORWARD) first");
+    }
     SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
     for (long long i = 0; i < t_to - t_from; ++i) {
         const long long t = ro.backward ? t_to - 1 - i : t_from + i;
+        if (tti) {   // the two launches of the rotated pair (engine_tti.cu)
+            tti_rot(P, t, SFB_PART_ALL);
+            tti_update(P, t, SFB_PART_ALL, with_points);
+            continue;
+        }
         step_compute(P, op, t, SFB_PART_ALL);
         if (with_points) step_points(P, op, t, SFB_PART_ALL);
     }
@@ -465,7 +476,8 @@ void run_window(Plan& P, int op, long long t_from, long long t_to, bool with_poi
     SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
     if (report) {
         const double own = double(P.n0) * double(P.N[1]) * double(P.N[2]);
-        const long long fpp = 3LL * P.K * P.ndim + 3LL * P.ndim + 11 + (ro.imaging ? 7 : 0);
+        const long long fpp = tti ? 57LL * P.K + 29
+                                  : 3LL * P.K * P.ndim + 3LL * P.ndim + 11 + (ro.imaging ? 7 : 0);
         report->seconds = ms * 1e-3;
         report->steps = long(t_to - t_from);
         report->flops = (long long)(double(fpp) * own * double(report->steps));

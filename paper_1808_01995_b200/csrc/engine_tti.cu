@@ -143,7 +143,7 @@ void tti_rot(Plan& P, long long t, int part) {
 // pass 2 and the update on the planes of `part`, then the point work of the part: Hz(p),
 // Hz(r) from the products (ghost planes of a g included), L(p), both leapfrog updates in
 // place over level t-1, injection into p and r, sampling of p
-void tti_update(Plan& P, long long t, int part) {
+void tti_update(Plan& P, long long t, int part, bool with_points) {
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;
     part_range(P, part, lo, hi);
@@ -188,7 +188,7 @@ void tti_update(Plan& P, long long t, int part) {
         ++P.launches;
         mark_stream(P, part);
     }
-    if (part != SFB_PART_LOW) {
+    if (with_points && part != SFB_PART_LOW) {
         // HIGH (called after LOW) carries the point work of both boundary plane groups, so
         // the injections land after both groups have been overwritten by the update
         const int op = SFB_OP_TTI_FORWARD;

@@ -276,95 +276,108 @@ class PeerPushDriver:
             self.plan.peer_wait_ipc()
 
 
-def bench_distributed(args, K, W, build_workload, workload_config, bytes_per_point, peaks):
-    """bench.py at N > 1: configs[1] cut into N slabs (strong scaling), NCCL halo exchange,
-    device time = max over ranks between barriers."""
-    import torch
-    import torch.distributed as dist
-    from . import capi
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    # NCCL prints its version banner on stdout; the contract is ONE JSON line there, so
-    # stdout is parked on stderr until the line is ready
-    import sys
-    sys.stdout.flush()
-    saved_stdout = os.dup(1)
-    os.dup2(2, 1)
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29577")
-    dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device(f"cuda:{local}"))
-    cfg, model, geom = build_workload(W + K)
-    N = model.grid.shape
-    order = model.space_order
-    bounds = split_slabs(N[0], world, order // 2)
-    plan = capi.Plan(N, model.grid.spacing, order, geom.dt, geom.nt, local, bounds[rank])
-    plan.set_model(model.m.array(), model.damp.array(), model.v_max)
-    plan.set_points(capi.CLOUD_SRC, np.array(geom.src.base_table).reshape(-1, 3),
-                    np.array(geom.src.weight_table).reshape(-1, 8))
-    plan.set_points(capi.CLOUD_REC, np.array(geom.rec.base_table).reshape(-1, 3),
-                    np.array(geom.rec.weight_table).reshape(-1, 8))
-    plan.upload_traces(capi.CLOUD_SRC, geom.src.traces)
-    eng = PlanEngine(plan, capi.OP_FORWARD, local)
-    ex = HaloExchanger(rank, world)
-    # the exchange: fused halo push over peer memory (default), NCCL send/recv as the fallback
-    halo = "nccl send/recv"
-    loop = lambda a, b: step_loop(eng, ex, a, b)   # noqa: E731
-    if world > 1 and os.environ.get("SFB_HALO", "push") == "push":
-        try:
-            drv = PeerPushDriver(plan, capi.OP_FORWARD, rank, world)
-            loop = drv.run
-            halo = "fused peer push (CUDA IPC stores from the boundary kernels)"
-        except RuntimeError as e:
-            if rank == 0:
-                print(f"[bench] {e}; falling back to NCCL send/recv", file=sys.stderr)
-    plan.step_begin(capi.OP_FORWARD)
-    torch.cuda.synchronize()
-    dist.barrier()   # nobody pushes into a neighbour that is still zeroing its fields
-    loop(1, 1 + W)
-    torch.cuda.synchronize()
-    launches0 = plan.launch_count()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    eng.s_main.wait_stream(eng.s_bnd)
-    with torch.cuda.stream(eng.s_main):
-        e0.record()
-    eng.s_bnd.wait_stream(eng.s_main)
-    loop(1 + W, 1 + W + K)
-    eng.s_main.wait_stream(eng.s_bnd)
-    with torch.cuda.stream(eng.s_main):
-        e1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    plan.step_end(capi.OP_FORWARD)
-    pts = float(np.prod(N))
-    sec = float(ms.item()) * 1e-3
-    sys.stdout.flush()
-    os.dup2(saved_stdout, 1)
-    os.close(saved_stdout)
-    if rank == 0:
-        peak, kind = peaks()
-        line = {
-            "metric": "acoustic_forward_gpts_per_s", "value": pts * K / sec / 1e9,
-            "unit": "GPts/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": sec / K * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(world),
-            "roofline": {"bound": "hbm", "achieved": bytes_per_point * pts * K / sec / 1e9 / world,
-                         "peak": peak, "unit": "GB/s",
-                         "frac": bytes_per_point * pts * K / sec / 1e9 / world / peak,
-                         "traffic": None, "peak_kind": kind,
-                         "note": "per-GPU figure of the whole step (update + exchange)"},
-            "cpu_baseline": None,
-            "e2e": None,
-            "gpu_launches": int(plan.launch_count() - launches0),
-            "halo_bytes_per_step_per_neighbour": int(plan.halo_blocks(capi.OP_FORWARD, 1)["count"] * 4),
-            "halo": halo,
-        }
-        print(json.dumps(line), flush=True)
-    plan.close()
-    dist.destroy_process_group()
+# ---- bench.py at N > 1 ----------------------------------------------------------------------
+
+def weak_extent(per_rank: int, world: int) -> int:
+    """Slab-axis extent of a weak-scaling run (BASELINE.json configs[4]: 128 physical planes
+    per GPU)."""
+    return per_rank * world
+
+
+class Comm:
+    """The few collectives the bench needs, over torch.distributed (nccl on GPUs, gloo in the
+    CPU test).  None of them is on the data path."""
+
+    def __init__(self, rank, world, device=None):
+        self.rank, self.world, self.device = rank, world, device
+        import torch
+        self.torch = torch
+        self.dist = torch.distributed if world > 1 else None
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def gather_floats(self, x):
+        """every rank's value of x, on every rank"""
+        if not self.dist:
+            return [float(x)]
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self.device)
+        out = [self.torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t)
+        return [float(o.item()) for o in out]
+
+
+def bench_core(comm: Comm, job, K: int, W: int):
+    """The timed region of one slab benchmark, backend-agnostic: W untimed warm-up steps, then
+    exactly K steps bracketed by a barrier and a device synchronisation on both sides, device
+    time per rank, MAX over ranks; then the end-to-end leg (upload of the injected traces,
+    K steps, download of the rank's sampled rows) by wall clock, max over ranks.
+
+    `job` provides begin(), loop(t_from, t_to), sync(), start()/stop() -> seconds of the
+    queued work on the device, points_owned, launches(), upload(), download() -> bytes moved.
+    Returns the measurements every rank agrees on."""
+    import time as _time
+    job.begin()
+    job.sync()
+    comm.barrier()   # nobody pushes into a neighbour that is still zeroing its fields
+    job.loop(1, 1 + W)
+    job.sync()
+    launches0 = job.launches()
+    comm.barrier()
+    job.start()
+    job.loop(1 + W, 1 + W + K)
+    sec_rank = job.stop()
+    job.sync()
+    comm.barrier()
+    launches = job.launches() - launches0
+    per_rank = comm.gather_floats(sec_rank)
+    pts = sum(comm.gather_floats(job.points_owned))
+    # end to end: host buffers in, host buffers out, every copy inside the timed region
+    comm.barrier()
+    t0 = _time.perf_counter()
+    h2d = job.upload()
+    job.begin()
+    job.loop(1, 1 + K)
+    d2h = job.download()
+    job.sync()
+    e2e_rank = _time.perf_counter() - t0
+    comm.barrier()
+    e2e = comm.gather_floats(e2e_rank)
+    return {"seconds": max(per_rank), "per_rank_ms_per_step": [s / K * 1e3 for s in per_rank],
+            "points": pts, "launches": int(launches), "e2e_seconds": max(e2e),
+            "h2d_bytes_per_step": sum(comm.gather_floats(h2d)) / K,
+            "d2h_bytes_per_step": sum(comm.gather_floats(d2h)) / K}
+
+
+def scaling_line(meas, *, metric, world, K, W, scaling, config, bytes_per_point, contract_bytes,
+                 peak, peak_kind, halo, halo_bytes, dtype="f32", extra=None):
+    """The JSON line of an N-GPU run from bench_core's measurements (rank 0 prints it)."""
+    sec, pts = meas["seconds"], meas["points"]
+    value = pts * K / sec / 1e9
+    per_gpu_gbs = bytes_per_point * pts * K / sec / 1e9 / world
+    line = {
+        "metric": metric, "value": value, "unit": "GPts/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": sec / K * 1e3, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config,
+        "roofline": {"bound": "hbm", "achieved": per_gpu_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": per_gpu_gbs / peak, "traffic": None, "peak_kind": peak_kind,
+                     "basis_bytes_per_point": bytes_per_point,
+                     "frac_contract": contract_bytes * pts * K / sec / 1e9 / world / peak,
+                     "contract_bytes_per_point": contract_bytes,
+                     "note": "per-GPU figure of the whole slab step (update + point work + "
+                             "exchange), not of one kernel"},
+        "e2e": {"value": pts * K / meas["e2e_seconds"] / 1e9, "unit": "GPts/s",
+                "h2d_bytes_per_step": meas["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": meas["d2h_bytes_per_step"],
+                "seconds": meas["e2e_seconds"],
+                "how": "per rank: upload of the injected trace table from host memory, K slab "
+                       "steps, download of the rank's sampled rows; wall clock between "
+                       "barriers, max over ranks"},
+        "gpu_launches": meas["launches"],
+        "per_rank_ms_per_step": meas["per_rank_ms_per_step"],
+        "halo": halo, "halo_bytes_per_step_per_neighbour": halo_bytes,
+    }
+    if extra:
+        line.update(extra)
+    return line

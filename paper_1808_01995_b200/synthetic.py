@@ -100,3 +100,67 @@ def time_axis(critical_dt, nsteps=None, tn=None):
     if tn is None or nsteps is not None:
         tn = (nsteps + 1.5) * dt
     return dt, tn
+
+
+# ---- slab-local generators (multi-GPU weak scaling: no rank ever holds a global field) ------
+
+def damping_profiles(N, nbl, spacing, v_max):
+    """The three 1-D profiles whose sum is build_damping's field (proj/src/model.cpp:35-56,
+    quadratic ramp): eta_d w^2 with w = (nbl - dist)/nbl for dist = min(i, N-1-i) < nbl,
+    eta_d = v_max ln(1000) / (nbl h_d).  Checked against the host SeismicModel in
+    tests/test_host_cpu.py."""
+    out = []
+    for n, h in zip(N, spacing):
+        i = np.arange(n)
+        dist = np.minimum(i, n - 1 - i)
+        w = np.where(dist < nbl, (nbl - dist) / float(nbl), 0.0)
+        out.append((v_max * np.log(1000.0) / (nbl * h)) * w * w)
+    return out
+
+
+def smooth_slab(shape, lo, hi, seed, sigma, vlo, vhi, spread=4.2):
+    """Planes [lo, hi) of axis 0 of a seeded smoothed-noise field over `shape`, computable by
+    a rank that owns only those planes: white noise is drawn per global plane (seed + plane),
+    blurred in-plane (periodic) and along axis 0 over a 3-sigma window of neighbouring planes
+    (periodic), normalised by its analytic standard deviation and mapped linearly, clipped at
+    `spread` standard deviations, to [vlo, vhi].  Any two ranks produce identical values for a
+    plane they both generate.  Same value range and correlation length as smooth_field."""
+    from scipy.ndimage import gaussian_filter1d
+    n0, n1, n2 = shape
+    R = int(3.0 * sigma + 0.5)
+    k = np.exp(-0.5 * (np.arange(-R, R + 1) / float(sigma)) ** 2)
+    k /= k.sum()
+    planes = {}
+    for z in range(lo - R, hi + R):
+        zz = z % n0
+        if zz in planes:
+            continue
+        g = np.random.default_rng([seed, zz]).standard_normal((n1, n2), dtype=np.float32)
+        for ax in (0, 1):
+            g = gaussian_filter1d(g, float(sigma), axis=ax, mode="wrap", truncate=3.0)
+        planes[zz] = g
+    out = np.empty((hi - lo, n1, n2), dtype=np.float64)
+    for z in range(lo, hi):
+        acc = np.zeros((n1, n2), dtype=np.float64)
+        for j in range(-R, R + 1):
+            acc += k[j + R] * planes[(z + j) % n0]
+        out[z - lo] = acc
+    std = float(np.sqrt((k ** 2).sum()) ** 3)   # unit white noise through three 1-D kernels
+    mid, half = 0.5 * (vlo + vhi), 0.5 * (vhi - vlo)
+    return mid + half * np.clip(out / (spread * std), -1.0, 1.0)
+
+
+def slab_model(phys_shape, nbl, spacing, z_lo, z_hi, velocity_planes, v_max):
+    """m = 1/v^2 and damp on padded planes [z_lo, z_hi) of axis 0 (edge-clamped extension,
+    proj/src/model.cpp:92-100; damping as a sum of the three profiles).  velocity_planes(lo,
+    hi) returns physical planes [lo, hi) of the velocity."""
+    N = [s + 2 * nbl for s in phys_shape]
+    p_lo = min(max(z_lo - nbl, 0), phys_shape[0] - 1)
+    p_hi = min(max(z_hi - 1 - nbl, 0), phys_shape[0] - 1) + 1
+    v = velocity_planes(p_lo, p_hi)
+    idx = np.clip(np.arange(z_lo, z_hi) - nbl, 0, phys_shape[0] - 1) - p_lo
+    v = np.pad(v, ((0, 0), (nbl, nbl), (nbl, nbl)), mode="edge")[idx]
+    m = 1.0 / (v * v)
+    dz, dy, dx = damping_profiles(N, nbl, spacing, v_max)
+    damp = dz[z_lo:z_hi, None, None] + dy[None, :, None] + dx[None, None, :]
+    return m, np.ascontiguousarray(damp)
