@@ -223,6 +223,15 @@ SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, v
  * overwrites next (a receiver cell that straddles the cut reads one).  Acoustic
  * operators; lo / hi are the plans of the slabs below / above, or NULL at an outer face. */
 SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi);
+/* The whole step of a linked slab as ONE update launch plus one point launch on the main
+ * stream: the first d0 chunk sweeps upwards and the last one downwards, so both boundary
+ * plane groups are the first planes computed and their peer stores travel while the rest of
+ * the slab updates; no block spends queue-fill planes on a boundary group of its own (the
+ * split protocol's boundary blocks stream 2K planes for K outputs).  The point launch
+ * mirrors injected boundary nodes and gathers; the plan's two counters / events are then
+ * signalled together.  Same results, bit for bit, as the split protocol and the single
+ * domain.  Follow it with sfb_peer_wait / sfb_peer_wait_ipc as usual. */
+SFB_API int sfb_step_slab_fused(sfb_plan* plan, int op, int64_t t);
 SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour);
 /* The same between processes (one per GPU): sfb_peer_export fills a blob of
  * SFB_PEER_BLOB_BYTES (CUDA IPC handles of the plan's wavefield buffers and of its step

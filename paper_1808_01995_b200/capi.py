@@ -46,7 +46,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_slab_fused", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune", "sfb_debug_stall",
 ]
@@ -76,6 +76,7 @@ lib.sfb_step_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int]
 lib.sfb_step_end.argtypes = [C.c_void_p, C.c_int]
 lib.sfb_step_slab_boundary.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_step_slab_interior.argtypes = [C.c_void_p, C.c_int, C.c_int64]
+lib.sfb_step_slab_fused.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_put_history.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(FieldView)]
 lib.sfb_get_gradient.argtypes = [C.c_void_p, C.POINTER(FieldView)]
 lib.sfb_halo_blocks.argtypes = [C.c_void_p, C.c_int, C.c_int64] + [C.POINTER(C.c_void_p)] * 4 + [C.POINTER(C.c_int64)]
@@ -333,6 +334,9 @@ class Plan:
 
     def step_slab_interior(self, op, t):
         self._chk(lib.sfb_step_slab_interior(self.h, op, t))
+
+    def step_slab_fused(self, op, t):
+        self._chk(lib.sfb_step_slab_fused(self.h, op, t))
 
     def step_end(self, op):
         self._chk(lib.sfb_step_end(self.h, op))

@@ -70,6 +70,12 @@ struct StepParams {
     // group).  A block-uniform offset instead of a second pointer: no per-thread register.
     long long peer_delta0;
     long long peer_delta1;
+    // PUSH kernels: only the first `push_planes` output planes of a block are pushed (the
+    // whole chunk in a boundary launch), and with desc_last the block with the highest
+    // blockIdx.z sweeps its chunk DOWNWARDS, so that a launch over the whole slab produces --
+    // and pushes -- both boundary plane groups first (single-launch slab step)
+    int push_planes;
+    int desc_last;
 };
 
 // the tensor maps of one launch: u[t] with halo box (u) and with plain box (f); u[t-1], r,
@@ -260,7 +266,8 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
                                              const float* cp, int tx, int ty, float4 o4, float4 r4,
                                              float4 d4, const float (&dxy)[4], float dzv,
                                              bool warp_dxy, bool rin, bool lane0,
-                                             uint64_t* done_bar, float* po, long long gc) {
+                                             uint64_t* done_bar, float* po, long long gc,
+                                             bool push_now = false) {
         constexpr int QC = (K + ROT) % (2 * K + 1);  // physical slot of the centre plane
         float acc[4];
         stencil_acc<K, KP, SW, ROT>(p.k, q, cp, tx, ty, acc);
@@ -309,8 +316,11 @@ __device__ __forceinline__ void plane_update(const StepParams& p, const float (&
             // into the neighbour's ghost planes over NVLink.  A separate instantiation: even a
             // never-taken branch here costs the issue-bound kernels 2-3 %.
             if constexpr (PUSH) {
-                const long long peer_delta = blockIdx.z ? p.peer_delta1 : p.peer_delta0;
-                if (peer_delta)
+                // low plane group: block z = 0; high plane group: the last block
+                const long long peer_delta =
+                    blockIdx.z == 0 ? p.peer_delta0
+                                    : (blockIdx.z == gridDim.z - 1 ? p.peer_delta1 : 0);
+                if (peer_delta && push_now)
                     *reinterpret_cast<float4*>(po + peer_delta) =
                         make_float4(un[0], un[1], un[2], un[3]);
             }
@@ -370,6 +380,13 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
     const int zb = p.z_lo + blockIdx.z * p.chunk + (blockIdx.z ? p.z_jump : 0);
     const int ze = min(zb + p.chunk, p.z_hi);
     const int nplanes = (ze - zb) + 2 * K;  // u buffer planes zb .. ze+2K-1 (ghost offset K)
+    // sweep direction (PUSH kernels only): iteration n loads buffer plane zl0 + dir n and,
+    // from n = 2K on, writes owned plane zo0 + dir (n - 2K).  The stencil is symmetric in
+    // d0, so a downward sweep computes the same sums with the two queue halves swapped.
+    const bool desc = PUSH && p.desc_last && gridDim.z > 1 && blockIdx.z == gridDim.z - 1;
+    const int dir = desc ? -1 : 1;
+    const int zl0 = desc ? ze - 1 + 2 * K : zb;
+    const int zo0 = desc ? ze - 1 : zb;
 
     if (tid == 0) {
 #pragma unroll
@@ -389,14 +406,14 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
                 if (n >= NAUX) mbar_wait(done + a, dph);  // iteration n - NAUX is finished
                 const bool out = n >= 2 * K;
                 mbar_arrive_expect_tx(full + s, (S::BOX + (out ? NARR * ABOX : 0)) * 4);
-                tma_load_3d(ring + s * STAGE, &tm.u, x0 - KP, y0 - K, zb + n, full + s);
+                tma_load_3d(ring + s * STAGE, &tm.u, x0 - KP, y0 - K, zl0 + dir * n, full + s);
                 if (out) {
                     // iteration n uses aux stage (n - 2K) % NAUX; 2K % NAUX is folded into a0
                     constexpr int A0 = (NAUX - (2 * K) % NAUX) % NAUX;
                     int as = a + A0;
                     if (as >= NAUX) as -= NAUX;
                     float* ad = aux + as * NARR * ABOX;
-                    const int zo = zb + n - 2 * K;
+                    const int zo = zo0 + dir * (n - 2 * K);
                     tma_load_3d(ad, &tm.o, x0, y0, zo + K, full + s);
                     tma_load_3d(ad + ABOX, &tm.r, x0, y0, zo, full + s);
                     if (!SEP) tma_load_3d(ad + 2 * ABOX, &tm.d, x0, y0, zo, full + s);
@@ -463,13 +480,14 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
     }
 
     // running element offset of this thread's float4 in the output plane
-    long long gc = (long long)zb * p.plane + (long long)y * p.pitch + x;  // compact arrays
+    long long gc = (long long)zo0 * p.plane + (long long)y * p.pitch + x;  // compact arrays
     float* po = p.uo + gc + (long long)K * p.plane;
+    const long long zstep = desc ? -p.plane : p.plane;
     int cs = K % NST;  // stage of the centre plane (plane K is the first centre)
     int as = 0;        // aux stage / done slot of this iteration: (n - 2K) % NAUX ...
     int ds = (2 * K) % NAUX;  // ... and n % NAUX
     float dzn = 0.f;
-    if (SEP) dzn = __ldg(p.dz + zb);
+    if (SEP) dzn = __ldg(p.dz + zo0);
 
     for (int n = 2 * K; n < nplanes; ++n) {
         mbar_wait(full + s, fph);
@@ -490,12 +508,12 @@ acoustic_step_kernel(const __grid_constant__ StepMaps tm, const __grid_constant_
         float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (!SEP) d4 = *reinterpret_cast<const float4*>(ap + 2 * ABOX);
         const float dzv = dzn;
-        if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
+        if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zo0 + dir * (n + 1 - 2 * K)));
 
         plane_update<K, KP, SW, SEP, 0, PUSH>(p, q, ring + cs * STAGE, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
-                                     rin, lane0, done + ds, po, gc);
-        po += p.plane;
-        gc += p.plane;
+                                     rin, lane0, done + ds, po, gc, PUSH && n - 2 * K < p.push_planes);
+        po += zstep;
+        gc += zstep;
         if (++s == NST) {
             s = 0;
             fph ^= 1;
@@ -562,6 +580,11 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
     const int zb = p.z_lo + blockIdx.z * p.chunk + (blockIdx.z ? p.z_jump : 0);
     const int ze = min(zb + p.chunk, p.z_hi);
     const int nplanes = (ze - zb) + 2 * K;
+    // sweep direction (PUSH kernels only), see acoustic_step_kernel
+    const bool desc = PUSH && p.desc_last && gridDim.z > 1 && blockIdx.z == gridDim.z - 1;
+    const int dir = desc ? -1 : 1;
+    const int zl0 = desc ? ze - 1 + 2 * K : zb;
+    const int zo0 = desc ? ze - 1 : zb;
 
     if (tid == 0) {
 #pragma unroll
@@ -583,9 +606,9 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
                 const bool out = n >= 2 * K;
                 float* st = ring + s * STAGE;
                 mbar_arrive_expect_tx(full + s, (ABOX + (out ? S::CBOX + NARR * ABOX : 0)) * 4);
-                tma_load_3d(st, &tm.f, x0, y0, zb + n, full + s);              // newest plane
+                tma_load_3d(st, &tm.f, x0, y0, zl0 + dir * n, full + s);       // newest plane
                 if (out) {
-                    const int zo = zb + n - 2 * K;
+                    const int zo = zo0 + dir * (n - 2 * K);
                     tma_load_3d(st + ABOX, &tm.u, x0 - KP, y0 - K, zo + K, full + s);  // centre
                     float* ad = st + ABOX + CPAD;
                     tma_load_3d(ad, &tm.o, x0, y0, zo + K, full + s);
@@ -627,10 +650,11 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
         for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
 
     const int aown = ty * TX + 4 * tx;
-    long long gc = (long long)zb * p.plane + (long long)y * p.pitch + x;
+    long long gc = (long long)zo0 * p.plane + (long long)y * p.pitch + x;
     float* po = p.uo + gc + (long long)K * p.plane;
+    const long long zstep = desc ? -p.plane : p.plane;
     float dzn = 0.f;
-    if (SEP) dzn = __ldg(p.dz + zb);
+    if (SEP) dzn = __ldg(p.dz + zo0);
     int s = 0;
     uint32_t fph = 0;
 
@@ -665,11 +689,12 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
             float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
             if (!SEP) d4 = *reinterpret_cast<const float4*>(ap + 2 * ABOX);
             const float dzv = dzn;
-            if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zb + n + 1 - 2 * K));
+            if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zo0 + dir * (n + 1 - 2 * K)));
             plane_update<K, KP, SW, SEP, R, PUSH>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
-                                            rin, lane0, done + s, po, gc);
-            po += p.plane;
-            gc += p.plane;
+                                            rin, lane0, done + s, po, gc,
+                                            PUSH && n - 2 * K < p.push_planes);
+            po += zstep;
+            gc += zstep;
         }
         if (++s == NS) {
             s = 0;

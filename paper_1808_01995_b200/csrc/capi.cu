@@ -684,6 +684,29 @@ SFB_API int sfb_step_slab_boundary(sfb_plan* plan, int op, int64_t t) {
     });
 }
 
+SFB_API int sfb_step_slab_fused(sfb_plan* plan, int op, int64_t t) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        static StreamValueFn write_value = stream_value_fn("cuStreamWriteValue32");
+        step_compute(P, op, t, kPartSlabFused);     // pushes both boundary plane groups first
+        step_points(P, op, t, kPartSlabFused);      // every injection (mirrored) + the gather
+        if (P.peer_lo[0] || P.peer_hi[0]) {
+            // one stream: the pushes have landed AND the ghost-plane readers are done
+            SFB_CUDA(cudaEventRecord(P.ev_push, P.s_main));
+            SFB_CUDA(cudaEventRecord(P.ev_done, P.s_main));
+            if (P.ipc_flag[0] || P.ipc_flag[1]) {
+                const CUdeviceptr f = reinterpret_cast<CUdeviceptr>(P.push_flag.p);
+                CUresult rc = write_value(P.s_main, f, ++P.push_count, 0);
+                if (rc == CUDA_SUCCESS) rc = write_value(P.s_main, f + 4, ++P.done_count, 0);
+                if (rc != CUDA_SUCCESS)
+                    throw Failure(SFB_ERR_CUDA, "cuStreamWriteValue32 failed with code " +
+                                                    std::to_string(int(rc)));
+            }
+        }
+    });
+}
+
 SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
@@ -805,10 +828,11 @@ SFB_API int sfb_peer_wait_ipc(sfb_plan* plan) {
             wait(P.s_main, f, P.push_count);
             if (P.s_bnd != P.s_main) wait(P.s_bnd, f, P.push_count);
             // (2) they have finished READING their own ghost planes of the level this plan's
-            // next boundary half-step overwrites (their last reader is the gather of the
-            // interior half-step, on their main stream): only the boundary stream stores
-            // into peer memory
+            // next step overwrites (their last reader is the gather of the interior
+            // half-step, on their main stream).  The split protocol stores into peer memory
+            // from the boundary stream, the single-launch step from the main stream.
             wait(P.s_bnd, f + 4, P.done_count);
+            if (P.s_bnd != P.s_main) wait(P.s_main, f + 4, P.done_count);
         }
     });
 }
@@ -821,8 +845,11 @@ SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour) {
         if (plan->s_bnd != plan->s_main)
             SFB_CUDA(cudaStreamWaitEvent(plan->s_bnd, neighbour->ev_push, 0));
         // (2) the neighbour's gather has finished reading the ghost planes this plan's next
-        // boundary half-step overwrites
+        // step overwrites (from the boundary stream in the split protocol, from the main
+        // stream in the single-launch step)
         SFB_CUDA(cudaStreamWaitEvent(plan->s_bnd, neighbour->ev_done, 0));
+        if (plan->s_bnd != plan->s_main)
+            SFB_CUDA(cudaStreamWaitEvent(plan->s_main, neighbour->ev_done, 0));
     });
 }
 

@@ -101,6 +101,10 @@ struct OpRoles {
 
 OpRoles roles(int op);
 constexpr int kPartBoundaryPair = 100;   // internal: LOW and HIGH plane groups in one launch
+// internal: the whole slab in ONE push launch -- chunk 0 sweeps up, the last chunk sweeps down,
+// so both boundary plane groups are computed and pushed first (sfb_step_slab_fused)
+constexpr int kPartSlabFused = 101;
+int fused_chunk(const Plan& P);
 
 // explicit fused outputs / buffer set of one step (checkpointed runs); without it the
 // save_every rules of the plain runs apply

@@ -70,6 +70,38 @@ void part_range(const Plan& P, int part, int& lo, int& hi) {
     }
 }
 
+// d0 chunk of the single-launch slab step: at least two chunks (the first sweeps up, the last
+// down), whole waves of the resident blocks, every chunk charged half a plane per queue-fill
+// plane like select_variant does
+int fused_chunk(const Plan& P) {
+    const StepVariant& v = *P.variant;
+    const void* fn = v.func_push ? v.func_push : v.func;
+    int bps = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, v.nthreads, v.smem) != cudaSuccess || bps < 1)
+        bps = 1;
+    const long long tiles = ((P.N[2] + v.tile_x - 1) / v.tile_x) * ((P.N[1] + v.tile_y - 1) / v.tile_y);
+    const long long slots = (long long)P.sm_count * bps;
+    int best = 2;
+    double best_score = -1;
+    const int max_nch = std::max(2, P.n0 / std::max(1, 2 * P.K));
+    for (int nch = 2; nch <= max_nch; ++nch) {
+        const int chunk = (P.n0 + nch - 1) / nch;
+        if (chunk < P.K) break;
+        const int real = (P.n0 + chunk - 1) / chunk;
+        if (real < 2) continue;
+        const long long total = tiles * real;
+        const long long waves = (total + slots - 1) / slots;
+        const double fill = double(total) / double(waves * slots);
+        const double score = fill / (1.0 + (2.0 * P.K / chunk) * 0.5);
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best = real;
+        }
+        if (total > 16 * slots) break;
+    }
+    return (P.n0 + best - 1) / best;
+}
+
 cudaStream_t part_stream(Plan& P, int part) {
     const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartBoundaryPair;
     cudaStream_t st = bnd ? P.s_bnd : P.s_main;
@@ -88,7 +120,7 @@ cudaStream_t part_stream(Plan& P, int part) {
 void mark_stream(Plan& P, int part) {
     // whole-domain launches have no other stream to order against, and an event record
     // between two kernels would break their programmatic dependent launch
-    if (part == SFB_PART_ALL) return;
+    if (part == SFB_PART_ALL || part == kPartSlabFused) return;
     const bool bnd = part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartBoundaryPair;
     if (P.s_bnd == P.s_main) return;
     if (bnd) {
@@ -117,7 +149,9 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;
     const bool pair = part == kPartBoundaryPair;   // needs n0 >= 2K (split_slabs guarantees it)
-    if (pair) {
+    const bool fused = part == kPartSlabFused;
+    if (pair || fused) {
+        require(P.n0 >= 2 * P.K, SFB_ERR_PARAMETER, "slab thinner than two halo widths");
         lo = 0;
         hi = P.n0;
     } else {
@@ -139,15 +173,18 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
     sp.z_lo = lo;
     sp.z_hi = hi;
     sp.chunk = pair ? P.K
-                    : (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? P.chunk : (hi - lo);
+               : fused ? fused_chunk(P)
+               : (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? P.chunk : (hi - lo);
     sp.z_jump = pair ? P.n0 - 2 * P.K : 0;   // block z = 1 starts at plane n0 - K
+    sp.push_planes = fused ? P.K : sp.chunk;   // boundary launches push all they compute
+    sp.desc_last = fused ? 1 : 0;
     // linked slabs: the boundary plane groups are also written into the neighbours' ghosts
     if (!(ex && ex->alt)) {
         // mirror of owned plane z: low group -> peer_lo + z planes, high group -> peer_hi +
         // (z - (n0 - K)) planes; owned plane z itself sits at uo + (z + K) planes
         const long long d_lo = P.peer_lo[oth] ? P.peer_lo[oth] - (sp.uo + (long long)P.K * P.plane) : 0;
         const long long d_hi = P.peer_hi[oth] ? P.peer_hi[oth] - (sp.uo + (long long)P.n0 * P.plane) : 0;
-        if (pair) {
+        if (pair || fused) {
             sp.peer_delta0 = d_lo;
             sp.peer_delta1 = d_hi;
         } else if (part == SFB_PART_LOW) {
@@ -180,7 +217,7 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
     maps.o = alt ? P.tm_fo[oth] : P.tm_o[oth];
     maps.r = P.tm_r;
     maps.d = P.sep ? P.tm_r : P.tm_d;
-    if (sp.peer_delta0 || sp.peer_delta1) {
+    if (sp.peer_delta0 || sp.peer_delta1 || fused) {
         require(v.launch_push != nullptr, SFB_ERR_CAPABILITY,
                 "the selected tile shape has no halo-push kernel (sfb_link_peers picks one that has)");
         SFB_CUDA(v.launch_push(maps, sp, grid, st));
@@ -189,7 +226,7 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
     }
     ++P.launches;
     mark_stream(P, part);
-    if (!alt && (part == SFB_PART_ALL || part == SFB_PART_INTERIOR)) {
+    if (!alt && (part == SFB_PART_ALL || part == SFB_PART_INTERIOR || fused)) {
         P.live_level[cur] = t;
         P.live_level[oth] = tnew;
     }
@@ -211,7 +248,7 @@ void step_points(Plan& P, int op, long long t, int part, float* target_override,
     Range rg[2] = {{0, 0}, {0, 0}};
     int nr = 1;
     bool gather = false;
-    if (part == SFB_PART_ALL) {
+    if (part == SFB_PART_ALL || part == kPartSlabFused) {
         rg[0] = {0, ci.ncell};
         gather = ro.smp >= 0 && allow_gather;
     } else if (part == SFB_PART_LOW || part == SFB_PART_HIGH) {
@@ -238,7 +275,8 @@ void step_points(Plan& P, int op, long long t, int part, float* target_override,
         pp.target = target_override ? target_override : P.u[oth].as<float>();
         pp.r = P.r.as<float>();
         pp.inv_dt2 = P.coef.inv_dt2;
-        if (!target_override && (part == SFB_PART_LOW || part == SFB_PART_HIGH)) {
+        if (!target_override &&
+            (part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartSlabFused)) {
             pp.peer_lo = P.peer_lo[oth];
             pp.peer_hi = P.peer_hi[oth];
             pp.plane = P.plane;

@@ -275,10 +275,9 @@ ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model,
     const auto t0 = std::chrono::steady_clock::now();
     for (long s = 0; s < w.nt - 2; ++s) {
         const long t = w.adjoint ? w.nt - 2 - s : 1 + s;
-        for (auto& e : eng) {
-            e->check(sfb_step_slab_boundary(e->plan(), op, t));
-            e->check(sfb_step_slab_interior(e->plan(), op, t));
-        }
+        // one update launch per slab and step: both boundary plane groups are computed and
+        // pushed first (the first chunk sweeps up, the last one down), the rest follows
+        for (auto& e : eng) e->check(sfb_step_slab_fused(e->plan(), op, t));
         for (long i = 0; i < nslab; ++i) {
             Engine& e = *eng[std::size_t(i)];
             if (i > 0) e.check(sfb_peer_wait(e.plan(), eng[std::size_t(i - 1)]->plan()));

@@ -269,10 +269,18 @@ class PeerPushDriver:
                                    ", ".join(f"{i}: {e}" for i, e in enumerate(errs) if e))
 
     def run(self, t_from: int, t_to: int, backward=False):
+        """One update launch + one point launch per step (sfb_step_slab_fused: the first d0
+        chunk sweeps up, the last one down, so both boundary plane groups are computed and
+        pushed first); SFB_SLAB_PROTOCOL=split runs the boundary / interior half-steps on two
+        streams instead (the protocol the NCCL fallback uses)."""
         steps = range(t_to - 1, t_from - 1, -1) if backward else range(t_from, t_to)
+        split = os.environ.get("SFB_SLAB_PROTOCOL", "fused") == "split"
         for t in steps:
-            self.plan.step_slab_boundary(self.op, t)
-            self.plan.step_slab_interior(self.op, t)
+            if split:
+                self.plan.step_slab_boundary(self.op, t)
+                self.plan.step_slab_interior(self.op, t)
+            else:
+                self.plan.step_slab_fused(self.op, t)
             self.plan.peer_wait_ipc()
 
 

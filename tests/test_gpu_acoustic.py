@@ -256,7 +256,7 @@ def test_unstable_dt_and_nan_guard():
 
 
 def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_forward=False,
-               fused=False, pushed=False, stall=None):
+               fused=False, pushed=False, stall=None, single_launch=False):
     """N plans on one device stepping in lockstep with device-to-device ghost copies:
     the single-GPU emulation of the multi-GPU slab protocol.  Returns the summed sampled
     traces, the assembled last level and (gradient) the assembled grad."""
@@ -276,6 +276,11 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
         for t in ts:
             if pushed:   # no copies and no host synchronisation: events order the slabs
                 for i, p in enumerate(plans):
+                    if single_launch:   # sfb_step_slab_fused: one update launch per step
+                        if stall and i == stall[0]:
+                            p.debug_stall(0, stall[1])
+                        p.step_slab_fused(o, t)
+                        continue
                     p.step_slab_boundary(o, t)
                     if stall and i == stall[0]:   # hold this slab's main stream back
                         p.debug_stall(0, stall[1])
@@ -327,9 +332,10 @@ def _run_slabs(model, geom, order, cuts, op=None, save_every=0, inj=None, prior_
     return rec, u, grad
 
 
+@pytest.mark.parametrize("single_launch", [False, True])
 @pytest.mark.parametrize("order,shape,nslab", [(8, [48, 30, 34], 3), (16, [64, 30, 34], 2),
-                                               (12, [64, 30, 34], 2)])
-def test_fused_halo_push_matches_single_domain_bitwise(order, shape, nslab):
+                                               (12, [64, 30, 34], 2), (4, [70, 30, 34], 3)])
+def test_fused_halo_push_matches_single_domain_bitwise(order, shape, nslab, single_launch):
     """sfb_link_peers: the boundary kernels store their planes (and the point kernel its
     injected nodes) directly into the neighbours' ghost planes; slabs are ordered by events
     only.  Forward, adjoint and gradient equal the single-domain run bit for bit (ring
@@ -349,17 +355,19 @@ def test_fused_halo_push_matches_single_domain_bitwise(order, shape, nslab):
     n0 = model.N[0]
     src_plane = int(geom.src_base[0][0])
     cuts = [0, 20, src_plane + 1, n0] if nslab == 3 else [0, src_plane + 1, n0]   # source on a cut
-    rec3, u3, _ = _run_slabs(model, geom, order, cuts, pushed=True)
+    sl = dict(pushed=True, single_launch=single_launch)
+    rec3, u3, _ = _run_slabs(model, geom, order, cuts, **sl)
     assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
-    srca3, v3, _ = _run_slabs(model, geom, order, cuts, op=capi.OP_ADJOINT, inj=data, pushed=True)
+    srca3, v3, _ = _run_slabs(model, geom, order, cuts, op=capi.OP_ADJOINT, inj=data, **sl)
     assert np.array_equal(srca3, srca1) and np.array_equal(v3, v1)
     _, _, g3 = _run_slabs(model, geom, order, cuts, op=capi.OP_GRADIENT, save_every=2, inj=data,
-                          prior_forward=True, pushed=True)
+                          prior_forward=True, **sl)
     assert np.abs(g1).max() > 0 and np.array_equal(g3, g1)
 
 
+@pytest.mark.parametrize("single_launch", [False, True])
 @pytest.mark.parametrize("slow_slab", [0, 1])
-def test_fused_halo_push_waits_for_the_ghost_plane_readers(slow_slab):
+def test_fused_halo_push_waits_for_the_ghost_plane_readers(slow_slab, single_launch):
     """A receiver cell that straddles a slab cut is gathered by the slab below, which reads
     its high ghost plane in the interior half-step.  The neighbour's next boundary half-step
     overwrites that plane, so it must wait for the gather, not only for the boundary
@@ -377,7 +385,8 @@ def test_fused_halo_push_waits_for_the_ghost_plane_readers(slow_slab):
     u1 = plan.wavefield(geom.nt - 1)
     plan.close()
     assert np.abs(rec1).min(axis=0).max() >= 0 and (np.abs(rec1).max(axis=0) > 0).all()
-    rec3, u3, _ = _run_slabs(model, geom, 8, cuts, pushed=True, stall=(slow_slab, 300))
+    rec3, u3, _ = _run_slabs(model, geom, 8, cuts, pushed=True, stall=(slow_slab, 300),
+                             single_launch=single_launch)
     assert np.array_equal(rec3, rec1) and np.array_equal(u3, u1)
     # the adjoint samples at the source cell: put it across the first cut as well
     src = [[(cuts[1] - 1 - nbl + 0.37) * h, 0.5 * (shape[1] - 1) * h, 2.13 * h]]
@@ -387,7 +396,7 @@ def test_fused_halo_push_waits_for_the_ghost_plane_readers(slow_slab):
     srca1, _ = plan.adjoint(data)
     plan.close()
     srca3, _, _ = _run_slabs(model, geom, 8, cuts, op=capi.OP_ADJOINT, inj=data, pushed=True,
-                             stall=(slow_slab, 300))
+                             stall=(slow_slab, 300), single_launch=single_launch)
     assert np.abs(srca1).max() > 0 and np.array_equal(srca3, srca1)
 
 

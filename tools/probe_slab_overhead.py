@@ -53,6 +53,9 @@ def parts(t):
     plan.step_slab_boundary(F, t)
     plan.step_slab_interior(F, t)
 
+def fused(t):
+    plan.step_slab_fused(F, t)
+
 def only_boundary(t):
     plan.step_slab_boundary(F, t)
 
@@ -72,11 +75,13 @@ def neighbour(lo, hi):
 below, above = neighbour(0, n0_slab), neighbour(2 * n0_slab, 3 * n0_slab)
 plan.link_peers(below, above)
 c = timed(parts)
+d = timed(fused)      # single-launch slab step: first chunk up, last chunk down, pushes first
 plan.link_peers(None, None)
 below.close(); above.close()
 K = order // 2
 print(json.dumps({"slab": [n0_slab, n, n], "order": order, "tile": plan.get_tile(),
                   "whole_ms": a * 1e3, "parts_ms": b * 1e3, "whole_gpts": pts / a / 1e9,
                   "parts_gpts": pts / b / 1e9, "protocol_efficiency": a / b, "boundary_alone_ms": bnd_only * 1e3, "interior_alone_ms": int_only * 1e3, "pushed_ms": c * 1e3, "pushed_efficiency": a / c,
+                  "single_launch_pushed_ms": d * 1e3, "single_launch_efficiency": a / d,
                   "halo_mb_per_neighbour": K * n * n * 4 / 1e6}))
 plan.close()
