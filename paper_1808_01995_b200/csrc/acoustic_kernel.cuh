@@ -196,11 +196,13 @@ __device__ __forceinline__ float2 f2_splat(float v) { return make_float2(v, v); 
 // The register queue is addressed through a compile-time rotation ROT: logical plane i of
 // the queue lives in q[(i + ROT) % (2K+1)].  Kernels that shift the queue every iteration
 // use ROT = 0; the unrolled-rotation kernels advance ROT instead of moving registers.
-template <int K, int KP, int SW, int ROT = 0>
-__device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&q)[2 * K + 1][4],
+// A queue array with more than 2K+1 slots is a sliding window instead: logical plane i lives
+// in q[i + ROT] (the unrolled-by-two kernels, which shift by two planes every second plane).
+template <int K, int KP, int SW, int ROT = 0, int QN = 2 * K + 1>
+__device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&q)[QN][4],
                                             const float* cp, int tx, int ty, float (&acc)[4]) {
         constexpr int Q = 2 * K + 1;
-#define SFB_Q(i) q[((i) + ROT) % Q]
+#define SFB_Q(i) q[QN == Q ? ((i) + ROT) % Q : (i) + ROT]
         // centre and streaming-axis neighbours from the register queue, two nodes per op
         float2 a01 = f2_mul(f2_splat(k.c0), make_float2(SFB_Q(K)[0], SFB_Q(K)[1]));
         float2 a23 = f2_mul(f2_splat(k.c0), make_float2(SFB_Q(K)[2], SFB_Q(K)[3]));
@@ -224,9 +226,11 @@ __device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&
                 a23 = f2_fma(w, f2_add(make_float2(lo.z, lo.w), make_float2(hi.z, hi.w)), a23);
             }
         }
-        // contiguous-axis neighbours: one aligned row segment; the shifted operands are not
-        // register-aligned pairs, so this part stays scalar
-        float ax[4] = {0.f, 0.f, 0.f, 0.f};
+        // contiguous-axis neighbours: one aligned row segment.  For even j the operand pairs
+        // (xr[KP+c-j], xr[KP+c+1-j]), c = 0, 2, are register-aligned pairs of the loaded
+        // float4s and run packed; for odd j they straddle two pairs and stay scalar.  Each
+        // node still accumulates j = 1 .. K in order with the same roundings.
+        float2 x01 = make_float2(0.f, 0.f), x23 = make_float2(0.f, 0.f);
         {
             float xr[2 * KP + 4];
             const float* rowp = cp + (ty + K) * SW + 4 * tx;
@@ -244,13 +248,23 @@ __device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&
                 }
             }
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-#pragma unroll
-                for (int j = 1; j <= K; ++j)
-                    ax[c] = fmaf(k.cx[j - 1], xr[KP + c - j] + xr[KP + c + j], ax[c]);
+            for (int j = 1; j <= K; ++j) {
+                if (j % 2 == 0) {
+                    const float2 w = f2_splat(k.cx[j - 1]);
+                    x01 = f2_fma(w, f2_add(make_float2(xr[KP - j], xr[KP + 1 - j]),
+                                           make_float2(xr[KP + j], xr[KP + 1 + j])), x01);
+                    x23 = f2_fma(w, f2_add(make_float2(xr[KP + 2 - j], xr[KP + 3 - j]),
+                                           make_float2(xr[KP + 2 + j], xr[KP + 3 + j])), x23);
+                } else {
+                    x01.x = fmaf(k.cx[j - 1], xr[KP - j] + xr[KP + j], x01.x);
+                    x01.y = fmaf(k.cx[j - 1], xr[KP + 1 - j] + xr[KP + 1 + j], x01.y);
+                    x23.x = fmaf(k.cx[j - 1], xr[KP + 2 - j] + xr[KP + 2 + j], x23.x);
+                    x23.y = fmaf(k.cx[j - 1], xr[KP + 3 - j] + xr[KP + 3 + j], x23.y);
+                }
+            }
         }
-        a01 = f2_add(a01, make_float2(ax[0], ax[1]));
-        a23 = f2_add(a23, make_float2(ax[2], ax[3]));
+        a01 = f2_add(a01, x01);
+        a23 = f2_add(a23, x23);
         acc[0] = a01.x;
         acc[1] = a01.y;
         acc[2] = a23.x;
@@ -261,16 +275,17 @@ __device__ __forceinline__ void stencil_acc(const StencilCoef& k, const float (&
 // One output plane for the four nodes of a thread: stencil from the register queue (d0)
 // and the centre plane in shared memory `cp` (d1, d2), then -- after telling the producer
 // that this iteration's shared-memory reads are over -- damping, leapfrog and the stores.
-template <int K, int KP, int SW, bool SEP, int ROT = 0, bool PUSH = false>
-__device__ __forceinline__ void plane_update(const StepParams& p, const float (&q)[2 * K + 1][4],
+template <int K, int KP, int SW, bool SEP, int ROT = 0, bool PUSH = false, int QN = 2 * K + 1>
+__device__ __forceinline__ void plane_update(const StepParams& p, const float (&q)[QN][4],
                                              const float* cp, int tx, int ty, float4 o4, float4 r4,
                                              float4 d4, const float (&dxy)[4], float dzv,
                                              bool warp_dxy, bool rin, bool lane0,
                                              uint64_t* done_bar, float* po, long long gc,
                                              bool push_now = false) {
-        constexpr int QC = (K + ROT) % (2 * K + 1);  // physical slot of the centre plane
+        // physical slot of the centre plane
+        constexpr int QC = QN == 2 * K + 1 ? (K + ROT) % (2 * K + 1) : K + ROT;
         float acc[4];
-        stencil_acc<K, KP, SW, ROT>(p.k, q, cp, tx, ty, acc);
+        stencil_acc<K, KP, SW, ROT, QN>(p.k, q, cp, tx, ty, acc);
 
         const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
         const float ov[4] = {o4.x, o4.y, o4.z, o4.w};
@@ -560,12 +575,19 @@ __device__ __forceinline__ void rotate_run(F& f, int& n, int nplanes) {
     }
 }
 
-template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROTATE, bool PUSH = false>
+// SLIDE: the queue is a window of 2K+2 slots; the plane loop is unrolled by two (plane n uses
+// slots [0, 2K], plane n+1 slots [1, 2K+1]) and the window moves by two slots afterwards:
+// half the register moves per plane of the plain shifting queue, two copies of the loop body
+// instead of the 2K+1 of ROTATE.
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool ROTATE, bool PUSH = false,
+          bool SLIDE = false>
 __global__ void __launch_bounds__(DualShape<K, TXV, TY, NS, SEP>::NTHREADS, MINB)
 acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
                           const __grid_constant__ StepParams p) {
     using S = DualShape<K, TXV, TY, NS, SEP>;
+    static_assert(!(ROTATE && SLIDE), "one queue scheme at a time");
     constexpr int KP = S::KP, SW = S::SW, STAGE = S::STAGE, Q = 2 * K + 1;
+    constexpr int QN = SLIDE ? Q + 1 : Q;
     constexpr int NARR = S::NARR, ABOX = S::ABOX, CPAD = S::CPAD, TX = S::TX;
     constexpr int NCW = S::NCONS / 32;
 
@@ -643,9 +665,9 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
         warp_dxy = __any_sync(0xffffffffu, (dxy[0] + dxy[1]) + (dxy[2] + dxy[3]) != 0.f);
     }
 
-    float q[Q][4];
+    float q[QN][4];
 #pragma unroll
-    for (int j = 0; j < Q; ++j)
+    for (int j = 0; j < QN; ++j)
 #pragma unroll
         for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
 
@@ -664,16 +686,16 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
         constexpr int R = decltype(rot)::value;
         mbar_wait(full + s, fph);
         const float* st = ring + s * STAGE;
+        // logical slot Q-1 (newest) under the rotation / window offset of this iteration
+        constexpr int NEW = SLIDE ? Q - 1 + R : (Q - 1 + R) % Q;
         {
             const float4 v = *reinterpret_cast<const float4*>(st + aown);
-            if constexpr (!ROTATE) {
+            if constexpr (!ROTATE && !SLIDE) {
 #pragma unroll
                 for (int j = 0; j < Q - 1; ++j)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
             }
-            // logical slot Q-1 (newest) under the rotation of this iteration
-            constexpr int NEW = (Q - 1 + R) % Q;
             q[NEW][0] = v.x;
             q[NEW][1] = v.y;
             q[NEW][2] = v.z;
@@ -681,7 +703,7 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
         }
         if (n < 2 * K) {
             __syncwarp();
-            if (lane0) mbar_release(done + s, q[(Q - 1 + R) % Q][0]);
+            if (lane0) mbar_release(done + s, q[NEW][0]);
         } else {
             const float* ap = st + ABOX + CPAD + aown;
             const float4 o4 = *reinterpret_cast<const float4*>(ap);
@@ -690,9 +712,9 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
             if (!SEP) d4 = *reinterpret_cast<const float4*>(ap + 2 * ABOX);
             const float dzv = dzn;
             if (SEP && n + 1 < nplanes) dzn = __ldg(p.dz + (zo0 + dir * (n + 1 - 2 * K)));
-            plane_update<K, KP, SW, SEP, R, PUSH>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv, warp_dxy,
-                                            rin, lane0, done + s, po, gc,
-                                            PUSH && n - 2 * K < p.push_planes);
+            plane_update<K, KP, SW, SEP, R, PUSH, QN>(p, q, st + ABOX, tx, ty, o4, r4, d4, dxy, dzv,
+                                                warp_dxy, rin, lane0, done + s, po, gc,
+                                                PUSH && n - 2 * K < p.push_planes);
             po += zstep;
             gc += zstep;
         }
@@ -708,6 +730,15 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
         while (n < nplanes) {
             auto step = [&](auto r) { iteration(std::integral_constant<int, (decltype(r)::value + 1) % Q>{}, n); };
             rotate_run<Q, 0>(step, n, nplanes);
+        }
+    } else if constexpr (SLIDE) {
+        for (int n = 0; n < nplanes; n += 2) {
+            iteration(std::integral_constant<int, 0>{}, n);
+            if (n + 1 < nplanes) iteration(std::integral_constant<int, 1>{}, n + 1);
+#pragma unroll
+            for (int j = 0; j < Q - 1; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 2][c];
         }
     } else {
         for (int n = 0; n < nplanes; ++n) iteration(std::integral_constant<int, 0>{}, n);

@@ -309,8 +309,7 @@ void bind_model(Plan& P, const sfb_field_view* m, const sfb_field_view* damp, do
     // the slab's own centre plane otherwise
     detect_separable_damping(P, dv, tmp, slab_local ? P.z_lo + P.n0 / 2 : P.N[0] / 2);
     if (P.sep) P.damp.release();
-    select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST,
-                   int(P.variant->dual) + int(P.variant->rotate));
+    select_variant(P, P.variant->TXV, P.variant->TY, P.variant->NST, variant_kind(*P.variant));
     P.model_set = true;
     P.history_valid = false;
 }
@@ -963,7 +962,7 @@ SFB_API int sfb_autotune(sfb_plan* plan, int steps) {
         float best_ms = 0.f;
         for (const StepVariant& v : step_variant_registry()) {
             if (v.K != P.K || v.sep != P.sep) continue;
-            select_variant(P, v.TXV, v.TY, v.NST, int(v.dual) + int(v.rotate));
+            select_variant(P, v.TXV, v.TY, v.NST, variant_kind(v));
             SFB_CUDA(cudaMemsetAsync(P.u[0].p, 0, size_t(P.ucount) * 4, P.s_main));
             SFB_CUDA(cudaMemsetAsync(P.u[1].p, 0, size_t(P.ucount) * 4, P.s_main));
             P.save_every = 0;
@@ -981,7 +980,7 @@ SFB_API int sfb_autotune(sfb_plan* plan, int steps) {
             }
         }
         require(best != nullptr, SFB_ERR_CAPABILITY, "no kernel image for this space order");
-        select_variant(P, best->TXV, best->TY, best->NST, int(best->dual) + int(best->rotate));
+        select_variant(P, best->TXV, best->TY, best->NST, variant_kind(*best));
         P.history_valid = false;
         P.live_level[0] = P.live_level[1] = -1;
     });
@@ -1003,9 +1002,11 @@ SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk)
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
         // stages < 0 selects the dual-stream kernel with |stages| stages; |stages| > 100 its
-        // rotated-queue variant with |stages| - 100 stages
+        // rotated-queue variant with |stages| - 100 stages; |stages| > 200 the 2 x 2 patch
+        // variant with |stages| - 200 stages; |stages| > 300 the sliding-window variant
         const int a = stages < 0 ? -stages : stages;
-        select_variant(*plan, txv, ty, a > 100 ? a - 100 : a, stages < 0 ? (a > 100 ? 2 : 1) : 0);
+        select_variant(*plan, txv, ty, a % 100,
+                       stages < 0 ? (a > 300 ? 4 : (a > 200 ? 3 : (a > 100 ? 2 : 1))) : 0);
         if (chunk > 0) plan->chunk = std::min(chunk, plan->n0);
     });
 }
@@ -1015,7 +1016,9 @@ SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* nst, int* chunk
     if (txv) *txv = plan->variant->TXV;
     if (ty) *ty = plan->variant->TY;
     if (nst)
-        *nst = plan->variant->dual ? -(plan->variant->NST + (plan->variant->rotate ? 100 : 0))
+        *nst = plan->variant->dual ? -(plan->variant->NST + (plan->variant->slide ? 300
+                                                             : plan->variant->patch ? 200
+                                                             : plan->variant->rotate ? 100 : 0))
                                    : plan->variant->NST;
     if (chunk) *chunk = plan->chunk;
     if (sep) *sep = plan->variant->sep ? 1 : 0;

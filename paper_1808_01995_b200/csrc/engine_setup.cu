@@ -68,20 +68,24 @@ void make_tensor_maps(Plan& P) {
 
 // ---- tile shape / chunk choice ----------------------------------------------------------
 
-// dual: -1 any, 0 ring kernel, 1 dual-stream, 2 dual-stream with the rotated (unrolled) queue
+// dual: -1 any, 0 ring kernel, 1 dual-stream, 2 dual-stream with the rotated (unrolled) queue,
+// 3 dual-stream with 2 x 2 patches per thread, 4 dual-stream with the sliding queue window
 void select_variant(Plan& P, int txv, int ty, int nst, int dual) {
     const StepVariant* best = nullptr;
     for (const StepVariant& v : step_variant_registry()) {
         if (v.K != P.K || v.sep != P.sep) continue;
-        if (dual >= 0 && (int(v.dual) + int(v.rotate)) != dual) continue;
+        if (dual >= 0 && variant_kind(v) != dual) continue;
         if (txv > 0 && (v.TXV != txv || v.TY != ty || (nst > 0 && v.NST != nst))) continue;
         if (txv <= 0) {
             // default shape (measured on B200, tools/probe_tiles.py): the ring kernel up to
-            // order 8, the dual-stream kernel (4 stages) above; 64 x 16 tiles, 64 x 14 from
-            // order 14 up
+            // order 8, the dual-stream kernel (4 stages) above -- with the sliding queue
+            // window from order 12 up; 64 x 16 tiles, 64 x 14 from order 14 up
             const bool want_dual = P.K >= 5;
+            const bool want_slide = P.K >= 6;
             const int want_ty = P.K >= 7 ? 14 : 16;
-            if (v.dual != want_dual || v.rotate || v.TXV != 16 || v.TY != want_ty) continue;
+            if (v.dual != want_dual || v.rotate || v.patch || v.slide != want_slide || v.TXV != 16 ||
+                v.TY != want_ty)
+                continue;
             if (v.NST != (want_dual ? 4 : P.K + 3)) continue;
         }
         if (!best) best = &v;

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "acoustic_kernel.cuh"
+#include "acoustic_patch_kernel.cuh"
 #include "launch.hpp"
 
 namespace sfb {
@@ -17,6 +18,8 @@ struct StepVariant {
     bool sep;
     bool dual;            // dual-stream kernel (u[t] fetched as feed + centre boxes)
     bool rotate;          // dual-stream kernel unrolled by 2K+1 (queue rotation, no moves)
+    bool patch = false;   // dual-stream kernel with 2 x 2 patches per thread (acoustic_patch_kernel.cuh)
+    bool slide = false;   // dual-stream kernel with the sliding queue window (unrolled by two)
     int tile_x, tile_y;   // output tile (d2, d1)
     int box_w, box_h;     // TMA box of u[t] (d2, d1)
     int halo_x;           // KP
@@ -30,6 +33,12 @@ struct StepVariant {
 };
 
 std::vector<StepVariant>& step_variant_registry();
+
+// kernel family of a variant: 0 ring, 1 dual-stream, 2 dual-stream with rotated queue, 3 patch,
+// 4 dual-stream with the sliding queue window
+inline int variant_kind(const StepVariant& v) {
+    return v.slide ? 4 : v.patch ? 3 : int(v.dual) + int(v.rotate);
+}
 
 template <int K, int TXV, int TY, int NST, bool SEP, bool PUSH = false>
 cudaError_t launch_step(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
@@ -84,6 +93,56 @@ void register_dual() {
     }
 }
 
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB, bool PUSH = false>
+cudaError_t launch_slide(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
+    using S = DualShape<K, TXV, TY, NS, SEP>;
+    return launch_pdl(&acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, false, PUSH, true>, grid,
+                      S::NTHREADS, S::SMEM, st, tm, p);
+}
+
+template <int K, int TXV, int TY, int NS, bool SEP, int MINB>
+void register_slide() {
+    using S = DualShape<K, TXV, TY, NS, SEP>;
+    if constexpr (S::SMEM * MINB <= 227 * 1024) {
+        StepVariant v;
+        v.K = K; v.TXV = TXV; v.TY = TY; v.NST = NS; v.sep = SEP; v.dual = true; v.rotate = false;
+        v.slide = true;
+        v.tile_x = S::TX; v.tile_y = TY; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
+        v.nthreads = S::NTHREADS; v.smem = S::SMEM;
+        v.func = reinterpret_cast<const void*>(
+            &acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, false, false, true>);
+        v.launch = &launch_slide<K, TXV, TY, NS, SEP, MINB>;
+        v.func_push = reinterpret_cast<const void*>(
+            &acoustic_step_dual_kernel<K, TXV, TY, NS, SEP, MINB, false, true, true>);
+        v.launch_push = &launch_slide<K, TXV, TY, NS, SEP, MINB, true>;
+        step_variant_registry().push_back(v);
+    }
+}
+
+template <int K, int NS, bool SEP, int MINB, bool PUSH = false>
+cudaError_t launch_patch(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
+    using S = PatchShape<K, NS, SEP>;
+    return launch_pdl(&acoustic_step_patch_kernel<K, NS, SEP, MINB, PUSH>, grid, S::NTHREADS,
+                      S::SMEM, st, tm, p);
+}
+
+template <int K, int NS, bool SEP, int MINB>
+void register_patch() {
+    using S = PatchShape<K, NS, SEP>;
+    if constexpr (S::SMEM * MINB <= 227 * 1024) {
+        StepVariant v;
+        v.K = K; v.TXV = 16; v.TY = 14; v.NST = NS; v.sep = SEP; v.dual = true; v.rotate = false;
+        v.patch = true;
+        v.tile_x = S::TX; v.tile_y = 14; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
+        v.nthreads = S::NTHREADS; v.smem = S::SMEM;
+        v.func = reinterpret_cast<const void*>(&acoustic_step_patch_kernel<K, NS, SEP, MINB>);
+        v.launch = &launch_patch<K, NS, SEP, MINB>;
+        v.func_push = reinterpret_cast<const void*>(&acoustic_step_patch_kernel<K, NS, SEP, MINB, true>);
+        v.launch_push = &launch_patch<K, NS, SEP, MINB, true>;
+        step_variant_registry().push_back(v);
+    }
+}
+
 template <int K, int TXV, int TY, int NST>
 void register_pair() {
     register_step<K, TXV, TY, NST, false>();
@@ -121,6 +180,17 @@ void register_all_for_K() {
     // is allocated in units of 4 warps); pays from order 14 up (order 16: +11 %)
     if constexpr (K >= 7) register_dual_pair<K, 16, 14, 4>();
     register_dual_pair<K, 32, 8, 3>();
+    // 2 x 2 patches per thread: half the shared-memory wavefronts of the d1 part (orders >= 12)
+    if constexpr (K >= 5) {   // sliding queue window: half the register moves per plane
+        register_slide<K, 16, K >= 7 ? 14 : 16, 4, false, 2>();
+        register_slide<K, 16, K >= 7 ? 14 : 16, 4, true, 2>();
+    }
+    if constexpr (K >= 6) {
+        register_patch<K, 4, false, 2>();
+        register_patch<K, 4, true, 2>();
+        register_patch<K, 3, false, 2>();
+        register_patch<K, 3, true, 2>();
+    }
     if constexpr (K <= 4) {  // unrolling by 2K+1 overflows the instruction cache above
         register_rotated_pair<K, 16, 16, 3>();
     }

@@ -179,7 +179,42 @@ def test_checkpointed_gradient_equals_full_history(nt, C):
     plan.close()
 
 
-@pytest.mark.parametrize("order,tile", [(8, None), (8, (16, 16, -3)), (12, None), (4, None)])
+@pytest.mark.parametrize("order", [12, 14, 16])
+def test_patch_kernel_agrees_bitwise_with_the_dual_stream_kernel(order):
+    """acoustic_patch_kernel.cuh (2 x 2 nodes per thread, queue window slid by two planes)
+    keeps the arithmetic and its order per node: forward with snapshots, adjoint and the
+    gradient with fused imaging equal the dual-stream kernel bit for bit, separable and dense
+    damping, ragged extents, several d0 chunks."""
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([75, 53, 67], 10.0, 9, order, 30, dt_frac=0.9, n_rec_line=40)
+    data = np.random.default_rng(2).standard_normal((geom.nt, geom.n_rec)) * np.hanning(geom.nt)[:, None]
+    for dense in (False, True):
+        plan = capi.Plan(model.N, model.spacing, order, geom.dt, geom.nt, dense_damping=dense)
+        plan.set_model(model.m, model.damp, model.v_max)
+        plan.set_points(capi.CLOUD_SRC, geom.src_base, geom.src_w)
+        plan.set_points(capi.CLOUD_REC, geom.rec_base, geom.rec_w)
+        out = {}
+        rows = 14 if order >= 14 else 16
+        for name, tile in (("dual", (16, rows, -4)), ("patch4", (16, 14, -204)),
+                           ("patch3", (16, 14, -203)), ("slide", (16, rows, -304))):
+            for chunk in (0, 11):
+                plan.set_tile(*tile, chunk)
+                assert plan.get_tile()["stages"] == tile[2]
+                rec, _ = plan.forward(geom.src, save_every=2)
+                u = plan.wavefield(geom.nt - 1)
+                g, _ = plan.gradient(data)
+                srca, _ = plan.adjoint(data)
+                out[(name, chunk)] = (rec, u, g, srca, plan.wavefield(0))
+        ref = out[("dual", 0)]
+        assert np.abs(ref[0]).max() > 0 and np.abs(ref[2]).max() > 0
+        for key, val in out.items():
+            for a, b in zip(val, ref):
+                assert np.array_equal(a, b), (order, dense, key)
+        plan.close()
+
+
+@pytest.mark.parametrize("order,tile", [(8, None), (8, (16, 16, -3)), (12, None), (4, None),
+                                        (16, (16, 14, -204))])
 def test_gradient_runs_are_bitwise_repeatable(order, tile):
     """Regression for a pipeline race found at sizes that fill the SMs with several blocks:
     a stage was released to the TMA producer while a warp's shared-memory loads were still
