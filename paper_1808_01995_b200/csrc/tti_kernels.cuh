@@ -146,32 +146,33 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
     float* const ob = p.bg[field];
     long long lo_off = (long long)zb * p.plane + (long long)y * p.pitch + x;   // compact
 
-    float q[Q][4];
+    // the d0 queue is a sliding window of 2K+2 slots: the plane loop is unrolled by two (plane
+    // n uses slots [0, 2K], plane n+1 slots [1, 2K+1]) and the window moves by two slots
+    // afterwards -- half the register moves of a queue shifted every plane
+    float q[Q + 1][4];
 #pragma unroll
-    for (int j = 0; j < Q; ++j)
+    for (int j = 0; j < Q + 1; ++j)
 #pragma unroll
         for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
 
     const int aown = ty * TX + 4 * tx;
     int s = 0;
     uint32_t fph = 0;
-    for (int n = 0; n < nplanes; ++n) {
+    auto iteration = [&](auto off, int n) {
+        constexpr int OFF = decltype(off)::value;
+#define SFB_TQ(i) q[(i) + OFF]
         mbar_wait(full + s, fph);
         const float* st = ring + s * STAGE;
         {
             const float4 v = *reinterpret_cast<const float4*>(st + field * ABOX + aown);
-#pragma unroll
-            for (int j = 0; j < Q - 1; ++j)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
-            q[Q - 1][0] = v.x;
-            q[Q - 1][1] = v.y;
-            q[Q - 1][2] = v.z;
-            q[Q - 1][3] = v.w;
+            SFB_TQ(Q - 1)[0] = v.x;
+            SFB_TQ(Q - 1)[1] = v.y;
+            SFB_TQ(Q - 1)[2] = v.z;
+            SFB_TQ(Q - 1)[3] = v.w;
         }
         if (n < 2 * K) {
             __syncwarp();
-            if (lane0) mbar_release(done + s, q[Q - 1][0]);
+            if (lane0) mbar_release(done + s, SFB_TQ(Q - 1)[0]);
         } else {
             const float* cp = st + OFF_CTR + field * CPAD;  // haloed centre box of this field
             const float* np = st + OFF_PLAIN + aown;
@@ -187,15 +188,15 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                 {   // d0 from the register queue, two nodes per instruction
                     float2 d01 = make_float2(0.f, 0.f), d23 = make_float2(0.f, 0.f);
                     if (LAP) {
-                        l01 = f2_mul(f2_splat(p.k.c0), make_float2(q[K][0], q[K][1]));
-                        l23 = f2_mul(f2_splat(p.k.c0), make_float2(q[K][2], q[K][3]));
+                        l01 = f2_mul(f2_splat(p.k.c0), make_float2(SFB_TQ(K)[0], SFB_TQ(K)[1]));
+                        l23 = f2_mul(f2_splat(p.k.c0), make_float2(SFB_TQ(K)[2], SFB_TQ(K)[3]));
                     }
 #pragma unroll
                     for (int j = 1; j <= K; ++j) {
-                        const float2 hi01 = make_float2(q[K + j][0], q[K + j][1]);
-                        const float2 hi23 = make_float2(q[K + j][2], q[K + j][3]);
-                        const float2 lo01 = make_float2(q[K - j][0], q[K - j][1]);
-                        const float2 lo23 = make_float2(q[K - j][2], q[K - j][3]);
+                        const float2 hi01 = make_float2(SFB_TQ(K + j)[0], SFB_TQ(K + j)[1]);
+                        const float2 hi23 = make_float2(SFB_TQ(K + j)[2], SFB_TQ(K + j)[3]);
+                        const float2 lo01 = make_float2(SFB_TQ(K - j)[0], SFB_TQ(K - j)[1]);
+                        const float2 lo23 = make_float2(SFB_TQ(K - j)[2], SFB_TQ(K - j)[3]);
                         const float2 w = f2_splat(p.k.fz[j - 1]);
                         d01 = f2_fma(w, f2_sub(hi01, lo01), d01);
                         d23 = f2_fma(w, f2_sub(hi23, lo23), d23);
@@ -227,8 +228,9 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                     g01 = f2_fma(make_float2(b4.x, b4.y), d01, g01);
                     g23 = f2_fma(make_float2(b4.z, b4.w), d23, g23);
                 }
-                float g[4], lap[4] = {0.f, 0.f, 0.f, 0.f};
-                {   // d2: one aligned row segment; the shifted operands stay scalar
+                float g[4], lap[4];
+                {   // d2: one aligned row segment; even j: the operand pairs are register-aligned
+                    // and run packed, odd j: they straddle two pairs and stay scalar
                     float xr[2 * KP + 4];
                     const float* rowp = cp + (ty + K) * SW + 4 * tx;
 #pragma unroll
@@ -239,24 +241,48 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                         xr[4 * v + 2] = t4.z;
                         xr[4 * v + 3] = t4.w;
                     }
-                    float d2[4] = {0.f, 0.f, 0.f, 0.f};
+                    float2 e01 = make_float2(0.f, 0.f), e23 = make_float2(0.f, 0.f);   // D2 f
+                    float2 m01 = make_float2(0.f, 0.f), m23 = make_float2(0.f, 0.f);   // D22 f
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int j = 1; j <= K; ++j) {
-                            d2[c] = fmaf(p.k.fx[j - 1], xr[KP + c + j] - xr[KP + c - j], d2[c]);
-                            if (LAP) lap[c] = fmaf(p.k.lx[j - 1], xr[KP + c + j] + xr[KP + c - j], lap[c]);
+                    for (int j = 1; j <= K; ++j) {
+                        if (j % 2 == 0) {
+                            const float2 h01 = make_float2(xr[KP + j], xr[KP + 1 + j]);
+                            const float2 h23 = make_float2(xr[KP + 2 + j], xr[KP + 3 + j]);
+                            const float2 o01 = make_float2(xr[KP - j], xr[KP + 1 - j]);
+                            const float2 o23 = make_float2(xr[KP + 2 - j], xr[KP + 3 - j]);
+                            const float2 w = f2_splat(p.k.fx[j - 1]);
+                            e01 = f2_fma(w, f2_sub(h01, o01), e01);
+                            e23 = f2_fma(w, f2_sub(h23, o23), e23);
+                            if (LAP) {
+                                const float2 wl = f2_splat(p.k.lx[j - 1]);
+                                m01 = f2_fma(wl, f2_add(h01, o01), m01);
+                                m23 = f2_fma(wl, f2_add(h23, o23), m23);
+                            }
+                        } else {
+                            e01.x = fmaf(p.k.fx[j - 1], xr[KP + j] - xr[KP - j], e01.x);
+                            e01.y = fmaf(p.k.fx[j - 1], xr[KP + 1 + j] - xr[KP + 1 - j], e01.y);
+                            e23.x = fmaf(p.k.fx[j - 1], xr[KP + 2 + j] - xr[KP + 2 - j], e23.x);
+                            e23.y = fmaf(p.k.fx[j - 1], xr[KP + 3 + j] - xr[KP + 3 - j], e23.y);
+                            if (LAP) {
+                                m01.x = fmaf(p.k.lx[j - 1], xr[KP + j] + xr[KP - j], m01.x);
+                                m01.y = fmaf(p.k.lx[j - 1], xr[KP + 1 + j] + xr[KP + 1 - j], m01.y);
+                                m23.x = fmaf(p.k.lx[j - 1], xr[KP + 2 + j] + xr[KP + 2 - j], m23.x);
+                                m23.y = fmaf(p.k.lx[j - 1], xr[KP + 3 + j] + xr[KP + 3 - j], m23.y);
+                            }
                         }
-                    g[0] = fmaf(c4.x, d2[0], g01.x);
-                    g[1] = fmaf(c4.y, d2[1], g01.y);
-                    g[2] = fmaf(c4.z, d2[2], g23.x);
-                    g[3] = fmaf(c4.w, d2[3], g23.y);
-                    if (LAP) {
-                        lap[0] += l01.x;
-                        lap[1] += l01.y;
-                        lap[2] += l23.x;
-                        lap[3] += l23.y;
                     }
+                    g01 = f2_fma(make_float2(c4.x, c4.y), e01, g01);
+                    g23 = f2_fma(make_float2(c4.z, c4.w), e23, g23);
+                    g[0] = g01.x;
+                    g[1] = g01.y;
+                    g[2] = g23.x;
+                    g[3] = g23.y;
+                    l01 = f2_add(m01, l01);
+                    l23 = f2_add(m23, l23);
+                    lap[0] = l01.x;
+                    lap[1] = l01.y;
+                    lap[2] = l23.x;
+                    lap[3] = l23.y;
                 }
                 // g[0] (+ lap[0]) depends on every shared-memory load of the iteration
                 __syncwarp();
@@ -283,6 +309,15 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
             s = 0;
             fph ^= 1;
         }
+#undef SFB_TQ
+    };
+    for (int n = 0; n < nplanes; n += 2) {
+        iteration(std::integral_constant<int, 0>{}, n);
+        if (n + 1 < nplanes) iteration(std::integral_constant<int, 1>{}, n + 1);
+#pragma unroll
+        for (int j = 0; j < Q - 1; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) q[j][c] = q[j + 2][c];
     }
 }
 
@@ -421,46 +456,44 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
         dxy[3] = dx4.w + dyv;
     }
 
-    float q[Q][4];
+    // sliding queue window, plane loop unrolled by two (see tti_rot_kernel)
+    float q[Q + 1][4];
 #pragma unroll
-    for (int j = 0; j < Q; ++j)
+    for (int j = 0; j < Q + 1; ++j)
 #pragma unroll
         for (int c = 0; c < 4; ++c) q[j][c] = 0.f;
 
     const int aown = ty * TX + 4 * tx;
     int s = 0;
     uint32_t fph = 0;
-    for (int n = 0; n < nplanes; ++n) {
+    auto iteration = [&](auto off, int n) {
+        constexpr int OFF = decltype(off)::value;
+#define SFB_TQ(i) q[(i) + OFF]
         mbar_wait(full + s, fph);
         float* st = ring + s * STAGE;
         {
-            float4 v = *reinterpret_cast<const float4*>(st + field * ABOX + aown);
+            const float4 v = *reinterpret_cast<const float4*>(st + field * ABOX + aown);
             const float4 a4 = *reinterpret_cast<const float4*>(st + 2 * ABOX + aown);
-            v.x *= a4.x;   // the queue holds a g
-            v.y *= a4.y;
-            v.z *= a4.z;
-            v.w *= a4.w;
-#pragma unroll
-            for (int j = 0; j < Q - 1; ++j)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 1][c];
-            q[Q - 1][0] = v.x;
-            q[Q - 1][1] = v.y;
-            q[Q - 1][2] = v.z;
-            q[Q - 1][3] = v.w;
+            // the queue holds a g
+            const float2 p01 = f2_mul(make_float2(v.x, v.y), make_float2(a4.x, a4.y));
+            const float2 p23 = f2_mul(make_float2(v.z, v.w), make_float2(a4.z, a4.w));
+            SFB_TQ(Q - 1)[0] = p01.x;
+            SFB_TQ(Q - 1)[1] = p01.y;
+            SFB_TQ(Q - 1)[2] = p23.x;
+            SFB_TQ(Q - 1)[3] = p23.y;
         }
         if (n < 2 * K) {
             __syncwarp();
-            if (lane0) mbar_release(done + s, q[Q - 1][0]);
+            if (lane0) mbar_release(done + s, SFB_TQ(Q - 1)[0]);
         } else {
             float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
             for (int j = 1; j <= K; ++j) {   // D0 (a g): register queue
                 const float2 w = f2_splat(p.k.fz[j - 1]);
-                a01 = f2_fma(w, f2_sub(make_float2(q[K + j][0], q[K + j][1]),
-                                       make_float2(q[K - j][0], q[K - j][1])), a01);
-                a23 = f2_fma(w, f2_sub(make_float2(q[K + j][2], q[K + j][3]),
-                                       make_float2(q[K - j][2], q[K - j][3])), a23);
+                a01 = f2_fma(w, f2_sub(make_float2(SFB_TQ(K + j)[0], SFB_TQ(K + j)[1]),
+                                       make_float2(SFB_TQ(K - j)[0], SFB_TQ(K - j)[1])), a01);
+                a23 = f2_fma(w, f2_sub(make_float2(SFB_TQ(K + j)[2], SFB_TQ(K + j)[3]),
+                                       make_float2(SFB_TQ(K - j)[2], SFB_TQ(K - j)[3])), a23);
             }
             {   // D1 (b g): rows above and below in the d1-haloed box
                 const float* colp = st + OFF_Y + field * YBOX + ty * TX + 4 * tx;
@@ -473,8 +506,9 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
                     a23 = f2_fma(w, f2_sub(make_float2(hi.z, hi.w), make_float2(lo.z, lo.w)), a23);
                 }
             }
-            float d2[4] = {0.f, 0.f, 0.f, 0.f};
-            {   // D2 (c g): one aligned row segment of g and of c in the d2-haloed boxes
+            float2 e01 = make_float2(0.f, 0.f), e23 = make_float2(0.f, 0.f);
+            {   // D2 (c g): one aligned row segment of g and of c in the d2-haloed boxes; the
+                // products and the even-j differences run packed
                 float xr[2 * KP + 4];
                 const float* rowp = st + OFF_X + field * XPAD + ty * SW + 4 * tx;
                 const float* crow = st + OFF_X + 2 * XPAD + ty * SW + 4 * tx;
@@ -482,22 +516,32 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
                 for (int v = 0; v < (2 * KP + 4) / 4; ++v) {
                     const float4 t4 = *reinterpret_cast<const float4*>(rowp + 4 * v);
                     const float4 n4 = *reinterpret_cast<const float4*>(crow + 4 * v);
-                    xr[4 * v + 0] = t4.x * n4.x;
-                    xr[4 * v + 1] = t4.y * n4.y;
-                    xr[4 * v + 2] = t4.z * n4.z;
-                    xr[4 * v + 3] = t4.w * n4.w;
+                    const float2 m01 = f2_mul(make_float2(t4.x, t4.y), make_float2(n4.x, n4.y));
+                    const float2 m23 = f2_mul(make_float2(t4.z, t4.w), make_float2(n4.z, n4.w));
+                    xr[4 * v + 0] = m01.x;
+                    xr[4 * v + 1] = m01.y;
+                    xr[4 * v + 2] = m23.x;
+                    xr[4 * v + 3] = m23.y;
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int j = 1; j <= K; ++j)
-                        d2[c] = fmaf(p.k.fx[j - 1], xr[KP + c + j] - xr[KP + c - j], d2[c]);
+                for (int j = 1; j <= K; ++j) {
+                    if (j % 2 == 0) {
+                        const float2 w = f2_splat(p.k.fx[j - 1]);
+                        e01 = f2_fma(w, f2_sub(make_float2(xr[KP + j], xr[KP + 1 + j]),
+                                               make_float2(xr[KP - j], xr[KP + 1 - j])), e01);
+                        e23 = f2_fma(w, f2_sub(make_float2(xr[KP + 2 + j], xr[KP + 3 + j]),
+                                               make_float2(xr[KP + 2 - j], xr[KP + 3 - j])), e23);
+                    } else {
+                        e01.x = fmaf(p.k.fx[j - 1], xr[KP + j] - xr[KP - j], e01.x);
+                        e01.y = fmaf(p.k.fx[j - 1], xr[KP + 1 + j] - xr[KP + 1 - j], e01.y);
+                        e23.x = fmaf(p.k.fx[j - 1], xr[KP + 2 + j] - xr[KP + 2 - j], e23.x);
+                        e23.y = fmaf(p.k.fx[j - 1], xr[KP + 3 + j] - xr[KP + 3 - j], e23.y);
+                    }
+                }
             }
-            float hz[4];
-            hz[0] = a01.x + d2[0];
-            hz[1] = a01.y + d2[1];
-            hz[2] = a23.x + d2[2];
-            hz[3] = a23.y + d2[3];
+            a01 = f2_add(a01, e01);
+            a23 = f2_add(a23, e23);
+            const float hz[4] = {a01.x, a01.y, a23.x, a23.y};
             // swap with the other group through this thread's own (already consumed) slot
             // of the feed box; the named barrier covers the 2 * GROUP consumer threads
             *reinterpret_cast<float4*>(st + field * ABOX + aown) =
@@ -545,6 +589,15 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
             s = 0;
             fph ^= 1;
         }
+#undef SFB_TQ
+    };
+    for (int n = 0; n < nplanes; n += 2) {
+        iteration(std::integral_constant<int, 0>{}, n);
+        if (n + 1 < nplanes) iteration(std::integral_constant<int, 1>{}, n + 1);
+#pragma unroll
+        for (int j = 0; j < Q - 1; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) q[j][c] = q[j + 2][c];
     }
 }
 
