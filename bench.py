@@ -299,7 +299,7 @@ def windows(plan, op, nt, W, K, runs=3, stencil_only=False):
     return sorted(out, key=lambda r: r.seconds)
 
 
-def roofline_of(op, pts, kernel_s, sep, images_every, tile, K_half, clocks, traffic=None):
+def roofline_of(op, pts, kernel_s, sep, images_every, tile, K_half, clocks, grid=None):
     """`achieved` uses the bytes this build's kernels must move per node-step (see
     actual_bytes); the SURVEY.md 8(d) contract figure is carried beside it."""
     peak, kind = peaks()
@@ -325,18 +325,19 @@ def roofline_of(op, pts, kernel_s, sep, images_every, tile, K_half, clocks, traf
         r["kernel"] = "acoustic_step_dual_kernel" if tile.get("stages", 0) < 0 else "acoustic_step_kernel"
     if op == "gradient":
         r["images_every"] = images_every
-    tr = traffic if traffic is not None else static_traffic(op, sep)
-    r.update(tr)
+    r.update(static_traffic(op, sep, grid, 2 * K_half))
     return r
 
 
-def static_traffic(op, sep):
-    """DRAM bytes per launch from the committed ncu --set full capture of the same kernel
-    (profiles/r02_traffic.json, written by tools/ncu_summary.py); cannot be measured inside
-    an unprofiled run."""
+def static_traffic(op, sep, grid, order):
+    """DRAM bytes per launch from the committed ncu --set full capture of the same kernel on
+    the same grid (profiles/r02_traffic.json, written by tools/ncu_summary.py); it cannot be
+    measured inside an unprofiled run, and there is a capture for the 592^3 grid only."""
     path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     key = {"forward": "acoustic_sep" if sep else "acoustic_dense", "adjoint": "acoustic_sep" if sep else "acoustic_dense",
            "gradient": "gradient", "tti": "tti"}[op]
+    if list(grid or []) != [592, 592, 592] or order != (12 if op == "tti" else 8):
+        return {"traffic": None, "traffic_source": "no ncu capture committed for this grid / order"}
     try:
         with open(path) as f:
             d = json.load(f)
@@ -373,7 +374,7 @@ def measure_op(wl, op, K, W, device, want_e2e=True):
            "value_runs": [pts * K / r.seconds / 1e9 for r in ws], "gpu_launches": int(rep.kernel_launches),
            "clocks": clocks,
            "roofline": roofline_of(op, pts, st.seconds / st.steps, sep, images_every,
-                                   plan.get_tile() if op != "tti" else {}, wl.order // 2, clocks)}
+                                   plan.get_tile() if op != "tti" else {}, wl.order // 2, clocks, wl.N)}
     if want_e2e:
         # the C-ABI call with HOST buffers over exactly K steps: a plan with nt = K + 2
         plan.close()
