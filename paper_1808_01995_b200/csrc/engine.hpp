@@ -67,6 +67,10 @@ void download_field(Plan& P, const float* dev, const sfb_field_mview* out);
 void detect_separable_damping(Plan& P, const IntView& v, const DevBuf& damp_f64, long long ref_plane);
 void build_cloud(Plan& P, Cloud& c);
 constexpr size_t kStageBytes = 32u << 20;  // per half
+// sampled rows leave the device in chunks of about this size while the loop runs: small enough
+// that the copy and the host-side widening of a chunk hide behind the next steps and the tail
+// after the last step is short (a 592^3 step is 0.54 ms, a row of 512 x 512 traces 1 MB)
+constexpr size_t kRowChunkBytes = 4u << 20;
 
 template <typename Fn>
 void parallel_chunks(long long n, Fn&& fn) {
@@ -137,7 +141,7 @@ struct RowStreamer {
     long long pend_row[2] = {0, 0}, pend_rows[2] = {0, 0};
 
     RowStreamer(Plan& p, Cloud& cl, double* h) : P(p), c(cl), host(h) {
-        rows = std::max<long long>(1, (long long)(kStageBytes / 4) / std::max<long long>(c.np, 1));
+        rows = std::max<long long>(1, (long long)(kRowChunkBytes / 4) / std::max<long long>(c.np, 1));
         P.stage.ensure(size_t(rows * c.np));
     }
     void drain(int i) {
