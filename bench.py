@@ -670,6 +670,15 @@ class SlabJob:
             self._loop = lambda a, b: slabs.tti_step_loop(self.eng, ex, a, b)     # noqa: E731
             if world > 1:
                 self.halo = "nccl send/recv (two exchanges per step: g, then p and r)"
+                if os.environ.get("SFB_HALO", "push") == "push":
+                    try:
+                        drv = slabs.TtiPeerPushDriver(plan, rank, world)
+                        self._loop = drv.run
+                        self.halo = ("fused peer push (CUDA IPC stores from both passes: g, then "
+                                     "the new p and r)")
+                    except RuntimeError as e:
+                        if rank == 0:
+                            log(f"[bench] {e}; falling back to NCCL send/recv")
         else:
             self.eng = slabs.PlanEngine(plan, self.oid, device)
             self._loop = lambda a, b: slabs.step_loop(self.eng, ex, a, b)         # noqa: E731

@@ -114,7 +114,8 @@ ExecutionReport run_gradient(GradientOp& g, Backend backend = Backend::Auto,
 ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model,
                                const AcquisitionGeometry& geom, const std::vector<int>& devices);
 // the TTI pair on slabs: two neighbour exchanges per step (g between the passes, the new p
-// and r levels after the update) as device-to-device copies between the plans
+// and r levels after the update), both fused into the passes as peer stores between the
+// linked plans (sfb_tti_step_rot_fused / sfb_tti_step_update_fused)
 ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model, const TtiModel& tti,
                                const AcquisitionGeometry& geom, const std::vector<int>& devices);
 

@@ -244,7 +244,7 @@ SFB_API int sfb_peer_wait(sfb_plan* plan, sfb_plan* neighbour);
  * plans must make the same sequence of boundary half-steps, link before any of them steps,
  * and stay alive until every rank has synchronised its last step (their streams read this
  * plan's counter). */
-#define SFB_PEER_BLOB_BYTES 256
+#define SFB_PEER_BLOB_BYTES 1024
 SFB_API int sfb_peer_export(sfb_plan* plan, void* blob);
 SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* hi_blob);
 SFB_API int sfb_peer_wait_ipc(sfb_plan* plan);
@@ -258,6 +258,19 @@ SFB_API int sfb_peer_wait_ipc(sfb_plan* plan);
  * sfb_step_begin(SFB_OP_TTI_FORWARD) zeroes the state, sfb_step_end closes the run. */
 enum { SFB_TTI_HALO_G_P = 0, SFB_TTI_HALO_G_R = 1, SFB_TTI_HALO_P = 2, SFB_TTI_HALO_R = 3 };
 SFB_API int sfb_tti_step_rot(sfb_plan* plan, int64_t t, int part);
+/* The TTI pair on LINKED slabs (sfb_link_peers / sfb_link_peers_ipc after sfb_set_model_tti):
+ * each pass of a step is one launch over the whole slab whose edge chunks sweep towards the
+ * interior and store their boundary planes -- g(p), g(r) in the first pass, the new p and r
+ * in the second -- straight into the neighbours' ghost planes; the point launches mirror
+ * injected boundary nodes of p and r.  One step of a plan is
+ *     sfb_tti_step_rot_fused;  sfb_tti_peer_wait_g (per neighbour) / _g_ipc;
+ *     sfb_tti_step_update_fused;  sfb_peer_wait (per neighbour) / sfb_peer_wait_ipc
+ * with every plan making each call before any plan makes the next one when one process
+ * drives several plans.  No copies, no send/recv; same bits as the single domain. */
+SFB_API int sfb_tti_step_rot_fused(sfb_plan* plan, int64_t t);
+SFB_API int sfb_tti_peer_wait_g(sfb_plan* plan, sfb_plan* neighbour);
+SFB_API int sfb_tti_peer_wait_g_ipc(sfb_plan* plan);
+SFB_API int sfb_tti_step_update_fused(sfb_plan* plan, int64_t t);
 SFB_API int sfb_tti_step_update(sfb_plan* plan, int64_t t, int part);
 SFB_API int sfb_tti_halo_blocks(sfb_plan* plan, int which, int64_t t, void** send_lo,
                                 void** send_hi, void** recv_lo, void** recv_hi, int64_t* count);

@@ -46,7 +46,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_slab_fused", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_slab_fused", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_step_rot_fused", "sfb_tti_peer_wait_g", "sfb_tti_peer_wait_g_ipc", "sfb_tti_step_update_fused", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune", "sfb_debug_stall",
 ]
@@ -83,12 +83,16 @@ lib.sfb_halo_blocks.argtypes = [C.c_void_p, C.c_int, C.c_int64] + [C.POINTER(C.c
 lib.sfb_tti_step_rot.argtypes = [C.c_void_p, C.c_int64, C.c_int]
 lib.sfb_tti_step_update.argtypes = [C.c_void_p, C.c_int64, C.c_int]
 lib.sfb_tti_halo_blocks.argtypes = lib.sfb_halo_blocks.argtypes
+lib.sfb_tti_step_rot_fused.argtypes = [C.c_void_p, C.c_int64]
+lib.sfb_tti_step_update_fused.argtypes = [C.c_void_p, C.c_int64]
+lib.sfb_tti_peer_wait_g.argtypes = [C.c_void_p, C.c_void_p]
+lib.sfb_tti_peer_wait_g_ipc.argtypes = [C.c_void_p]
 lib.sfb_link_peers.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 lib.sfb_peer_wait.argtypes = [C.c_void_p, C.c_void_p]
 lib.sfb_peer_export.argtypes = [C.c_void_p, C.c_void_p]
 lib.sfb_link_peers_ipc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 lib.sfb_peer_wait_ipc.argtypes = [C.c_void_p]
-PEER_BLOB_BYTES = 256
+PEER_BLOB_BYTES = 1024
 lib.sfb_stream_sync.argtypes = [C.c_void_p]
 lib.sfb_debug_stall.argtypes = [C.c_void_p, C.c_int, C.c_int64]
 lib.sfb_streams.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
@@ -353,6 +357,18 @@ class Plan:
 
     def tti_step_update(self, t, part):
         self._chk(lib.sfb_tti_step_update(self.h, t, part))
+
+    def tti_step_rot_fused(self, t):
+        self._chk(lib.sfb_tti_step_rot_fused(self.h, t))
+
+    def tti_step_update_fused(self, t):
+        self._chk(lib.sfb_tti_step_update_fused(self.h, t))
+
+    def tti_peer_wait_g(self, neighbour):
+        self._chk(lib.sfb_tti_peer_wait_g(self.h, neighbour.h))
+
+    def tti_peer_wait_g_ipc(self):
+        self._chk(lib.sfb_tti_peer_wait_g_ipc(self.h))
 
     def tti_halo_blocks(self, which, t):
         p = [C.c_void_p() for _ in range(4)]

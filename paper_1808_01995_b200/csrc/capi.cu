@@ -39,6 +39,10 @@ struct PeerBlob {   // what sfb_peer_export writes into the caller's SFB_PEER_BL
     cudaIpcMemHandle_t u[2];
     cudaIpcMemHandle_t flag;
     int64_t z_lo, z_hi, n1, n2, pitch, plane, K;
+    // TTI pair (has_tti != 0): g(p), g(r) and the two levels of r
+    int64_t has_tti;
+    cudaIpcMemHandle_t g[2];
+    cudaIpcMemHandle_t r[2];
 };
 static_assert(sizeof(PeerBlob) <= SFB_PEER_BLOB_BYTES, "peer blob");
 
@@ -57,6 +61,11 @@ void close_ipc(Plan& P) {
         for (int b = 0; b < 2; ++b)
             if (P.ipc_u[side][b]) cudaIpcCloseMemHandle(P.ipc_u[side][b]);
         if (P.ipc_flag[side]) cudaIpcCloseMemHandle(P.ipc_flag[side]);
+        for (int b = 0; b < 2; ++b) {
+            if (P.ipc_g[side][b]) cudaIpcCloseMemHandle(P.ipc_g[side][b]);
+            if (P.ipc_r[side][b]) cudaIpcCloseMemHandle(P.ipc_r[side][b]);
+            P.ipc_g[side][b] = P.ipc_r[side][b] = nullptr;
+        }
         P.ipc_u[side][0] = P.ipc_u[side][1] = P.ipc_flag[side] = nullptr;
     }
 }
@@ -233,6 +242,7 @@ SFB_API int sfb_plan_create(const sfb_plan_desc* desc, sfb_plan** out) {
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_bnd, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_push, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreateWithFlags(&P.ev_done, cudaEventDisableTiming));
+        SFB_CUDA(cudaEventCreateWithFlags(&P.ev_g, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreate(&P.ev_t0));
         SFB_CUDA(cudaEventCreate(&P.ev_t1));
         P.u[0].alloc(size_t(P.ucount) * 4);
@@ -260,6 +270,7 @@ SFB_API int sfb_plan_destroy(sfb_plan* plan) {
     if (plan->ev_bnd) cudaEventDestroy(plan->ev_bnd);
     if (plan->ev_push) cudaEventDestroy(plan->ev_push);
     if (plan->ev_done) cudaEventDestroy(plan->ev_done);
+    if (plan->ev_g) cudaEventDestroy(plan->ev_g);
     close_ipc(*plan);
     if (plan->ev_t0) cudaEventDestroy(plan->ev_t0);
     if (plan->ev_t1) cudaEventDestroy(plan->ev_t1);
@@ -382,10 +393,17 @@ SFB_API int sfb_set_model_tti(sfb_plan* plan, const sfb_field_view* epsilon,
         SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_rot,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(P.tti_variant->smem_rot)));
-        for (int i = 0; i < 2; ++i)
+        SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_rot_push,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(P.tti_variant->smem_rot)));
+        for (int i = 0; i < 2; ++i) {
             SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_div[i],
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(P.tti_variant->smem_div[i])));
+            SFB_CUDA(cudaFuncSetAttribute(P.tti_variant->f_div_push[i],
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(P.tti_variant->smem_div[i])));
+        }
         tti_make_maps(P);
         const long long rows = (long long)P.n0 * P.N[1];
         tti_setup_kernel<<<row_grid(P, rows), 256, 0, P.s_main>>>(
@@ -706,6 +724,74 @@ SFB_API int sfb_step_slab_fused(sfb_plan* plan, int op, int64_t t) {
     });
 }
 
+namespace {
+void signal_word(Plan& P, int word, unsigned value) {
+    static StreamValueFn write_value = stream_value_fn("cuStreamWriteValue32");
+    CUresult rc = write_value(P.s_main, reinterpret_cast<CUdeviceptr>(P.push_flag.p) + 4 * word,
+                              value, 0);
+    if (rc != CUDA_SUCCESS)
+        throw Failure(SFB_ERR_CUDA, "cuStreamWriteValue32 failed with code " + std::to_string(int(rc)));
+}
+bool tti_linked(const Plan& P) {
+    return P.peer_g_lo[0] || P.peer_g_hi[0];
+}
+}  // namespace
+
+SFB_API int sfb_tti_step_rot_fused(sfb_plan* plan, int64_t t) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(P.tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
+        require(!(P.peer_lo[0] || P.peer_hi[0]) || tti_linked(P), SFB_ERR_BINDING,
+                "link the plans after sfb_set_model_tti so that the TTI buffers are mapped");
+        tti_rot(P, t, kPartSlabFused);   // pushes both boundary plane groups of g first
+        if (tti_linked(P)) {
+            SFB_CUDA(cudaEventRecord(P.ev_g, P.s_main));
+            if (P.ipc_flag[0] || P.ipc_flag[1]) signal_word(P, 2, ++P.g_count);
+        }
+    });
+}
+
+SFB_API int sfb_tti_peer_wait_g(sfb_plan* plan, sfb_plan* neighbour) {
+    if (!plan || !neighbour) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        SFB_CUDA(cudaStreamWaitEvent(plan->s_main, neighbour->ev_g, 0));
+    });
+}
+
+SFB_API int sfb_tti_peer_wait_g_ipc(sfb_plan* plan) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        static StreamValueFn wait_value = stream_value_fn("cuStreamWaitValue32");
+        for (int side = 0; side < 2; ++side) {
+            if (!P.ipc_flag[side]) continue;
+            CUresult rc = wait_value(P.s_main, reinterpret_cast<CUdeviceptr>(P.ipc_flag[side]) + 8,
+                                     P.g_count, CU_STREAM_WAIT_VALUE_GEQ);
+            if (rc != CUDA_SUCCESS)
+                throw Failure(SFB_ERR_CUDA, "cuStreamWaitValue32 failed with code " +
+                                                std::to_string(int(rc)));
+        }
+    });
+}
+
+SFB_API int sfb_tti_step_update_fused(sfb_plan* plan, int64_t t) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        require(P.tti_set, SFB_ERR_BINDING, "TTI fields are not bound (sfb_set_model_tti)");
+        tti_update(P, t, kPartSlabFused);   // pushes the new p and r boundary planes first
+        if (tti_linked(P)) {
+            SFB_CUDA(cudaEventRecord(P.ev_push, P.s_main));
+            SFB_CUDA(cudaEventRecord(P.ev_done, P.s_main));
+            if (P.ipc_flag[0] || P.ipc_flag[1]) {
+                signal_word(P, 0, ++P.push_count);
+                signal_word(P, 1, ++P.done_count);
+            }
+        }
+    });
+}
+
 SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi) {
     if (!plan) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {
@@ -714,7 +800,9 @@ SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi) {
             return Q.K == P.K && Q.N[1] == P.N[1] && Q.N[2] == P.N[2] && Q.pitch == P.pitch &&
                    Q.plane == P.plane;
         };
-        for (int b = 0; b < 2; ++b) P.peer_lo[b] = P.peer_hi[b] = nullptr;
+        for (int b = 0; b < 2; ++b)
+            P.peer_lo[b] = P.peer_hi[b] = P.peer_g_lo[b] = P.peer_g_hi[b] = P.peer_r_lo[b] =
+                P.peer_r_hi[b] = nullptr;
         if ((lo || hi) && !P.variant->launch_push) {
             select_variant(P, 0, 0, 0);   // the default shape of the order carries the push kernel
             require(P.variant->launch_push != nullptr, SFB_ERR_CAPABILITY,
@@ -723,13 +811,24 @@ SFB_API int sfb_link_peers(sfb_plan* plan, sfb_plan* lo, sfb_plan* hi) {
         if (lo) {
             require(compatible(*lo) && lo->z_hi == P.z_lo, SFB_ERR_PARAMETER,
                     "link_peers: the lower plan is not the slab below this one");
+            const long long hg = (long long)(lo->n0 + lo->K) * lo->plane;
             for (int b = 0; b < 2; ++b)   // its high ghost planes: buffer planes n0 + K ...
-                P.peer_lo[b] = lo->u[b].as<float>() + (long long)(lo->n0 + lo->K) * lo->plane;
+                P.peer_lo[b] = lo->u[b].as<float>() + hg;
+            if (P.tti_set && lo->tti_set)
+                for (int b = 0; b < 2; ++b) {
+                    P.peer_g_lo[b] = lo->t_g[b].as<float>() + hg;
+                    P.peer_r_lo[b] = lo->t_r[b].as<float>() + hg;
+                }
         }
         if (hi) {
             require(compatible(*hi) && hi->z_lo == P.z_hi, SFB_ERR_PARAMETER,
                     "link_peers: the upper plan is not the slab above this one");
             for (int b = 0; b < 2; ++b) P.peer_hi[b] = hi->u[b].as<float>();   // planes 0 .. K-1
+            if (P.tti_set && hi->tti_set)
+                for (int b = 0; b < 2; ++b) {
+                    P.peer_g_hi[b] = hi->t_g[b].as<float>();
+                    P.peer_r_hi[b] = hi->t_r[b].as<float>();
+                }
         }
         if ((lo && lo->device != P.device) || (hi && hi->device != P.device)) {
             // one process driving several GPUs: map the neighbours' memory
@@ -761,6 +860,12 @@ SFB_API int sfb_peer_export(sfb_plan* plan, void* blob) {
         pb.pitch = P.pitch;
         pb.plane = P.plane;
         pb.K = P.K;
+        pb.has_tti = P.tti_set ? 1 : 0;
+        if (P.tti_set)
+            for (int b = 0; b < 2; ++b) {
+                SFB_CUDA(cudaIpcGetMemHandle(&pb.g[b], P.t_g[b].p));
+                SFB_CUDA(cudaIpcGetMemHandle(&pb.r[b], P.t_r[b].p));
+            }
         std::memset(blob, 0, SFB_PEER_BLOB_BYTES);
         std::memcpy(blob, &pb, sizeof pb);
     });
@@ -771,7 +876,9 @@ SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* 
     return guarded(plan, [&] {
         Plan& P = *plan;
         close_ipc(P);
-        for (int b = 0; b < 2; ++b) P.peer_lo[b] = P.peer_hi[b] = nullptr;
+        for (int b = 0; b < 2; ++b)
+            P.peer_lo[b] = P.peer_hi[b] = P.peer_g_lo[b] = P.peer_g_hi[b] = P.peer_r_lo[b] =
+                P.peer_r_hi[b] = nullptr;
         if (!lo_blob && !hi_blob) return;
         if (!P.variant->launch_push) {
             select_variant(P, 0, 0, 0);
@@ -793,15 +900,33 @@ SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* 
                                               cudaIpcMemLazyEnablePeerAccess));
             SFB_CUDA(cudaIpcOpenMemHandle(&P.ipc_flag[side], pb.flag, cudaIpcMemLazyEnablePeerAccess));
             const long long n0q = pb.z_hi - pb.z_lo;
+            const long long hg = (n0q + pb.K) * pb.plane;
             for (int b = 0; b < 2; ++b) {
                 float* base = static_cast<float*>(P.ipc_u[side][b]);
                 if (side == 0)
-                    P.peer_lo[b] = base + (n0q + pb.K) * pb.plane;   // its high ghost planes
+                    P.peer_lo[b] = base + hg;   // its high ghost planes
                 else
-                    P.peer_hi[b] = base;                              // its low ghost planes
+                    P.peer_hi[b] = base;        // its low ghost planes
+            }
+            if (P.tti_set && pb.has_tti) {
+                for (int b = 0; b < 2; ++b) {
+                    SFB_CUDA(cudaIpcOpenMemHandle(&P.ipc_g[side][b], pb.g[b],
+                                                  cudaIpcMemLazyEnablePeerAccess));
+                    SFB_CUDA(cudaIpcOpenMemHandle(&P.ipc_r[side][b], pb.r[b],
+                                                  cudaIpcMemLazyEnablePeerAccess));
+                    float* gb = static_cast<float*>(P.ipc_g[side][b]);
+                    float* rb = static_cast<float*>(P.ipc_r[side][b]);
+                    if (side == 0) {
+                        P.peer_g_lo[b] = gb + hg;
+                        P.peer_r_lo[b] = rb + hg;
+                    } else {
+                        P.peer_g_hi[b] = gb;
+                        P.peer_r_hi[b] = rb;
+                    }
+                }
             }
         }
-        P.push_count = P.done_count = 0;
+        P.push_count = P.done_count = P.g_count = 0;
         SFB_CUDA(cudaMemsetAsync(P.push_flag.p, 0, 256, P.s_main));
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
     });

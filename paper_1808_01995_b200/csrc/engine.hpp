@@ -125,8 +125,11 @@ void mark_stream(Plan& P, int part);
 void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex = nullptr);
 // part: SFB_PART_ALL = every node + gather; SFB_PART_LOW = nodes of both boundary plane
 // groups (boundary stream); SFB_PART_INTERIOR = remaining nodes + gather
+// peer_lo / peer_hi: with a target override, the neighbours' ghost planes of THAT field (the
+// TTI pair injects into r as well); without one the plan's own peer pointers are used
 void step_points(Plan& P, int op, long long t, int part, float* target_override = nullptr,
-                 bool allow_gather = true, const StepExtras* ex = nullptr);
+                 bool allow_gather = true, const StepExtras* ex = nullptr,
+                 float* peer_lo = nullptr, float* peer_hi = nullptr);
 void finite_guard(Plan& P, const char* what);
 // Streams the sampled trace rows to the caller's f64 table while the time loop runs: every
 // `rows` completed rows are copied (fp32, copy stream, pinned half) and the previous chunk

@@ -235,7 +235,7 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex) 
 // part: SFB_PART_ALL = every node + gather; SFB_PART_LOW = nodes of both boundary plane
 // groups (boundary stream); SFB_PART_INTERIOR = remaining nodes + gather
 void step_points(Plan& P, int op, long long t, int part, float* target_override, bool allow_gather,
-                 const StepExtras* ex) {
+                 const StepExtras* ex, float* peer_lo, float* peer_hi) {
     const OpRoles ro = roles(op);
     check_step_op(P, op, ro, ex);
     const int cur = int(t & 1), oth = cur ^ 1;
@@ -275,10 +275,9 @@ void step_points(Plan& P, int op, long long t, int part, float* target_override,
         pp.target = target_override ? target_override : P.u[oth].as<float>();
         pp.r = P.r.as<float>();
         pp.inv_dt2 = P.coef.inv_dt2;
-        if (!target_override &&
-            (part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartSlabFused)) {
-            pp.peer_lo = P.peer_lo[oth];
-            pp.peer_hi = P.peer_hi[oth];
+        if (part == SFB_PART_LOW || part == SFB_PART_HIGH || part == kPartSlabFused) {
+            pp.peer_lo = target_override ? peer_lo : P.peer_lo[oth];
+            pp.peer_hi = target_override ? peer_hi : P.peer_hi[oth];
             pp.plane = P.plane;
             pp.K = P.K;
             pp.n0 = P.n0;

@@ -98,17 +98,55 @@ dim3 tti_grid(const Plan& P, int lo, int hi, int chunk) {
                 unsigned((P.N[1] + v.tile_y - 1) / v.tile_y), unsigned((hi - lo + chunk - 1) / chunk));
 }
 
+// d0 chunk of a single-launch slab pass: at least two chunks (the first sweeps up, the last
+// down), whole waves of the one resident block per SM
+int tti_fused_chunk(const Plan& P) {
+    const TtiVariant& v = *P.tti_variant;
+    const long long tiles = ((P.N[2] + v.tile_x - 1) / v.tile_x) * ((P.N[1] + v.tile_y - 1) / v.tile_y);
+    const long long slots = P.sm_count;
+    int best = 2;
+    double best_score = -1;
+    const int max_nch = std::max(2, P.n0 / std::max(1, 2 * P.K));
+    for (int c = 2; c <= max_nch; ++c) {
+        const int ch = (P.n0 + c - 1) / c;
+        if (ch < P.K) break;
+        const int real = (P.n0 + ch - 1) / ch;
+        if (real < 2) continue;
+        const long long total = tiles * real;
+        const long long waves = (total + slots - 1) / slots;
+        const double score = double(total) / double(waves * slots) / (1.0 + (2.0 * P.K / ch) * 0.5);
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best = real;
+        }
+        if (total > 16 * slots) break;
+    }
+    return (P.n0 + best - 1) / best;
+}
+
 int tti_part_chunk(const Plan& P, int which, int part, int lo, int hi) {
+    if (part == kPartSlabFused) return tti_fused_chunk(P);
     return (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) ? std::min(P.tti_chunk[which], hi - lo)
                                                                : (hi - lo);
+}
+
+static void tti_part_bounds(const Plan& P, int part, int& lo, int& hi) {
+    if (part == kPartSlabFused) {
+        require(P.n0 >= 2 * P.K, SFB_ERR_PARAMETER, "slab thinner than two halo widths");
+        lo = 0;
+        hi = P.n0;
+    } else {
+        part_range(P, part, lo, hi);
+    }
 }
 
 // pass 1 on the planes of `part`: the products a g, b g, c g of p and r (level t)
 void tti_rot(Plan& P, long long t, int part) {
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;
-    part_range(P, part, lo, hi);
+    tti_part_bounds(P, part, lo, hi);
     if (hi <= lo) return;
+    const bool fused = part == kPartSlabFused;
     const TtiVariant& v = *P.tti_variant;
     const int cur = int(t & 1);
     RotParams rp{};
@@ -135,7 +173,21 @@ void tti_rot(Plan& P, long long t, int part) {
     m1.b = P.tt_plain[Plan::TF_B];
     m1.c = P.tt_plain[Plan::TF_C];
     cudaStream_t st = part_stream(P, part);
-    SFB_CUDA(v.rot(m1, rp, tti_grid(P, lo, hi, rp.chunk), st));
+    if (fused) {
+        // mirrors of the boundary planes of g in the neighbours' ghost planes: owned plane z of
+        // g[f] sits at g[f] + (z + K) planes; low group -> peer_g_lo + z planes, high group ->
+        // peer_g_hi + (z - (n0 - K)) planes
+        for (int f = 0; f < 2; ++f) {
+            float* g = P.t_g[f].as<float>();
+            rp.peer_lo[f] = P.peer_g_lo[f] ? P.peer_g_lo[f] - (g + (long long)P.K * P.plane) : 0;
+            rp.peer_hi[f] = P.peer_g_hi[f] ? P.peer_g_hi[f] - (g + (long long)P.n0 * P.plane) : 0;
+        }
+        rp.push_planes = P.K;
+        rp.desc_last = 1;
+        SFB_CUDA(v.rot_push(m1, rp, tti_grid(P, lo, hi, rp.chunk), st));
+    } else {
+        SFB_CUDA(v.rot(m1, rp, tti_grid(P, lo, hi, rp.chunk), st));
+    }
     ++P.launches;
     mark_stream(P, part);
 }
@@ -146,7 +198,8 @@ void tti_rot(Plan& P, long long t, int part) {
 void tti_update(Plan& P, long long t, int part, bool with_points) {
     require(t >= 1 && t <= P.desc.nt - 2, SFB_ERR_PARAMETER, "time index outside [1, nt-1)");
     int lo, hi;
-    part_range(P, part, lo, hi);
+    tti_part_bounds(P, part, lo, hi);
+    const bool fused = part == kPartSlabFused;
     const TtiVariant& v = *P.tti_variant;
     const int cur = int(t & 1), oth = cur ^ 1;
     const int sepi = P.sep ? 1 : 0;
@@ -184,7 +237,20 @@ void tti_update(Plan& P, long long t, int part, bool with_points) {
         m2.e1 = P.tt_c[Plan::TC_E1];
         m2.e2 = P.tt_c[Plan::TC_E2];
         m2.d = P.tt_c[Plan::TC_DAMP];
-        SFB_CUDA(v.div[sepi](m2, dp, tti_grid(P, lo, hi, dp.chunk), st));
+        if (fused) {
+            float* bufs[2] = {dp.po, dp.ro};
+            float* plo[2] = {P.peer_lo[oth], P.peer_r_lo[oth]};
+            float* phi[2] = {P.peer_hi[oth], P.peer_r_hi[oth]};
+            for (int f = 0; f < 2; ++f) {
+                dp.peer_lo[f] = plo[f] ? plo[f] - (bufs[f] + (long long)P.K * P.plane) : 0;
+                dp.peer_hi[f] = phi[f] ? phi[f] - (bufs[f] + (long long)P.n0 * P.plane) : 0;
+            }
+            dp.push_planes = P.K;
+            dp.desc_last = 1;
+            SFB_CUDA(v.div_push[sepi](m2, dp, tti_grid(P, lo, hi, dp.chunk), st));
+        } else {
+            SFB_CUDA(v.div[sepi](m2, dp, tti_grid(P, lo, hi, dp.chunk), st));
+        }
         ++P.launches;
         mark_stream(P, part);
     }
@@ -194,9 +260,10 @@ void tti_update(Plan& P, long long t, int part, bool with_points) {
         const int op = SFB_OP_TTI_FORWARD;
         const int pp = part == SFB_PART_HIGH ? SFB_PART_LOW : part;
         step_points(P, op, t, pp);                                    // p: scatter + gather
-        step_points(P, op, t, pp, P.t_r[oth].as<float>(), false);     // r: scatter
+        step_points(P, op, t, pp, P.t_r[oth].as<float>(), false, nullptr,   // r: scatter
+                    P.peer_r_lo[oth], P.peer_r_hi[oth]);
     }
-    if (part == SFB_PART_ALL || part == SFB_PART_INTERIOR) {
+    if (part == SFB_PART_ALL || part == SFB_PART_INTERIOR || fused) {
         P.live_level[cur] = t;
         P.live_level[oth] = t + 1;
     }

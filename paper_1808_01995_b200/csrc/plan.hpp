@@ -147,13 +147,23 @@ struct Plan {
     // of this slab's ghost planes of the current level: a neighbour may overwrite them (the
     // push of its next boundary half-step) only after it
     cudaEvent_t ev_done = nullptr;
+    // TTI pair on linked slabs: the neighbours' ghost planes of g(p), g(r) (one buffer per
+    // field) and of r (by level parity; those of p are peer_lo / peer_hi), and the event that
+    // closes the first pass of a step (the neighbours' second pass waits on it)
+    float* peer_g_lo[2] = {nullptr, nullptr};
+    float* peer_g_hi[2] = {nullptr, nullptr};
+    float* peer_r_lo[2] = {nullptr, nullptr};
+    float* peer_r_hi[2] = {nullptr, nullptr};
+    cudaEvent_t ev_g = nullptr;
     // neighbours in other processes (sfb_peer_export / sfb_link_peers_ipc): their buffers are
     // mapped through CUDA IPC, and the boundary half-steps are counted in a device word per
     // plan that the neighbours' streams wait on (stream memory operations: no host handshake)
     DevBuf push_flag;                    // [0]: boundary half-steps completed since linking,
                                          // [1]: interior half-steps (ghost-plane readers done)
-    unsigned push_count = 0, done_count = 0;
+    unsigned push_count = 0, done_count = 0, g_count = 0;   // g: word [2], TTI first passes
     void* ipc_u[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [lo/hi][parity], opened
+    void* ipc_g[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [lo/hi][field]
+    void* ipc_r[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [lo/hi][parity]
     void* ipc_flag[2] = {nullptr, nullptr};                         // [lo/hi], opened
     bool main_pending = false, bnd_pending = false;
 

@@ -52,6 +52,12 @@ struct RotParams {
     int N1, N2, pitch;
     long long plane;
     int z_lo, z_hi, chunk;
+    // PUSH kernels (linked slabs, single-launch step): the first `push_planes` planes of g
+    // that the edge block rows output -- block row 0 sweeping up, the last one sweeping down
+    // with desc_last -- are also stored into the neighbour's ghost planes of g: distance in
+    // floats from a node of g[field] to its mirror, low / high group (0 = no neighbour)
+    long long peer_lo[2], peer_hi[2];
+    int push_planes, desc_last;
 };
 
 template <int K, int TXV, int TY, int NS>
@@ -71,7 +77,7 @@ struct RotShape {
     static_assert(GROUP % 32 == 0 && (ABOX * 4) % 128 == 0, "tile shape");
 };
 
-template <int K, int TXV, int TY, int NS>
+template <int K, int TXV, int TY, int NS, bool PUSH = false>
 __global__ void __launch_bounds__(RotShape<K, TXV, TY, NS>::NTHREADS)
 tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotParams p) {
     using S = RotShape<K, TXV, TY, NS>;
@@ -92,6 +98,12 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
     const int zb = p.z_lo + blockIdx.z * p.chunk;
     const int ze = min(zb + p.chunk, p.z_hi);
     const int nplanes = (ze - zb) + 2 * K;
+    // sweep direction (PUSH kernels only; see acoustic_step_kernel): iteration n loads buffer
+    // plane zl0 + dir n and, from n = 2K on, outputs local plane zo0 + dir (n - 2K)
+    const bool desc = PUSH && p.desc_last && gridDim.z > 1 && blockIdx.z == gridDim.z - 1;
+    const int dir = desc ? -1 : 1;
+    const int zl0 = desc ? ze - 1 + 2 * K : zb;
+    const int zo0 = desc ? ze - 1 : zb;
 
     if (tid == 0) {
 #pragma unroll
@@ -115,10 +127,10 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                 const int feed_b = 2 * ABOX, rest_b = 2 * S::CBOX + 3 * ABOX;
                 mbar_arrive_expect_tx(full + s, (feed_b + (out ? rest_b : 0)) * 4);
                 // every field lives in the wavefield layout: buffer plane = local plane + K
-                tma_load_3d(st, &tm.f0_feed, x0, y0, zb + n, full + s);
-                tma_load_3d(st + ABOX, &tm.f1_feed, x0, y0, zb + n, full + s);
+                tma_load_3d(st, &tm.f0_feed, x0, y0, zl0 + dir * n, full + s);
+                tma_load_3d(st + ABOX, &tm.f1_feed, x0, y0, zl0 + dir * n, full + s);
                 if (out) {
-                    const int zc = zb + n - K;  // centre plane (buffer index)
+                    const int zc = zo0 + dir * (n - 2 * K) + K;  // centre plane (buffer index)
                     tma_load_3d(st + OFF_CTR, &tm.f0_ctr, x0 - KP, y0 - K, zc, full + s);
                     tma_load_3d(st + OFF_CTR + CPAD, &tm.f1_ctr, x0 - KP, y0 - K, zc, full + s);
                     tma_load_3d(st + OFF_PLAIN, &tm.a, x0, y0, zc, full + s);
@@ -141,10 +153,15 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
     const int x = x0 + 4 * tx, y = y0 + ty;
     const bool rin = x < p.N2 && y < p.N1;
     const bool lane0 = (tid & 31) == 0;
-    long long go = p.out_off + (long long)zb * p.plane + (long long)y * p.pitch + x;
+    long long go = p.out_off + (long long)zo0 * p.plane + (long long)y * p.pitch + x;
     float* const og = p.g[field];
     float* const ob = p.bg[field];
-    long long lo_off = (long long)zb * p.plane + (long long)y * p.pitch + x;   // compact
+    long long lo_off = (long long)zo0 * p.plane + (long long)y * p.pitch + x;   // compact
+    const long long zstep = desc ? -p.plane : p.plane;
+    long long peer_delta = 0;
+    if constexpr (PUSH)
+        peer_delta = blockIdx.z == 0 ? p.peer_lo[field]
+                                     : (blockIdx.z == gridDim.z - 1 ? p.peer_hi[field] : 0);
 
     // the d0 queue is a sliding window of 2K+2 slots: the plane loop is unrolled by two (plane
     // n uses slots [0, 2K], plane n+1 slots [1, 2K+1]) and the window moves by two slots
@@ -205,6 +222,12 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                             l01 = f2_fma(wl, f2_add(hi01, lo01), l01);
                             l23 = f2_fma(wl, f2_add(hi23, lo23), l23);
                         }
+                    }
+                    // a downward sweep holds the queue in reverse: the first derivative (odd in
+                    // d0, unlike the Laplacian) comes out with the opposite sign, exactly
+                    if (PUSH && desc) {
+                        d01 = make_float2(-d01.x, -d01.y);
+                        d23 = make_float2(-d23.x, -d23.y);
                     }
                     g01 = f2_mul(make_float2(a4.x, a4.y), d01);
                     g23 = f2_mul(make_float2(a4.z, a4.w), d23);
@@ -296,14 +319,19 @@ tti_rot_kernel(const __grid_constant__ RotMaps tm, const __grid_constant__ RotPa
                     __stcs(reinterpret_cast<float4*>(og + go), make_float4(g[0], g[1], g[2], g[3]));
                     __stcs(reinterpret_cast<float4*>(ob + go),
                            make_float4(b4.x * g[0], b4.y * g[1], b4.z * g[2], b4.w * g[3]));
+                    if constexpr (PUSH) {   // the neighbour differentiates a g along d0: g only
+                        if (peer_delta && n - 2 * K < p.push_planes)
+                            *reinterpret_cast<float4*>(og + go + peer_delta) =
+                                make_float4(g[0], g[1], g[2], g[3]);
+                    }
                 }
             };
             if (field == 0)   // warp-uniform
                 body(std::true_type{});
             else
                 body(std::false_type{});
-            lo_off += p.plane;
-            go += p.plane;
+            lo_off += zstep;
+            go += zstep;
         }
         if (++s == NS) {
             s = 0;
@@ -343,6 +371,10 @@ struct DivParams {
     int N1, N2, pitch;
     long long plane;
     int z_lo, z_hi, chunk;
+    // PUSH kernels: mirrors of the new p (index 0) / r (index 1) planes in the neighbours'
+    // ghost planes, as in RotParams
+    long long peer_lo[2], peer_hi[2];
+    int push_planes, desc_last;
 };
 
 template <int K, int TXV, int TY, int NS, bool SEP>
@@ -364,7 +396,7 @@ struct DivShape {
     static_assert(GROUP % 32 == 0 && (ABOX * 4) % 128 == 0 && (YBOX * 4) % 128 == 0, "tile shape");
 };
 
-template <int K, int TXV, int TY, int NS, bool SEP>
+template <int K, int TXV, int TY, int NS, bool SEP, bool PUSH = false>
 __global__ void __launch_bounds__(DivShape<K, TXV, TY, NS, SEP>::NTHREADS)
 tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant__ DivParams p) {
     using S = DivShape<K, TXV, TY, NS, SEP>;
@@ -385,6 +417,10 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
     const int zb = p.z_lo + blockIdx.z * p.chunk;
     const int ze = min(zb + p.chunk, p.z_hi);
     const int nplanes = (ze - zb) + 2 * K;
+    const bool desc = PUSH && p.desc_last && gridDim.z > 1 && blockIdx.z == gridDim.z - 1;
+    const int dir = desc ? -1 : 1;
+    const int zl0 = desc ? ze - 1 + 2 * K : zb;
+    const int zo0 = desc ? ze - 1 : zb;
 
     if (tid == 0) {
 #pragma unroll
@@ -407,11 +443,11 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
                 float* st = ring + s * STAGE;
                 mbar_arrive_expect_tx(
                     full + s, (3 * ABOX + (out ? 2 * YBOX + 3 * S::XBOX + NPL * ABOX : 0)) * 4);
-                tma_load_3d(st, &tm.g0, x0, y0, zb + n, full + s);
-                tma_load_3d(st + ABOX, &tm.g1, x0, y0, zb + n, full + s);
-                tma_load_3d(st + 2 * ABOX, &tm.a, x0, y0, zb + n, full + s);
+                tma_load_3d(st, &tm.g0, x0, y0, zl0 + dir * n, full + s);
+                tma_load_3d(st + ABOX, &tm.g1, x0, y0, zl0 + dir * n, full + s);
+                tma_load_3d(st + 2 * ABOX, &tm.a, x0, y0, zl0 + dir * n, full + s);
                 if (out) {
-                    const int zo = zb + n - 2 * K;  // output plane (compact); buffer plane zo + K
+                    const int zo = zo0 + dir * (n - 2 * K);  // output plane (compact); buffer plane zo + K
                     const int zc = zo + K;
                     tma_load_3d(st + OFF_Y, &tm.bg0, x0, y0 - K, zc, full + s);
                     tma_load_3d(st + OFF_Y + YBOX, &tm.bg1, x0, y0 - K, zc, full + s);
@@ -444,7 +480,12 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
     const int x = x0 + 4 * tx, y = y0 + ty;
     const bool rin = x < p.N2 && y < p.N1;
     const bool lane0 = (tid & 31) == 0;
-    float* outp = (field ? p.ro : p.po) + (long long)(zb + K) * p.plane + (long long)y * p.pitch + x;
+    float* outp = (field ? p.ro : p.po) + (long long)(zo0 + K) * p.plane + (long long)y * p.pitch + x;
+    const long long zstep = desc ? -p.plane : p.plane;
+    long long peer_delta = 0;
+    if constexpr (PUSH)
+        peer_delta = blockIdx.z == 0 ? p.peer_lo[field]
+                                     : (blockIdx.z == gridDim.z - 1 ? p.peer_hi[field] : 0);
 
     float dxy[4] = {0.f, 0.f, 0.f, 0.f};
     if (SEP && rin) {
@@ -494,6 +535,10 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
                                        make_float2(SFB_TQ(K - j)[0], SFB_TQ(K - j)[1])), a01);
                 a23 = f2_fma(w, f2_sub(make_float2(SFB_TQ(K + j)[2], SFB_TQ(K + j)[3]),
                                        make_float2(SFB_TQ(K - j)[2], SFB_TQ(K - j)[3])), a23);
+            }
+            if (PUSH && desc) {   // reversed queue: D0 is odd in d0 (see tti_rot_kernel)
+                a01 = make_float2(-a01.x, -a01.y);
+                a23 = make_float2(-a23.x, -a23.y);
             }
             {   // D1 (b g): rows above and below in the d1-haloed box
                 const float* colp = st + OFF_Y + field * YBOX + ty * TX + 4 * tx;
@@ -560,7 +605,7 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
             float4 dm4 = make_float4(0.f, 0.f, 0.f, 0.f);
             if (!SEP) dm4 = *reinterpret_cast<const float4*>(ap + A_D * ABOX);
             float dzv = 0.f;
-            if (SEP) dzv = __ldg(p.dz + (zb + n - 2 * K));
+            if (SEP) dzv = __ldg(p.dz + (zo0 + dir * (n - 2 * K)));
             const float lpv[4] = {lp4.x, lp4.y, lp4.z, lp4.w}, rmv[4] = {rm4.x, rm4.y, rm4.z, rm4.w};
             const float e1v[4] = {e14.x, e14.y, e14.z, e14.w}, e2v[4] = {e24.x, e24.y, e24.z, e24.w};
             const float olv[4] = {ol4.x, ol4.y, ol4.z, ol4.w}, cuv[4] = {cu4.x, cu4.y, cu4.z, cu4.w};
@@ -582,8 +627,15 @@ tti_div_update_kernel(const __grid_constant__ DivMaps tm, const __grid_constant_
             // un[0] depends on every shared-memory load of the iteration (see mbar_release)
             __syncwarp();
             if (lane0) mbar_release(done + s, un[0]);
-            if (rin) __stcs(reinterpret_cast<float4*>(outp), make_float4(un[0], un[1], un[2], un[3]));
-            outp += p.plane;
+            if (rin) {
+                __stcs(reinterpret_cast<float4*>(outp), make_float4(un[0], un[1], un[2], un[3]));
+                if constexpr (PUSH) {
+                    if (peer_delta && n - 2 * K < p.push_planes)
+                        *reinterpret_cast<float4*>(outp + peer_delta) =
+                            make_float4(un[0], un[1], un[2], un[3]);
+                }
+            }
+            outp += zstep;
         }
         if (++s == NS) {
             s = 0;

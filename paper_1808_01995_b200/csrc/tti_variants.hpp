@@ -29,21 +29,27 @@ struct TtiVariant {
     const void* f_div[2];
     cudaError_t (*rot)(const RotMaps&, const RotParams&, dim3, cudaStream_t);
     cudaError_t (*div[2])(const DivMaps&, const DivParams&, dim3, cudaStream_t);
+    // the same kernels with the fused halo push (linked slabs)
+    const void* f_rot_push;
+    const void* f_div_push[2];
+    cudaError_t (*rot_push)(const RotMaps&, const RotParams&, dim3, cudaStream_t);
+    cudaError_t (*div_push[2])(const DivMaps&, const DivParams&, dim3, cudaStream_t);
 };
 
 std::vector<TtiVariant>& tti_variant_registry();
 
-template <int K>
+template <int K, bool PUSH = false>
 cudaError_t launch_rot(const RotMaps& tm, const RotParams& p, dim3 grid, cudaStream_t st) {
     using S = RotShape<K, kTtiTXV, kTtiTY, kTtiNS>;
-    return launch_pdl(&tti_rot_kernel<K, kTtiTXV, kTtiTY, kTtiNS>, grid, S::NTHREADS, S::SMEM, st, tm, p);
+    return launch_pdl(&tti_rot_kernel<K, kTtiTXV, kTtiTY, kTtiNS, PUSH>, grid, S::NTHREADS, S::SMEM,
+                      st, tm, p);
 }
 
-template <int K, bool SEP>
+template <int K, bool SEP, bool PUSH = false>
 cudaError_t launch_div(const DivMaps& tm, const DivParams& p, dim3 grid, cudaStream_t st) {
     using S = DivShape<K, kTtiTXV, kTtiTY, kTtiNSDiv, SEP>;
-    return launch_pdl(&tti_div_update_kernel<K, kTtiTXV, kTtiTY, kTtiNSDiv, SEP>, grid, S::NTHREADS,
-                      S::SMEM, st, tm, p);
+    return launch_pdl(&tti_div_update_kernel<K, kTtiTXV, kTtiTY, kTtiNSDiv, SEP, PUSH>, grid,
+                      S::NTHREADS, S::SMEM, st, tm, p);
 }
 
 template <int K>
@@ -66,6 +72,14 @@ void register_tti() {
     v.rot = &launch_rot<K>;
     v.div[0] = &launch_div<K, false>;
     v.div[1] = &launch_div<K, true>;
+    v.f_rot_push = reinterpret_cast<const void*>(&tti_rot_kernel<K, kTtiTXV, kTtiTY, kTtiNS, true>);
+    v.f_div_push[0] = reinterpret_cast<const void*>(
+        &tti_div_update_kernel<K, kTtiTXV, kTtiTY, kTtiNSDiv, false, true>);
+    v.f_div_push[1] = reinterpret_cast<const void*>(
+        &tti_div_update_kernel<K, kTtiTXV, kTtiTY, kTtiNSDiv, true, true>);
+    v.rot_push = &launch_rot<K, true>;
+    v.div_push[0] = &launch_div<K, false, true>;
+    v.div_push[1] = &launch_div<K, true, true>;
     tti_variant_registry().push_back(v);
 }
 

@@ -337,32 +337,28 @@ ExecutionReport run_wave_slabs(WaveOp& w, const SeismicModel& model, const TtiMo
         e.check(sfb_step_begin(e.plan(), op, 0));
         lo = hi;
     }
-    auto sync_all = [&] {
-        for (auto& e : eng) e->check(sfb_stream_sync(e->plan()));
-    };
-    // ghost planes of `which` between every pair of neighbouring slabs
-    auto exchange = [&](int which, long t) {
-        sync_all();
-        for (long i = 0; i + 1 < nslab; ++i) {
-            Engine &a = *eng[std::size_t(i)], &b = *eng[std::size_t(i + 1)];
-            void *a_slo, *a_shi, *a_rlo, *a_rhi, *b_slo, *b_shi, *b_rlo, *b_rhi;
-            int64_t n = 0;
-            a.check(sfb_tti_halo_blocks(a.plan(), which, t, &a_slo, &a_shi, &a_rlo, &a_rhi, &n));
-            b.check(sfb_tti_halo_blocks(b.plan(), which, t, &b_slo, &b_shi, &b_rlo, &b_rhi, &n));
-            b.check(sfb_copy_halo(b.plan(), b_rlo, a_shi, n));
-            a.check(sfb_copy_halo(a.plan(), a_rhi, b_slo, n));
+    // the plans are linked (after the TTI fields are bound: the link maps g and r as well):
+    // each pass of a step is one launch per slab whose edge chunks push their boundary planes
+    // into the neighbours' ghost planes; events order the slabs, nothing is copied
+    for (long i = 0; i < nslab; ++i) {
+        Engine& e = *eng[std::size_t(i)];
+        e.check(sfb_link_peers(e.plan(), i > 0 ? eng[std::size_t(i - 1)]->plan() : nullptr,
+                               i + 1 < nslab ? eng[std::size_t(i + 1)]->plan() : nullptr));
+    }
+    for (auto& e : eng) e->check(sfb_stream_sync(e->plan()));
+    auto for_neighbours = [&](auto&& wait) {
+        for (long i = 0; i < nslab; ++i) {
+            Engine& e = *eng[std::size_t(i)];
+            if (i > 0) e.check(wait(e.plan(), eng[std::size_t(i - 1)]->plan()));
+            if (i + 1 < nslab) e.check(wait(e.plan(), eng[std::size_t(i + 1)]->plan()));
         }
-        sync_all();
     };
-    sync_all();
     const auto t0 = std::chrono::steady_clock::now();
     for (long t = 1; t < w.nt - 1; ++t) {
-        for (auto& e : eng) e->check(sfb_tti_step_rot(e->plan(), t, SFB_PART_ALL));
-        exchange(SFB_TTI_HALO_G_P, t);
-        exchange(SFB_TTI_HALO_G_R, t);
-        for (auto& e : eng) e->check(sfb_tti_step_update(e->plan(), t, SFB_PART_ALL));
-        exchange(SFB_TTI_HALO_P, t);
-        exchange(SFB_TTI_HALO_R, t);
+        for (auto& e : eng) e->check(sfb_tti_step_rot_fused(e->plan(), t));
+        for_neighbours(sfb_tti_peer_wait_g);
+        for (auto& e : eng) e->check(sfb_tti_step_update_fused(e->plan(), t));
+        for_neighbours(sfb_peer_wait);
     }
     for (auto& e : eng) e->check(sfb_step_end(e->plan(), op));
     const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

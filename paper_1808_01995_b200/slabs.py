@@ -284,6 +284,25 @@ class PeerPushDriver:
             self.plan.peer_wait_ipc()
 
 
+class TtiPeerPushDriver(PeerPushDriver):
+    """The TTI pair with the fused halo push between processes: link after
+    sfb_set_model_tti (the blob then carries the handles of g(p), g(r) and r as well); each pass
+    of a step is one launch per slab that pushes its boundary planes, the ranks are ordered by
+    three device-side counters (first pass done / pushes landed / ghost readers done)."""
+
+    def __init__(self, plan, rank: int, world: int, group=None):
+        from . import capi
+        super().__init__(plan, capi.OP_TTI_FORWARD, rank, world, group)
+
+    def run(self, t_from: int, t_to: int, backward=False):
+        assert not backward, "the TTI operator is forward-only"
+        for t in range(t_from, t_to):
+            self.plan.tti_step_rot_fused(t)
+            self.plan.tti_peer_wait_g_ipc()
+            self.plan.tti_step_update_fused(t)
+            self.plan.peer_wait_ipc()
+
+
 # ---- bench.py at N > 1 ----------------------------------------------------------------------
 
 def weak_extent(per_rank: int, world: int) -> int:

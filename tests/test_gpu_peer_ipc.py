@@ -45,6 +45,46 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
+def _tti_inputs():
+    from tests.test_gpu_tti import tti_fields, tti_problem
+    model, geom = tti_problem([44, 26, 30], 8, 30)
+    return model, geom, tti_fields(model.N, seed=3)
+
+
+def _tti_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from paper_1808_01995_b200 import capi, slabs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    model, geom, fields = _tti_inputs()
+    bounds = slabs.split_slabs(model.N[0], world, 4)
+    plan = make_plan(model, geom, 8, slab=bounds[rank])
+    plan.set_model_tti(*fields)
+    plan.upload_traces(capi.CLOUD_SRC, geom.src)
+    drv = slabs.TtiPeerPushDriver(plan, rank, world)
+    plan.step_begin(capi.OP_TTI_FORWARD)
+    plan.sync()
+    dist.barrier()
+    drv.run(1, geom.nt - 1)
+    plan.step_end(capi.OP_TTI_FORWARD)
+    rec = torch.from_numpy(plan.download_traces(capi.CLOUD_REC))
+    p, r = np.zeros(model.N), np.zeros(model.N)
+    plan.wavefield(geom.nt - 1, out=p, field=0)
+    plan.wavefield(geom.nt - 1, out=r, field=1)
+    p, r = torch.from_numpy(p), torch.from_numpy(r)
+    for x in (rec, p, r):
+        dist.all_reduce(x)
+    dist.barrier()
+    if rank == 0:
+        np.save(out + "_rec.npy", rec.numpy())
+        np.save(out + "_p.npy", p.numpy())
+        np.save(out + "_r.npy", r.numpy())
+    plan.close()
+    dist.destroy_process_group()
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -64,3 +104,20 @@ def test_peer_push_between_processes_matches_single_domain(tmp_path, world):
     assert np.abs(rec1).max() > 0
     assert np.array_equal(np.load(out + "_rec.npy"), rec1)
     assert np.array_equal(np.load(out + "_u.npy"), u1)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tti_peer_push_between_processes_matches_single_domain(tmp_path, world):
+    import torch.multiprocessing as mp
+    model, geom, fields = _tti_inputs()
+    plan = make_plan(model, geom, 8)
+    plan.set_model_tti(*fields)
+    rec1, _ = plan.tti_forward(geom.src)
+    p1 = plan.wavefield(geom.nt - 1, field=0)
+    r1 = plan.wavefield(geom.nt - 1, field=1)
+    plan.close()
+    out = str(tmp_path / "ipc_tti")
+    mp.spawn(_tti_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert np.abs(rec1).max() > 0
+    assert np.array_equal(np.load(out + "_rec.npy"), rec1)
+    assert np.array_equal(np.load(out + "_p.npy"), p1) and np.array_equal(np.load(out + "_r.npy"), r1)

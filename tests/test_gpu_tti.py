@@ -135,15 +135,37 @@ def test_tti_through_the_host_layer():
         H.tti_forward_operator(model, tti, geom2, order)
 
 
-def _run_tti_slabs(model, geom, order, fields, cuts, overlap_parts=True):
+def _run_tti_slabs(model, geom, order, fields, cuts, overlap_parts=True, pushed=False, stall=None):
     """N TTI plans on one device stepping in lockstep with device-to-device ghost copies:
-    the single-GPU emulation of the two-exchange slab protocol (include/sfb200.h)."""
+    the single-GPU emulation of the two-exchange slab protocol (include/sfb200.h).  pushed:
+    the plans are linked instead and every pass stores its boundary planes straight into the
+    neighbours' ghost planes (no copies, no host synchronisation inside the loop)."""
     from paper_1808_01995_b200 import capi
     plans = [make_plan(model, geom, order, slab=(cuts[i], cuts[i + 1])) for i in range(len(cuts) - 1)]
     for p in plans:
         p.set_model_tti(*fields)
         p.upload_traces(capi.CLOUD_SRC, geom.src)
         p.step_begin(capi.OP_TTI_FORWARD)
+    if pushed:
+        nb = lambda i: [plans[j] for j in (i - 1, i + 1) if 0 <= j < len(plans)]   # noqa: E731
+        for i, p in enumerate(plans):
+            p.link_peers(plans[i - 1] if i > 0 else None, plans[i + 1] if i + 1 < len(plans) else None)
+        for p in plans:
+            p.sync()
+        for t in range(1, geom.nt - 1):
+            for i, p in enumerate(plans):
+                if stall and i == stall[0]:
+                    p.debug_stall(0, stall[1])
+                p.tti_step_rot_fused(t)
+            for i, p in enumerate(plans):
+                for q in nb(i):
+                    p.tti_peer_wait_g(q)
+            for p in plans:
+                p.tti_step_update_fused(t)
+            for i, p in enumerate(plans):
+                for q in nb(i):
+                    p.peer_wait(q)
+        return _collect_tti(plans, model, geom)
 
     def exchange(which, t):
         for p in plans:
@@ -168,6 +190,11 @@ def _run_tti_slabs(model, geom, order, fields, cuts, overlap_parts=True):
                 p.tti_step_update(t, part)
         exchange(capi.TTI_HALO_P, t)
         exchange(capi.TTI_HALO_R, t)
+    return _collect_tti(plans, model, geom)
+
+
+def _collect_tti(plans, model, geom):
+    from paper_1808_01995_b200 import capi
     rec = np.zeros((geom.nt, geom.n_rec))
     pf, rf = np.zeros(model.N), np.zeros(model.N)
     for p in plans:
@@ -199,6 +226,28 @@ def test_tti_slab_decomposition_matches_single_domain_bitwise(order, parts):
     cuts = [0, 2 * K + 3, src_plane + 1, n0]      # the source cell straddles the second cut
     rec3, p3, r3 = _run_tti_slabs(model, geom, order, fields, cuts, overlap_parts=parts)
     assert np.array_equal(rec3, rec1)
+    assert np.array_equal(p3, p1) and np.array_equal(r3, r1)
+
+
+@pytest.mark.parametrize("order,stall", [(8, None), (12, None), (8, (1, 300)), (8, (0, 300))])
+def test_tti_fused_halo_push_matches_single_domain_bitwise(order, stall):
+    """Linked TTI slabs: each pass is one launch per slab whose edge chunks sweep towards the
+    interior and push their boundary planes (g in the first pass, the new p and r in the
+    second) into the neighbours' ghost planes; events order the slabs.  Bit for bit the
+    single-domain run, also with one slab's stream held back 300 us every step."""
+    model, geom = tti_problem([48, 26, 30], order, 40)
+    fields = tti_fields(model.N, seed=3)
+    plan = make_plan(model, geom, order)
+    plan.set_model_tti(*fields)
+    rec1, _ = plan.tti_forward(geom.src)
+    p1 = plan.wavefield(geom.nt - 1, field=0)
+    r1 = plan.wavefield(geom.nt - 1, field=1)
+    plan.close()
+    K = order // 2
+    src_plane = int(geom.src_base[0][0])
+    cuts = [0, 2 * K + 3, src_plane + 1, model.N[0]]
+    rec3, p3, r3 = _run_tti_slabs(model, geom, order, fields, cuts, pushed=True, stall=stall)
+    assert np.abs(rec1).max() > 0 and np.array_equal(rec3, rec1)
     assert np.array_equal(p3, p1) and np.array_equal(r3, r1)
 
 
