@@ -192,6 +192,16 @@ class Workload:
             self._build_slab_local(nsteps, syn, capi)
         else:
             self._build_global(nsteps, syn)
+        if world > 1:
+            # a point is sampled by the rank that owns its base plane: a rank binds -- and later
+            # downloads -- only its own receivers (the record is the concatenation over ranks)
+            lo, hi = self.slab
+            own = (self.rec_base[:, 0] >= lo) & (self.rec_base[:, 0] < hi)
+            self.n_rec_global = int(self.rec_base.shape[0])
+            self.rec_base, self.rec_w = self.rec_base[own], self.rec_w[own]
+            if self.rec_base.shape[0] == 0:   # keep the cloud non-empty: one receiver of the rank below
+                self.rec_base = np.array([[lo, 0, 0]], dtype=np.int64)
+                self.rec_w = np.zeros((1, 8))
         log(f"[bench] rank {rank}: workload {config} built in {time.time() - t0:.1f}s: N={self.N} "
             f"dt={self.dt:.6f} nt={self.nt} n_src={self.src_base.shape[0]} n_rec={self.rec_base.shape[0]}")
 

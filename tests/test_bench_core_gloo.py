@@ -119,3 +119,25 @@ def test_slab_local_generators_agree_with_the_global_model():
     a = syn.smooth_slab([64, 48, 40], 10, 30, 7, 4.0, 1.5, 4.5)
     b = syn.smooth_slab([64, 48, 40], 20, 44, 7, 4.0, 1.5, 4.5)
     assert np.array_equal(a[10:], b[:10]) and 1.5 <= a.min() < a.max() <= 4.5
+
+
+def test_bench_workload_deals_every_receiver_to_exactly_one_rank(monkeypatch):
+    """bench.Workload at N > 1 (host side only): slab bounds, the receivers a rank binds."""
+    import bench
+    monkeypatch.setitem(bench.CONFIGS[2], "n", 48)
+    world, seen, total = 4, [], None
+    for rank in range(world):
+        wl = bench.Workload(2, "forward", 6, rank, world, "strong")
+        lo, hi = wl.slab
+        assert wl.bounds == slabs.split_slabs(48 + 2 * bench.NBL, world, 4)
+        assert ((wl.rec_base[:, 0] >= lo) & (wl.rec_base[:, 0] < hi)).all()
+        total = wl.n_rec_global
+        real = wl.rec_w.any(axis=1)    # a rank without receivers binds one weightless dummy
+        seen.append({tuple(b) for b in wl.rec_base[real]})
+        assert wl.src_base.shape[0] == 1 and wl.nt == 8
+    assert sum(len(s) for s in seen) == total == 48 * 48
+    assert len(set().union(*seen)) == total
+    # the weak-scaling series grows the slab axis with the rank count
+    N, phys = bench.grid_of(5, 8, "weak")
+    assert phys == [1024, 1024, 1024] and N == [1104] * 3
+    assert bench.grid_of(5, 2, "weak")[1] == [256, 1024, 1024]
