@@ -478,6 +478,25 @@ def oracle_dense(N, order, dt, steps, threads=None):
     return float(np.prod(N)) * steps / sec / 1e9, o.num_threads(), sec
 
 
+def oracle_tti(planes, order, nsteps):
+    """The builder's f64 TTI restatement (oracle/sf_oracle.c, OpenMP) on a planes x 592 x 592
+    cut of configs[3]'s grid with analytic Thomsen fields; returns (GPts/s, threads, seconds).
+    The reference has no TTI operator: this port is the only CPU implementation there is."""
+    from oracle import oracle as o
+    n = CONFIGS[4]["n"]
+    phys = [max(planes - 2 * NBL, 16), n, n]
+    om = o.Model(phys, [H] * 3, [0.0] * 3, np.full(phys, 3.0), NBL, order)
+    dt = o.tti_critical_dt(om, order, 0.3)
+    c = H * (n - 1) / 2.0 + H / 4.0
+    og = o.Geometry(om, [H * (phys[0] - 1) / 2.0, c, 18.75], [[0.0, c, 25.0]], 0.0, (nsteps + 1.5) * dt,
+                    dt, 0.015)
+    eps, delta, theta, phi = cheap_tti_fields(om.N)
+    t0 = time.time()
+    o.tti_forward(om, og, order, eps, delta, theta, phi)
+    sec = time.time() - t0
+    return float(np.prod(om.N)) * nsteps / sec / 1e9, o.num_threads(), sec, om.N
+
+
 def reference_inputs(config, planes, vel=None):
     """configs[1] / configs[4] inputs cut to `planes` physical planes along the slowest axis
     (the whole workload when planes = the configuration's extent)"""
@@ -552,6 +571,16 @@ def reference_arm(args):
                   + ("" if planes == phys[0] else f", {planes} of {phys[0]} physical planes along the "
                      "slowest axis (bounded sample)")
                   + f": {K} time steps incl. source injection and receiver sampling, order {order}")
+    elif op == "tti":
+        kind = "port"
+        g1, cores, s1, N1 = oracle_tti(96, order, 1)
+        rate = float(np.prod(N1)) / s1
+        planes = int(max(96, min(N[0], budget * rate / (K + W) / (n1 * n1), 2.5e8 / (n1 * n1))))
+        oracle_tti(planes, order, W)
+        gpts, cores, sec, Nt = oracle_tti(planes, order, K)
+        sample = (f"{K} time steps of the builder's f64 TTI restatement (oracle/sf_oracle.c, OpenMP, "
+                  f"{cores} threads) on {Nt[0]}x{Nt[1]}x{Nt[2]} computed nodes (configs[3]: 592^3), order {order}, "
+                  "analytic Thomsen fields; the reference itself has no TTI operator")
     else:
         kind = "port"
         from paper_1808_01995_b200 import capi
@@ -585,6 +614,12 @@ def cpu_baseline_leg(config, vel=None):
     c = CONFIGS[config]
     order, n1 = c["order"], c["n"] + 2 * NBL
     dt = capi.critical_dt([H] * 3, 4.5, order)
+    if config == 4:   # the TTI pair: the builder's f64 restatement is the only CPU implementation
+        g, cores, s, Nt = oracle_tti(176, order, 3)
+        return {"value": g, "unit": "GPts/s", "cores": cores, "kind": "port",
+                "sample": f"3 time steps of the f64 TTI restatement (oracle/sf_oracle.c, OpenMP) on "
+                          f"{Nt[0]}x{Nt[1]}x{Nt[2]} computed nodes, order {order}, {s:.1f} s; the reference "
+                          "has no TTI operator"}
     planes, nst = (336, 10) if config != 5 else (96, 10)
     oracle_dense([planes, n1, n1], order, dt, 1)            # first touch of the oracle's buffers
     g, cores, s = oracle_dense([planes, n1, n1], order, dt, nst)
