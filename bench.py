@@ -842,6 +842,9 @@ def ours(args):
     if not torch.cuda.is_available() or capi.device_count() < 1:
         raise SystemExit("bench.py needs a CUDA device: there is no CPU fallback")
     if world > 1 or os.environ.get("SFB_BENCH_FORCE_DIST"):
+        if args.op in ("adjoint", "gradient"):
+            raise SystemExit("N > 1 runs time the forward operators (acoustic, TTI); the backward sweeps "
+                             "decompose the same way (tests/test_gpu_acoustic.py) but have no bench loop")
         return multi_gpu(args)
     return single_gpu(args)
 

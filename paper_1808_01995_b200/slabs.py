@@ -365,6 +365,8 @@ def bench_core(comm: Comm, job, K: int, W: int):
     t0 = _time.perf_counter()
     h2d = job.upload()
     job.begin()
+    job.sync()
+    comm.barrier()   # as above: no push may land in a field its owner is still zeroing
     job.loop(1, 1 + K)
     d2h = job.download()
     job.sync()
