@@ -783,7 +783,11 @@ def multi_gpu(args):
     from paper_1808_01995_b200 import capi, slabs
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # SFB_BENCH_DEVICE / SFB_BENCH_BACKEND=gloo: functional check of this code path with several
+    # ranks sharing ONE device (CUDA IPC works between contexts on a device, NCCL does not
+    # accept it); a number measured that way means nothing
+    local = int(os.environ.get("SFB_BENCH_DEVICE", os.environ.get("LOCAL_RANK", rank)))
+    backend = os.environ.get("SFB_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     # NCCL prints its banner (and, with NCCL_DEBUG=INFO, its communicator lines) on stdout;
     # the contract is ONE JSON line there, so stdout is parked on stderr until the line is ready
@@ -795,8 +799,11 @@ def multi_gpu(args):
     os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator lines -> stderr
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if world > 1 or os.environ.get("SFB_BENCH_INIT_PG"):
-        dist.init_process_group("nccl", rank=rank, world_size=world,
-                                device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
     K, W = args.steps, max(args.warmup, 3)
     config, op = args.config, args.op
     wl = Workload(config, op, W + K, rank, world, args.scaling)
@@ -805,7 +812,7 @@ def multi_gpu(args):
     sep = bool(plan.get_tile()["sep"])
     plan.upload_traces(capi.CLOUD_SRC, wl.src)
     job = SlabJob(wl, plan, op, local, rank, world)
-    comm = slabs.Comm(rank, world, torch.device(f"cuda:{local}"))
+    comm = slabs.Comm(rank, world, torch.device(f"cuda:{local}") if backend == "nccl" else None)
     with ClockSampler(local) as clk:
         meas = slabs.bench_core(comm, job, K, W)
     clocks = clk.summary()
