@@ -75,8 +75,9 @@ __device__ __forceinline__ void patch_stencil(const StencilCoef& k, const float 
             hprev = hj;
         }
     }
-    // d2: one row segment per patch row, scalar (the shifted operands are not aligned pairs)
-    float ax[4] = {0.f, 0.f, 0.f, 0.f};
+    // d2: one row segment per patch row; even j: the operand pair (xr[KE-j], xr[KE+1-j]) is a
+    // register-aligned float2 and runs packed, odd j stays scalar (same roundings per node)
+    float ax[4];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         float xr[2 * KE + 2];
@@ -92,11 +93,20 @@ __device__ __forceinline__ void patch_stencil(const StencilCoef& k, const float 
                 xr[2 * v + 1] = t2.y;
             }
         }
+        float2 x2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int j = 1; j <= K; ++j)
-                ax[2 * r + c] = fmaf(k.cx[j - 1], xr[KE + c - j] + xr[KE + c + j], ax[2 * r + c]);
+        for (int j = 1; j <= K; ++j) {
+            if (j % 2 == 0) {
+                x2 = f2_fma(f2_splat(k.cx[j - 1]),
+                            f2_add(make_float2(xr[KE - j], xr[KE + 1 - j]),
+                                   make_float2(xr[KE + j], xr[KE + 1 + j])), x2);
+            } else {
+                x2.x = fmaf(k.cx[j - 1], xr[KE - j] + xr[KE + j], x2.x);
+                x2.y = fmaf(k.cx[j - 1], xr[KE + 1 - j] + xr[KE + 1 + j], x2.y);
+            }
+        }
+        ax[2 * r] = x2.x;
+        ax[2 * r + 1] = x2.y;
     }
     a01 = f2_add(a01, make_float2(ax[0], ax[1]));
     a23 = f2_add(a23, make_float2(ax[2], ax[3]));

@@ -188,8 +188,6 @@ void register_all_for_K() {
     if constexpr (K >= 6) {
         register_patch<K, 4, false, 2>();
         register_patch<K, 4, true, 2>();
-        register_patch<K, 3, false, 2>();
-        register_patch<K, 3, true, 2>();
     }
     if constexpr (K <= 4) {  // unrolling by 2K+1 overflows the instruction cache above
         register_rotated_pair<K, 16, 16, 3>();

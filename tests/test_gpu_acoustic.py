@@ -195,8 +195,8 @@ def test_patch_kernel_agrees_bitwise_with_the_dual_stream_kernel(order):
         plan.set_points(capi.CLOUD_REC, geom.rec_base, geom.rec_w)
         out = {}
         rows = 14 if order >= 14 else 16
-        for name, tile in (("dual", (16, rows, -4)), ("patch4", (16, 14, -204)),
-                           ("patch3", (16, 14, -203)), ("slide", (16, rows, -304))):
+        for name, tile in (("dual", (16, rows, -4)), ("patch", (16, 14, -204)),
+                           ("slide", (16, rows, -304))):
             for chunk in (0, 11):
                 plan.set_tile(*tile, chunk)
                 assert plan.get_tile()["stages"] == tile[2]
