@@ -5,6 +5,8 @@
 // then step t over [1, nt-1), ascending for the forward operator and descending for the
 // adjoint and gradient operators, each step being dense update -> scatter -> gather in
 // that order (proj/tests/test_compiler.cpp:109-120).
+#include <cstdlib>
+
 #include "engine.hpp"
 #include "point_kernels.cuh"
 
@@ -496,18 +498,40 @@ void run_window(Plan& P, int op, long long t_from, long long t_to, bool with_poi
         require(P.n0 == P.N[0], SFB_ERR_CAPABILITY, "TTI windows run one whole domain");
         require(P.tti_chunk[0] > 0, SFB_ERR_PARAMETER, "call sfb_step_begin(SFB_OP_TTI_FORWARD) first");
     }
-    SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
-    for (long long i = 0; i < t_to - t_from; ++i) {
-        const long long t = ro.backward ? t_to - 1 - i : t_from + i;
-        if (tti) {   // the two launches of the rotated pair (engine_tti.cu)
-            tti_rot(P, t, SFB_PART_ALL);
-            tti_update(P, t, SFB_PART_ALL, with_points);
-            continue;
+    auto enqueue = [&] {
+        for (long long i = 0; i < t_to - t_from; ++i) {
+            const long long t = ro.backward ? t_to - 1 - i : t_from + i;
+            if (tti) {   // the two launches of the rotated pair (engine_tti.cu)
+                tti_rot(P, t, SFB_PART_ALL);
+                tti_update(P, t, SFB_PART_ALL, with_points);
+                continue;
+            }
+            step_compute(P, op, t, SFB_PART_ALL);
+            if (with_points) step_points(P, op, t, SFB_PART_ALL);
         }
-        step_compute(P, op, t, SFB_PART_ALL);
-        if (with_points) step_points(P, op, t, SFB_PART_ALL);
+    };
+    // SFB_GRAPH=1 (measurement aid): the window is captured into a CUDA graph and replayed as
+    // one graph launch.  The loop is device-bound (the host enqueues a step several times
+    // faster than the device runs it), so this is not the default: see DESIGN.md 3.2.
+    static const bool use_graph = std::getenv("SFB_GRAPH") != nullptr;
+    if (use_graph) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        SFB_CUDA(cudaStreamBeginCapture(P.s_main, cudaStreamCaptureModeThreadLocal));
+        enqueue();
+        SFB_CUDA(cudaStreamEndCapture(P.s_main, &graph));
+        SFB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+        SFB_CUDA(cudaGraphLaunch(exec, P.s_main));
+        SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+        SFB_CUDA(cudaStreamSynchronize(P.s_main));
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+    } else {
+        SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
+        enqueue();
+        SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
     }
-    SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
     SFB_CUDA(cudaStreamSynchronize(P.s_main));
     float ms = 0.f;
     SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
