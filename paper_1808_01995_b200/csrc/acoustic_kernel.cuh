@@ -587,7 +587,11 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
     using S = DualShape<K, TXV, TY, NS, SEP>;
     static_assert(!(ROTATE && SLIDE), "one queue scheme at a time");
     constexpr int KP = S::KP, SW = S::SW, STAGE = S::STAGE, Q = 2 * K + 1;
-    constexpr int QN = SLIDE ? Q + 1 : Q;
+#ifndef SFB_SLIDE_U
+#define SFB_SLIDE_U 2
+#endif
+    constexpr int SU = SFB_SLIDE_U;               // planes per slide of the window
+    constexpr int QN = SLIDE ? Q + SU - 1 : Q;
     constexpr int NARR = S::NARR, ABOX = S::ABOX, CPAD = S::CPAD, TX = S::TX;
     constexpr int NCW = S::NCONS / 32;
 
@@ -732,13 +736,19 @@ acoustic_step_dual_kernel(const __grid_constant__ StepMaps tm,
             rotate_run<Q, 0>(step, n, nplanes);
         }
     } else if constexpr (SLIDE) {
-        for (int n = 0; n < nplanes; n += 2) {
+        for (int n = 0; n < nplanes; n += SU) {
             iteration(std::integral_constant<int, 0>{}, n);
             if (n + 1 < nplanes) iteration(std::integral_constant<int, 1>{}, n + 1);
+            if constexpr (SU > 2) {
+                if (n + 2 < nplanes) iteration(std::integral_constant<int, 2>{}, n + 2);
+            }
+            if constexpr (SU > 3) {
+                if (n + 3 < nplanes) iteration(std::integral_constant<int, 3>{}, n + 3);
+            }
 #pragma unroll
             for (int j = 0; j < Q - 1; ++j)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) q[j][c] = q[j + 2][c];
+                for (int c = 0; c < 4; ++c) q[j][c] = q[j + SU][c];
         }
     } else {
         for (int n = 0; n < nplanes; ++n) iteration(std::integral_constant<int, 0>{}, n);
