@@ -408,7 +408,8 @@ def measure_op(wl, op, K, W, device, want_e2e=True):
         else:
             d2 = wk.residual_traces()
             p2.forward(wk.src, save_every=images_every)            # the history the sweep images against
-            call = lambda: p2.gradient(d2)[0]                      # noqa: E731
+            gbuf = np.zeros(wk.N)                                  # the caller owns the gradient array
+            call = lambda: p2.gradient(d2, out=gbuf)[0]            # noqa: E731
             h2d, d2h = n_rec * 8, int(pts * 8 / K)                 # grad (f64, padded grid) comes back once
         call()                                                     # warm-up: allocations, first touch
         t0 = time.perf_counter()

@@ -267,9 +267,13 @@ class Plan:
         self._chk(lib.sfb_adjoint(self.h, rec.ctypes.data, srca.ctypes.data, C.byref(rep)))
         return srca, rep
 
-    def gradient(self, resid):
+    def gradient(self, resid, out=None):
+        """out: optional f64 array of the padded grid shape to fill (the reference's callers own
+        the gradient Function, proj/include/sf/seismic_ops.hpp:49-58); allocated when omitted."""
         resid = np.ascontiguousarray(resid, dtype=np.float64)
-        grad = np.zeros(self.shape)
+        grad = np.zeros(self.shape) if out is None else out
+        if tuple(grad.shape) != tuple(self.shape) or grad.dtype != np.float64:
+            raise ValueError("out must be a float64 array of the padded grid shape")
         rep = Report()
         self._chk(lib.sfb_gradient(self.h, resid.ctypes.data, C.byref(_view(grad)), C.byref(rep)))
         return grad, rep

@@ -519,8 +519,8 @@ SFB_API int sfb_adjoint(sfb_plan* plan, const double* rec, double* srca, sfb_rep
         Plan& P = *plan;
         require(rec && srca, SFB_ERR_PARAMETER, "adjoint: null trace table");
         require(P.cloud[0].set && P.cloud[1].set, SFB_ERR_BINDING, "point clouds are not bound");
-        upload_traces(P, P.cloud[SFB_CLOUD_REC], rec);
-        run_op(P, SFB_OP_ADJOINT, 0, report, srca);
+        // the receiver table is fed to the device row by row while the sweep runs
+        run_op(P, SFB_OP_ADJOINT, 0, report, srca, rec);
     });
 }
 
@@ -533,11 +533,12 @@ SFB_API int sfb_gradient(sfb_plan* plan, const double* resid, const sfb_field_mv
         require(P.cloud[1].set, SFB_ERR_BINDING, "receiver cloud is not bound");
         require((P.history_valid && P.save_every > 0) || P.ckpt_valid, SFB_ERR_PARAMETER,
                 "gradient_operator: saved forward history required");
-        upload_traces(P, P.cloud[SFB_CLOUD_REC], resid);
-        if (P.ckpt_valid && !P.history_valid)
+        if (P.ckpt_valid && !P.history_valid) {
+            upload_traces(P, P.cloud[SFB_CLOUD_REC], resid);
             gradient_checkpointed(P, report);
-        else
-            run_op(P, SFB_OP_GRADIENT, P.save_every, report);
+        } else {
+            run_op(P, SFB_OP_GRADIENT, P.save_every, report, nullptr, resid);
+        }
         download_field(P, P.grad.as<float>(), grad);
     });
 }

@@ -69,8 +69,9 @@ void build_cloud(Plan& P, Cloud& c);
 constexpr size_t kStageBytes = 32u << 20;  // per half
 // sampled rows leave the device in chunks of about this size while the loop runs: small enough
 // that the copy and the host-side widening of a chunk hide behind the next steps and the tail
-// after the last step is short (a 592^3 step is 0.54 ms, a row of 512 x 512 traces 1 MB)
-constexpr size_t kRowChunkBytes = 4u << 20;
+// after the last step is short (a 592^3 step is 0.54 ms, a row of 512 x 512 traces 1 MB;
+// measured on configs[1] over 20 steps: 4 MB chunks leave 1.0 ms outside the loop, 1 MB 0.78)
+constexpr size_t kRowChunkBytes = 1u << 20;
 
 template <typename Fn>
 void parallel_chunks(long long n, Fn&& fn) {
@@ -130,7 +131,8 @@ void step_compute(Plan& P, int op, long long t, int part, const StepExtras* ex =
 void step_points(Plan& P, int op, long long t, int part, float* target_override = nullptr,
                  bool allow_gather = true, const StepExtras* ex = nullptr,
                  float* peer_lo = nullptr, float* peer_hi = nullptr);
-void finite_guard(Plan& P, const char* what);
+// only >= 0: scan that wavefield buffer alone (the level computed last)
+void finite_guard(Plan& P, const char* what, int only = -1);
 // Streams the sampled trace rows to the caller's f64 table while the time loop runs: every
 // `rows` completed rows are copied (fp32, copy stream, pinned half) and the previous chunk
 // is widened on host threads in the shadow of the GPU.
@@ -182,8 +184,64 @@ struct RowStreamer {
     }
 };
 
+// The mirror image for the injected cloud: a table of many traces (the receiver data of an
+// adjoint run or a gradient sweep) reaches the device chunk by chunk in sweep order, one chunk
+// ahead of the step that injects it (narrowed on the host, copy stream, pinned halves of its
+// own), instead of as a whole before the first step.
+struct RowFeeder {
+    Plan& P;
+    Cloud& c;
+    const double* host;
+    bool backward;
+    long long rows, next;      // rows per chunk; next row to send, in sweep order
+    int b = 0;
+    bool used[2] = {false, false};
 
-void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stream_out = nullptr);
+    RowFeeder(Plan& p, Cloud& cl, const double* h, bool back)
+        : P(p), c(cl), host(h), backward(back) {
+        rows = std::max<long long>(1, (long long)(kRowChunkBytes / 4) / std::max<long long>(c.np, 1));
+        next = backward ? P.desc.nt - 2 : 1;
+        P.stage_in.ensure(size_t(rows * c.np));
+    }
+    ~RowFeeder() {
+        if (more()) c.has_in = false;   // a run that failed half-way leaves a partial table
+    }
+    bool more() const { return backward ? next >= 1 : next <= P.desc.nt - 2; }
+    void send() {
+        long long lo, hi;
+        if (backward) {
+            hi = next;
+            lo = std::max<long long>(1, hi - rows + 1);
+            next = lo - 1;
+        } else {
+            lo = next;
+            hi = std::min<long long>(P.desc.nt - 2, lo + rows - 1);
+            next = hi + 1;
+        }
+        PinnedStage& st = P.stage_in;
+        if (used[b]) SFB_CUDA(cudaEventSynchronize(st.moved[b]));
+        narrow(host + lo * c.np, st.p[b], (hi - lo + 1) * c.np);
+        SFB_CUDA(cudaMemcpyAsync(c.tr_in.as<float>() + lo * c.np, st.p[b],
+                                 size_t((hi - lo + 1) * c.np) * 4, cudaMemcpyHostToDevice, st.copy));
+        SFB_CUDA(cudaEventRecord(st.moved[b], st.copy));
+        SFB_CUDA(cudaStreamWaitEvent(P.s_main, st.moved[b], 0));   // later launches see the rows
+        used[b] = true;
+        b ^= 1;
+    }
+    // the rows of step t, and the chunk after them, are on their way
+    void before_step(long long t) {
+        while (more() && (backward ? next >= t - rows : next <= t + rows)) send();
+    }
+    void finish() {
+        while (more()) send();
+        c.has_in = true;
+    }
+};
+
+// stream_out: the sampled table goes to this host table while the loop runs; stream_in: the
+// injected table comes from this host table while the loop runs (else it is resident already)
+void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stream_out = nullptr,
+            const double* stream_in = nullptr);
 void run_window(Plan& P, int op, long long t_from, long long t_to, bool with_points,
                 sfb_report* report);
 void forward_checkpointed(Plan& P, long long C, sfb_report* rep, double* stream_out);

@@ -323,10 +323,11 @@ void step_points(Plan& P, int op, long long t, int part, float* target_override,
     mark_stream(P, part);
 }
 
-void finite_guard(Plan& P, const char* what) {
+void finite_guard(Plan& P, const char* what, int only) {
     P.flag.alloc(sizeof(int), false);
     SFB_CUDA(cudaMemsetAsync(P.flag.p, 0, sizeof(int), P.s_main));
     for (int b = 0; b < 2; ++b) {
+        if (only >= 0 && b != only) continue;
         finite_check_kernel<<<P.sm_count * 8, 256, 0, P.s_main>>>(P.u[b].as<float>(), P.ucount,
                                                                  P.flag.as<int>());
         SFB_CUDA(cudaGetLastError());
@@ -337,8 +338,14 @@ void finite_guard(Plan& P, const char* what) {
     if (bad) throw Failure(SFB_ERR_STABILITY, std::string(what) + ": wavefield went non-finite");
 }
 
-void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stream_out) {
+void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stream_out,
+            const double* stream_in) {
     const OpRoles ro = roles(op);
+    std::unique_ptr<RowFeeder> feed;
+    if (stream_in) {
+        feed.reset(new RowFeeder(P, P.cloud[ro.inj], stream_in, ro.backward));
+        P.cloud[ro.inj].has_in = true;   // every row a step reads is sent before that step
+    }
     step_begin(P, op, save_every);
     const long long nt = P.desc.nt;
     std::unique_ptr<RowStreamer> rs;
@@ -346,13 +353,21 @@ void run_op(Plan& P, int op, long long save_every, sfb_report* rep, double* stre
     SFB_CUDA(cudaEventRecord(P.ev_t0, P.s_main));
     for (long long i = 0; i < nt - 2; ++i) {
         const long long t = ro.backward ? nt - 2 - i : 1 + i;
+        if (feed) feed->before_step(t);
         step_compute(P, op, t, SFB_PART_ALL);
         step_points(P, op, t, SFB_PART_ALL);
         if (rs) rs->row_done(t);
     }
     SFB_CUDA(cudaEventRecord(P.ev_t1, P.s_main));
+    if (feed) feed->finish();
     if (rs) rs->flush();   // the last rows travel while the NaN guard scans the fields
-    finite_guard(P, op == SFB_OP_FORWARD ? "forward" : (op == SFB_OP_ADJOINT ? "adjoint" : "gradient"));
+    // a non-finite value of one level stays in place in the next one (the update adds twice the
+    // centre value), so the level computed last holds every node that ever went bad
+    int newest = -1;
+    for (int b = 0; b < 2; ++b)
+        if (nt > 2 && P.live_level[b] == (ro.backward ? 0 : nt - 1)) newest = b;
+    finite_guard(P, op == SFB_OP_FORWARD ? "forward" : (op == SFB_OP_ADJOINT ? "adjoint" : "gradient"),
+                 newest);
     float ms = 0.f;
     SFB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
     if (op == SFB_OP_FORWARD && save_every > 0) P.history_valid = true;

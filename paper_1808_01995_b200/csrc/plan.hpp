@@ -175,6 +175,7 @@ struct Plan {
 
     Cloud cloud[2];
     PinnedStage stage;
+    PinnedStage stage_in;   // rows fed to the injected cloud while a run is under way
 
     // TTI operator state (builder-defined formulation, csrc/tti_kernels.cuh)
     bool tti_set = false;
