@@ -929,6 +929,19 @@ SFB_API int sfb_link_peers_ipc(sfb_plan* plan, const void* lo_blob, const void* 
         }
         P.push_count = P.done_count = P.g_count = 0;
         SFB_CUDA(cudaMemsetAsync(P.push_flag.p, 0, 256, P.s_main));
+        // the ordering of the ranks rests on stream waits on the NEIGHBOURS' counters: prove
+        // here, where the caller can still fall back to send/recv, that this driver accepts
+        // such a wait on peer-mapped memory (>= 0 holds at once, whatever the neighbour does)
+        static StreamValueFn wait_value = stream_value_fn("cuStreamWaitValue32");
+        for (int side = 0; side < 2; ++side) {
+            if (!P.ipc_flag[side]) continue;
+            const CUresult rc = wait_value(P.s_main, reinterpret_cast<CUdeviceptr>(P.ipc_flag[side]),
+                                           0u, CU_STREAM_WAIT_VALUE_GEQ);
+            if (rc != CUDA_SUCCESS)
+                throw Failure(SFB_ERR_CAPABILITY,
+                              "link_peers_ipc: stream wait on the neighbour's counter refused "
+                              "(code " + std::to_string(int(rc)) + ")");
+        }
         SFB_CUDA(cudaStreamSynchronize(P.s_main));
     });
 }
