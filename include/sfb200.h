@@ -289,7 +289,9 @@ SFB_API int sfb_copy_halo(sfb_plan* dst_plan, void* dst, const void* src, int64_
 /* ---- tile shape (the counterpart of the reference's loop-blocking autotune,
  * proj/include/sf/execute.hpp:56): threads along the contiguous axis (x4 nodes each),
  * tile rows, ring stages (0 = any; negative = the dual-stream kernel with that many
- * stages), output planes per block (0 = automatic).  Only compiled shapes are accepted. */
+ * stages; -(100 + s) its rotated-queue, -(200 + s) its 2 x 2 patch, -(300 + s) its
+ * sliding-window and -(400 + s) its tall variant with s stages), output planes per block
+ * (0 = automatic).  Only compiled shapes are accepted. */
 SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk);
 SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* stages, int* chunk,
                          int* separable_damping);

@@ -1142,10 +1142,11 @@ SFB_API int sfb_set_tile(sfb_plan* plan, int txv, int ty, int stages, int chunk)
     return guarded(plan, [&] {
         // stages < 0 selects the dual-stream kernel with |stages| stages; |stages| > 100 its
         // rotated-queue variant with |stages| - 100 stages; |stages| > 200 the 2 x 2 patch
-        // variant with |stages| - 200 stages; |stages| > 300 the sliding-window variant
+        // variant with |stages| - 200 stages; |stages| > 300 the sliding-window variant;
+        // |stages| > 400 the tall variant (two rows of four nodes per thread)
         const int a = stages < 0 ? -stages : stages;
         select_variant(*plan, txv, ty, a % 100,
-                       stages < 0 ? (a > 300 ? 4 : (a > 200 ? 3 : (a > 100 ? 2 : 1))) : 0);
+                       stages < 0 ? (a > 400 ? 5 : a > 300 ? 4 : (a > 200 ? 3 : (a > 100 ? 2 : 1))) : 0);
         if (chunk > 0) plan->chunk = std::min(chunk, plan->n0);
     });
 }
@@ -1155,7 +1156,8 @@ SFB_API int sfb_get_tile(sfb_plan* plan, int* txv, int* ty, int* nst, int* chunk
     if (txv) *txv = plan->variant->TXV;
     if (ty) *ty = plan->variant->TY;
     if (nst)
-        *nst = plan->variant->dual ? -(plan->variant->NST + (plan->variant->slide ? 300
+        *nst = plan->variant->dual ? -(plan->variant->NST + (plan->variant->tall ? 400
+                                                             : plan->variant->slide ? 300
                                                              : plan->variant->patch ? 200
                                                              : plan->variant->rotate ? 100 : 0))
                                    : plan->variant->NST;

@@ -74,7 +74,8 @@ void make_tensor_maps(Plan& P) {
 // ---- tile shape / chunk choice ----------------------------------------------------------
 
 // dual: -1 any, 0 ring kernel, 1 dual-stream, 2 dual-stream with the rotated (unrolled) queue,
-// 3 dual-stream with 2 x 2 patches per thread, 4 dual-stream with the sliding queue window
+// 3 dual-stream with 2 x 2 patches per thread, 4 dual-stream with the sliding queue window,
+// 5 tall (two rows of four nodes per thread)
 void select_variant(Plan& P, int txv, int ty, int nst, int dual) {
     const StepVariant* best = nullptr;
     for (const StepVariant& v : step_variant_registry()) {
@@ -88,7 +89,7 @@ void select_variant(Plan& P, int txv, int ty, int nst, int dual) {
             const bool want_dual = P.K >= 5;
             const bool want_slide = P.K >= 6;
             const int want_ty = P.K >= 7 ? 14 : 16;
-            if (v.dual != want_dual || v.rotate || v.patch || v.slide != want_slide || v.TXV != 16 ||
+            if (v.dual != want_dual || v.rotate || v.patch || v.tall || v.slide != want_slide || v.TXV != 16 ||
                 v.TY != want_ty)
                 continue;
             if (v.NST != (want_dual ? 4 : P.K + 3)) continue;

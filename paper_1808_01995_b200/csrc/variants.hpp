@@ -9,6 +9,7 @@
 
 #include "acoustic_kernel.cuh"
 #include "acoustic_patch_kernel.cuh"
+#include "acoustic_tall_kernel.cuh"
 #include "launch.hpp"
 
 namespace sfb {
@@ -20,6 +21,7 @@ struct StepVariant {
     bool rotate;          // dual-stream kernel unrolled by 2K+1 (queue rotation, no moves)
     bool patch = false;   // dual-stream kernel with 2 x 2 patches per thread (acoustic_patch_kernel.cuh)
     bool slide = false;   // dual-stream kernel with the sliding queue window (unrolled by two)
+    bool tall = false;    // dual-stream kernel with two rows of four nodes per thread (acoustic_tall_kernel.cuh)
     int tile_x, tile_y;   // output tile (d2, d1)
     int box_w, box_h;     // TMA box of u[t] (d2, d1)
     int halo_x;           // KP
@@ -35,9 +37,9 @@ struct StepVariant {
 std::vector<StepVariant>& step_variant_registry();
 
 // kernel family of a variant: 0 ring, 1 dual-stream, 2 dual-stream with rotated queue, 3 patch,
-// 4 dual-stream with the sliding queue window
+// 4 dual-stream with the sliding queue window, 5 tall (2 x 4 nodes per thread)
 inline int variant_kind(const StepVariant& v) {
-    return v.slide ? 4 : v.patch ? 3 : int(v.dual) + int(v.rotate);
+    return v.tall ? 5 : v.slide ? 4 : v.patch ? 3 : int(v.dual) + int(v.rotate);
 }
 
 template <int K, int TXV, int TY, int NST, bool SEP, bool PUSH = false>
@@ -143,6 +145,30 @@ void register_patch() {
     }
 }
 
+template <int K, int NS, bool SEP, int TYT, bool PUSH = false>
+cudaError_t launch_tall(const StepMaps& tm, const StepParams& p, dim3 grid, cudaStream_t st) {
+    using S = TallShape<K, NS, SEP, TYT>;
+    return launch_pdl(&acoustic_step_tall_kernel<K, NS, SEP, PUSH, TYT>, grid, S::NTHREADS, S::SMEM,
+                      st, tm, p);
+}
+
+template <int K, int NS, bool SEP, int TYT = 14>
+void register_tall() {
+    using S = TallShape<K, NS, SEP, TYT>;
+    if constexpr (S::SMEM <= 227 * 1024) {
+        StepVariant v;
+        v.K = K; v.TXV = 16; v.TY = 2 * TYT; v.NST = NS; v.sep = SEP; v.dual = true; v.rotate = false;
+        v.tall = true;
+        v.tile_x = S::TX; v.tile_y = 2 * TYT; v.box_w = S::SW; v.box_h = S::SH; v.halo_x = S::KP;
+        v.nthreads = S::NTHREADS; v.smem = S::SMEM;
+        v.func = reinterpret_cast<const void*>(&acoustic_step_tall_kernel<K, NS, SEP, false, TYT>);
+        v.launch = &launch_tall<K, NS, SEP, TYT>;
+        v.func_push = reinterpret_cast<const void*>(&acoustic_step_tall_kernel<K, NS, SEP, true, TYT>);
+        v.launch_push = &launch_tall<K, NS, SEP, TYT, true>;
+        step_variant_registry().push_back(v);
+    }
+}
+
 template <int K, int TXV, int TY, int NST>
 void register_pair() {
     register_step<K, TXV, TY, NST, false>();
@@ -188,6 +214,11 @@ void register_all_for_K() {
     if constexpr (K >= 6) {
         register_patch<K, 4, false, 2>();
         register_patch<K, 4, true, 2>();
+    }
+    // two rows of four nodes per thread: 15 LDS.128 per four nodes instead of 23 at order 16
+    if constexpr (K >= 7) {
+        register_tall<K, 4, false>();
+        register_tall<K, 4, true>();
     }
     if constexpr (K <= 4) {  // unrolling by 2K+1 overflows the instruction cache above
         register_rotated_pair<K, 16, 16, 3>();

@@ -181,8 +181,8 @@ def test_checkpointed_gradient_equals_full_history(nt, C):
 
 @pytest.mark.parametrize("order", [12, 14, 16])
 def test_patch_kernel_agrees_bitwise_with_the_dual_stream_kernel(order):
-    """acoustic_patch_kernel.cuh (2 x 2 nodes per thread, queue window slid by two planes)
-    keeps the arithmetic and its order per node: forward with snapshots, adjoint and the
+    """acoustic_patch_kernel.cuh (2 x 2 nodes per thread, queue window slid by two planes) and
+    acoustic_tall_kernel.cuh (2 x 4 nodes per thread) keep the arithmetic and its order per node: forward with snapshots, adjoint and the
     gradient with fused imaging equal the dual-stream kernel bit for bit, separable and dense
     damping, ragged extents, several d0 chunks."""
     from paper_1808_01995_b200 import capi
@@ -195,8 +195,10 @@ def test_patch_kernel_agrees_bitwise_with_the_dual_stream_kernel(order):
         plan.set_points(capi.CLOUD_REC, geom.rec_base, geom.rec_w)
         out = {}
         rows = 14 if order >= 14 else 16
-        for name, tile in (("dual", (16, rows, -4)), ("patch", (16, 14, -204)),
-                           ("slide", (16, rows, -304))):
+        tiles = [("dual", (16, rows, -4)), ("patch", (16, 14, -204)), ("slide", (16, rows, -304))]
+        if order >= 14:   # two rows of four nodes per thread (acoustic_tall_kernel.cuh)
+            tiles += [("tall", (16, 28, -404))]
+        for name, tile in tiles:
             for chunk in (0, 11):
                 plan.set_tile(*tile, chunk)
                 assert plan.get_tile()["stages"] == tile[2]

@@ -1,6 +1,6 @@
 """One tile shape of the acoustic step on an n^3 grid for an ncu capture:
     python tools/ncu_case.py <n> <order> <txv> <ty> <stages> [steps] [dense]
-(stages < 0: dual-stream, < -100 rotated, < -200 patch, < -300 sliding window).  A trailing
+(stages < 0: dual-stream, < -100 rotated, < -200 patch, < -300 sliding window, < -400 tall).  A trailing
 "grad" runs forward (every level saved) and then the gradient sweep: the update launches
 after the first `steps` are imaging launches.  Cheap random medium, no oracle."""
 import os, sys

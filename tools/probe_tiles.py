@@ -35,7 +35,10 @@ src = np.sin(np.arange(nt) * 0.1).reshape(nt, 1)
 plan.upload_traces(capi.CLOUD_SRC, src)
 print("points up", time.time() - t0, flush=True)
 K = order // 2
-tiles = [(16, 16, K + 3), (16, 16, K + 4), (32, 8, K + 3), (16, 32, K + 3), (32, 16, K + 3), (16, 16, -3), (16, 16, -4), (16, 14, -4), (32, 8, -3), (16, 16, -103), (16, 14, -204), (16, 14, -304), (16, 16, -304)]
+tiles = [(16, 16, K + 3), (16, 16, K + 4), (32, 8, K + 3), (16, 32, K + 3), (32, 16, K + 3), (16, 16, -3), (16, 16, -4), (16, 14, -4), (32, 8, -3), (16, 16, -103), (16, 14, -204), (16, 14, -304), (16, 16, -304), (16, 28, -404)]
+if len(sys.argv) > 5:   # only the listed stage codes
+    keep = {int(c) for c in sys.argv[5].split(',')}
+    tiles = [t for t in tiles if t[2] in keep]
 for tile in tiles:
     for chunk in (0,):
         try:
