@@ -711,6 +711,11 @@ class SlabJob:
         lo, hi = wl.bounds[rank]
         self.points_owned = float(hi - lo) * wl.N[1] * wl.N[2]
         self.halo = "none (one GPU)"
+        self.drv = None
+        # the caller owns the sampled table; written once here so that its pages exist, as
+        # those of a long-lived buffer do (np.zeros alone maps them lazily)
+        self.rec = np.empty((wl.nt, wl.rec_base.shape[0]))
+        self.rec.fill(0.0)
         ex = slabs.HaloExchanger(rank, world)
         if op == "tti":
             self.eng = slabs.TtiPlanEngine(plan, device)
@@ -720,7 +725,7 @@ class SlabJob:
                 if os.environ.get("SFB_HALO", "push") == "push":
                     try:
                         drv = slabs.TtiPeerPushDriver(plan, rank, world)
-                        self._loop = drv.run
+                        self._loop, self.drv = drv.run, drv
                         self.halo = ("fused peer push (CUDA IPC stores from both passes: g, then "
                                      "the new p and r)")
                     except RuntimeError as e:
@@ -734,11 +739,16 @@ class SlabJob:
                 if os.environ.get("SFB_HALO", "push") == "push":
                     try:
                         drv = slabs.PeerPushDriver(plan, self.oid, rank, world)
-                        self._loop = drv.run
+                        self._loop, self.drv = drv.run, drv
                         self.halo = "fused peer push (CUDA IPC stores from the boundary kernels)"
                     except RuntimeError as e:
                         if rank == 0:
                             log(f"[bench] {e}; falling back to NCCL send/recv")
+        if world == 1 and os.environ.get("SFB_HALO", "push") == "push":
+            # one slab = the whole domain: the same single-launch step and streamed tables
+            self.drv = (slabs.TtiPeerPushDriver(plan, rank, 1) if op == "tti"
+                        else slabs.PeerPushDriver(plan, self.oid, rank, 1))
+            self._loop = self.drv.run
         self.e0 = torch.cuda.Event(enable_timing=True)
         self.e1 = torch.cuda.Event(enable_timing=True)
 
@@ -777,6 +787,15 @@ class SlabJob:
         rec = self.plan.download_traces(self.capi.CLOUD_REC)
         self.rec = rec
         return float(rec.nbytes)
+
+    def run_e2e(self, a, b):
+        """the K steps with the sampled rows streaming into the host table while they run
+        (sfb_slab_run); the send/recv fallback steps from Python and downloads afterwards"""
+        if self.drv is None:
+            self.loop(a, b)
+            return self.download()
+        self.drv.run_tables(a, b, smp=self.rec)
+        return float((b - a) * self.rec.shape[1] * 8)
 
 
 def multi_gpu(args):

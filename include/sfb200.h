@@ -274,6 +274,21 @@ SFB_API int sfb_tti_step_update_fused(sfb_plan* plan, int64_t t);
 SFB_API int sfb_tti_step_update(sfb_plan* plan, int64_t t, int part);
 SFB_API int sfb_tti_halo_blocks(sfb_plan* plan, int which, int64_t t, void** send_lo,
                                 void** send_hi, void** recv_lo, void** recv_hi, int64_t* count);
+/* A range of steps [t_from, t_to) of ONE rank's slab in a single call, with the trace tables
+ * moving while the loop runs -- the slab counterpart of sfb_forward / sfb_adjoint /
+ * sfb_tti_forward for a plan that is linked through CUDA IPC (or not linked at all: one
+ * slab = the whole domain).  Per step: sfb_step_slab_fused + sfb_peer_wait_ipc (the TTI pair:
+ * the four calls above).  `smp` (may be NULL): host f64 table [nt][np] of the sampled cloud;
+ * its rows of the stepped range are filled as they are computed (fp32 over the bus, widened
+ * on host threads in the shadow of the loop).  `inj` (may be NULL): host f64 table [nt][np]
+ * of the injected cloud, fed to the device one chunk ahead of the step that needs it; NULL =
+ * the table uploaded with sfb_upload_traces.  Backward operators run t_to - 1 down to t_from.
+ * Bracket with sfb_step_begin (and a barrier between the ranks: nobody pushes into a field
+ * its owner is still zeroing) and sfb_step_end.  Plans linked in-process (sfb_link_peers)
+ * are stepped call by call instead: their ordering needs every plan to make each call
+ * before any plan makes the next. */
+SFB_API int sfb_slab_run(sfb_plan* plan, int op, int64_t t_from, int64_t t_to, const double* inj,
+                         double* smp);
 SFB_API int sfb_stream_sync(sfb_plan* plan);
 /* test aid: keeps the plan's main (0) or boundary (1) stream busy for `microseconds`
  * (<= 1 s) at the point of the call, to shake out ordering races between linked slabs */

@@ -46,7 +46,7 @@ SYMBOLS = [
     "sfb_set_model_tti", "sfb_set_points", "sfb_locate", "sfb_forward", "sfb_forward_checkpointed", "sfb_adjoint",
     "sfb_gradient", "sfb_tti_forward", "sfb_get_wavefield", "sfb_upload_traces",
     "sfb_download_traces", "sfb_run_resident", "sfb_run_steps", "sfb_time_stencil", "sfb_step_begin", "sfb_step_compute",
-    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_slab_fused", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_step_rot_fused", "sfb_tti_peer_wait_g", "sfb_tti_peer_wait_g_ipc", "sfb_tti_step_update_fused", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
+    "sfb_step_points", "sfb_step_slab_boundary", "sfb_step_slab_interior", "sfb_step_slab_fused", "sfb_step_end", "sfb_tti_step_rot", "sfb_tti_step_update", "sfb_tti_step_rot_fused", "sfb_tti_peer_wait_g", "sfb_tti_peer_wait_g_ipc", "sfb_tti_step_update_fused", "sfb_slab_run", "sfb_tti_halo_blocks", "sfb_link_peers", "sfb_peer_wait", "sfb_peer_export", "sfb_link_peers_ipc", "sfb_peer_wait_ipc", "sfb_put_history", "sfb_get_gradient", "sfb_halo_blocks", "sfb_stream_sync", "sfb_streams",
     "sfb_set_streams", "sfb_copy_halo", "sfb_set_tile", "sfb_get_tile",
     "sfb_set_dense_damping", "sfb_launch_count", "sfb_autotune", "sfb_debug_stall",
 ]
@@ -85,6 +85,7 @@ lib.sfb_tti_step_update.argtypes = [C.c_void_p, C.c_int64, C.c_int]
 lib.sfb_tti_halo_blocks.argtypes = lib.sfb_halo_blocks.argtypes
 lib.sfb_tti_step_rot_fused.argtypes = [C.c_void_p, C.c_int64]
 lib.sfb_tti_step_update_fused.argtypes = [C.c_void_p, C.c_int64]
+lib.sfb_slab_run.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
 lib.sfb_tti_peer_wait_g.argtypes = [C.c_void_p, C.c_void_p]
 lib.sfb_tti_peer_wait_g_ipc.argtypes = [C.c_void_p]
 lib.sfb_link_peers.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -367,6 +368,24 @@ class Plan:
 
     def tti_step_update_fused(self, t):
         self._chk(lib.sfb_tti_step_update_fused(self.h, t))
+
+    def slab_run(self, op, t_from, t_to, inj=None, smp=None):
+        """Steps [t_from, t_to) of this rank's slab in one call (sfb_slab_run); `smp`: f64
+        [nt][np] table of the sampled cloud filled while the loop runs, `inj`: f64 [nt][np]
+        table of the injected cloud fed while the loop runs (None: the uploaded one)."""
+        def table(a, cloud_np):
+            if a is None:
+                return None
+            if a.dtype != np.float64 or not a.flags.c_contiguous or a.shape[0] != self.nt \
+                    or a.size != self.nt * cloud_np:
+                raise ValueError("trace tables are C-contiguous float64 [nt][np] arrays")
+            return a.ctypes.data
+        backward = op in (OP_ADJOINT, OP_GRADIENT)
+        c_inj = CLOUD_REC if backward else CLOUD_SRC
+        c_smp = CLOUD_SRC if backward else CLOUD_REC
+        self._chk(lib.sfb_slab_run(self.h, op, t_from, t_to, table(inj, self.np[c_inj]),
+                                   table(smp, self.np[c_smp])))
+        return smp
 
     def tti_peer_wait_g(self, neighbour):
         self._chk(lib.sfb_tti_peer_wait_g(self.h, neighbour.h))

@@ -1040,6 +1040,51 @@ SFB_API int sfb_halo_blocks(sfb_plan* plan, int op, int64_t t, void** send_lo, v
     });
 }
 
+namespace {
+// a C-ABI call made from inside another one: its failure becomes this call's failure
+void chain(sfb_plan* plan, int rc) {
+    if (rc != SFB_OK) throw Failure(rc, plan->err);
+}
+}  // namespace
+
+SFB_API int sfb_slab_run(sfb_plan* plan, int op, int64_t t_from, int64_t t_to, const double* inj,
+                         double* smp) {
+    if (!plan) return SFB_ERR_PARAMETER;
+    return guarded(plan, [&] {
+        Plan& P = *plan;
+        const OpRoles ro = roles(op);
+        require(t_from >= 1 && t_from <= t_to && t_to <= P.desc.nt - 1, SFB_ERR_PARAMETER,
+                "slab_run: steps must lie in [1, nt - 1)");
+        const bool linked = P.peer_lo[0] || P.peer_hi[0];
+        require(!linked || P.ipc_flag[0] || P.ipc_flag[1], SFB_ERR_CAPABILITY,
+                "slab_run: plans linked in-process are stepped call by call "
+                "(sfb_step_slab_fused + sfb_peer_wait)");
+        const bool tti = op == SFB_OP_TTI_FORWARD;
+        std::unique_ptr<RowStreamer> rs;
+        if (smp && ro.smp >= 0) rs.reset(new RowStreamer(P, P.cloud[ro.smp], smp));
+        std::unique_ptr<RowFeeder> feed;
+        if (inj) {
+            feed.reset(new RowFeeder(P, P.cloud[ro.inj], inj, ro.backward, t_from, t_to - 1));
+            P.cloud[ro.inj].has_in = true;
+        }
+        for (int64_t i = 0; i < t_to - t_from; ++i) {
+            const int64_t t = ro.backward ? t_to - 1 - i : t_from + i;
+            if (feed) feed->before_step(t);
+            if (tti) {
+                chain(plan, sfb_tti_step_rot_fused(plan, t));
+                chain(plan, sfb_tti_peer_wait_g_ipc(plan));
+                chain(plan, sfb_tti_step_update_fused(plan, t));
+            } else {
+                chain(plan, sfb_step_slab_fused(plan, op, t));
+            }
+            chain(plan, sfb_peer_wait_ipc(plan));
+            if (rs) rs->row_done(t);
+        }
+        if (feed) feed->finish();
+        if (rs) rs->finish();
+    });
+}
+
 SFB_API int sfb_debug_stall(sfb_plan* plan, int boundary_stream, int64_t microseconds) {
     if (!plan || microseconds < 0 || microseconds > 1000000) return SFB_ERR_PARAMETER;
     return guarded(plan, [&] {

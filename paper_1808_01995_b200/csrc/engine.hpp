@@ -194,28 +194,31 @@ struct RowFeeder {
     const double* host;
     bool backward;
     long long rows, next;      // rows per chunk; next row to send, in sweep order
+    long long first, last;     // rows the run reads: [first, last] (default: 1 .. nt - 2)
     int b = 0;
     bool used[2] = {false, false};
 
-    RowFeeder(Plan& p, Cloud& cl, const double* h, bool back)
-        : P(p), c(cl), host(h), backward(back) {
+    RowFeeder(Plan& p, Cloud& cl, const double* h, bool back, long long row_first = 1,
+              long long row_last = -1)
+        : P(p), c(cl), host(h), backward(back), first(row_first),
+          last(row_last < 0 ? p.desc.nt - 2 : row_last) {
         rows = std::max<long long>(1, (long long)(kRowChunkBytes / 4) / std::max<long long>(c.np, 1));
-        next = backward ? P.desc.nt - 2 : 1;
+        next = backward ? last : first;
         P.stage_in.ensure(size_t(rows * c.np));
     }
     ~RowFeeder() {
         if (more()) c.has_in = false;   // a run that failed half-way leaves a partial table
     }
-    bool more() const { return backward ? next >= 1 : next <= P.desc.nt - 2; }
+    bool more() const { return backward ? next >= first : next <= last; }
     void send() {
         long long lo, hi;
         if (backward) {
             hi = next;
-            lo = std::max<long long>(1, hi - rows + 1);
+            lo = std::max<long long>(first, hi - rows + 1);
             next = lo - 1;
         } else {
             lo = next;
-            hi = std::min<long long>(P.desc.nt - 2, lo + rows - 1);
+            hi = std::min<long long>(last, lo + rows - 1);
             next = hi + 1;
         }
         PinnedStage& st = P.stage_in;

@@ -632,3 +632,40 @@ def test_fed_and_resident_trace_tables_agree():
     assert np.abs(grad_fed).max() > 0
     assert np.array_equal(grad_fed, grad_res)
     plan.close()
+
+
+def test_slab_run_of_a_single_slab_equals_the_whole_domain_calls():
+    """sfb_slab_run on an unlinked plan (one slab = the whole domain): forward with the
+    sampled rows streamed out and the adjoint with the receiver table fed in reproduce
+    sfb_forward / sfb_adjoint bit for bit; a partial range leaves the other rows alone."""
+    from paper_1808_01995_b200 import capi
+    rng = np.random.default_rng(11)
+    shape, order, nsteps = [40, 36, 30], 8, 37
+    L = [(s - 1) * 10.0 for s in shape]
+    rec_xyz = rng.uniform(0.0, 1.0, size=(30000, 3)) * np.asarray(L)
+    model, geom = make_problem(shape, 10.0, 6, order, nsteps, rec=rec_xyz)
+    plan = make_plan(model, geom, order)
+    rec1, _ = plan.forward(geom.src)
+    u1 = plan.wavefield(geom.nt - 1)
+    data = rng.standard_normal((geom.nt, rec_xyz.shape[0]))
+    data[[0, geom.nt - 1]] = 0.0
+    srca1, _ = plan.adjoint(data)
+    # forward, in two ranges
+    plan.upload_traces(capi.CLOUD_SRC, geom.src)
+    table = np.full((geom.nt, geom.n_rec), np.nan)
+    plan.step_begin(capi.OP_FORWARD)
+    plan.slab_run(capi.OP_FORWARD, 1, 15, smp=table)
+    assert np.array_equal(table[1:15], rec1[1:15]) and np.isnan(table[15:geom.nt - 1]).all()
+    plan.slab_run(capi.OP_FORWARD, 15, geom.nt - 1, smp=table)
+    plan.step_end(capi.OP_FORWARD)
+    assert np.array_equal(table, rec1)
+    assert np.array_equal(plan.wavefield(geom.nt - 1), u1)
+    # adjoint, the receiver table fed while the sweep runs
+    out = np.full((geom.nt, 1), np.nan)
+    plan.step_begin(capi.OP_ADJOINT)
+    plan.slab_run(capi.OP_ADJOINT, 1, geom.nt - 1, inj=data, smp=out)
+    plan.step_end(capi.OP_ADJOINT)
+    assert np.abs(srca1).max() > 0 and np.array_equal(out, srca1)
+    with pytest.raises(capi.SfbError):
+        plan.slab_run(capi.OP_FORWARD, 0, 5)
+    plan.close()

@@ -15,7 +15,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
 SHAPE, ORDER, NSTEPS = [44, 30, 34], 8, 40
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, streamed=False):
     import torch
     import torch.distributed as dist
     from paper_1808_01995_b200 import capi, slabs
@@ -29,9 +29,16 @@ def _worker(rank, world, port, out):
     drv = slabs.PeerPushDriver(plan, capi.OP_FORWARD, rank, world)
     plan.step_begin(capi.OP_FORWARD)
     dist.barrier()   # nobody pushes into a neighbour that is still zeroing its fields
-    drv.run(1, geom.nt - 1)
-    plan.step_end(capi.OP_FORWARD)
-    rec = torch.from_numpy(plan.download_traces(capi.CLOUD_REC))
+    if streamed:   # the loop inside the library, sampled rows streaming into the host table
+        table = np.full((geom.nt, geom.n_rec), np.nan)
+        drv.run_tables(1, geom.nt - 1, smp=table)
+        plan.step_end(capi.OP_FORWARD)
+        assert np.array_equal(table, plan.download_traces(capi.CLOUD_REC))
+        rec = torch.from_numpy(table)
+    else:
+        drv.run(1, geom.nt - 1)
+        plan.step_end(capi.OP_FORWARD)
+        rec = torch.from_numpy(plan.download_traces(capi.CLOUD_REC))
     u = np.zeros(model.N)
     plan.wavefield(geom.nt - 1, out=u)
     u = torch.from_numpy(u)
@@ -51,7 +58,7 @@ def _tti_inputs():
     return model, geom, tti_fields(model.N, seed=3)
 
 
-def _tti_worker(rank, world, port, out):
+def _tti_worker(rank, world, port, out, streamed=False):
     import torch
     import torch.distributed as dist
     from paper_1808_01995_b200 import capi, slabs
@@ -67,9 +74,15 @@ def _tti_worker(rank, world, port, out):
     plan.step_begin(capi.OP_TTI_FORWARD)
     plan.sync()
     dist.barrier()
-    drv.run(1, geom.nt - 1)
-    plan.step_end(capi.OP_TTI_FORWARD)
-    rec = torch.from_numpy(plan.download_traces(capi.CLOUD_REC))
+    if streamed:
+        table = np.full((geom.nt, geom.n_rec), np.nan)
+        drv.run_tables(1, geom.nt - 1, smp=table)
+        plan.step_end(capi.OP_TTI_FORWARD)
+        rec = torch.from_numpy(table)
+    else:
+        drv.run(1, geom.nt - 1)
+        plan.step_end(capi.OP_TTI_FORWARD)
+        rec = torch.from_numpy(plan.download_traces(capi.CLOUD_REC))
     p, r = np.zeros(model.N), np.zeros(model.N)
     plan.wavefield(geom.nt - 1, out=p, field=0)
     plan.wavefield(geom.nt - 1, out=r, field=1)
@@ -91,8 +104,8 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_push_between_processes_matches_single_domain(tmp_path, world):
+@pytest.mark.parametrize("world,streamed", [(2, False), (3, False), (3, True)])
+def test_peer_push_between_processes_matches_single_domain(tmp_path, world, streamed):
     import torch.multiprocessing as mp
     model, geom = make_problem(SHAPE, 10.0, 8, ORDER, NSTEPS)
     plan = make_plan(model, geom, ORDER)
@@ -100,14 +113,14 @@ def test_peer_push_between_processes_matches_single_domain(tmp_path, world):
     u1 = plan.wavefield(geom.nt - 1)
     plan.close()
     out = str(tmp_path / "ipc")
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, streamed), nprocs=world, join=True)
     assert np.abs(rec1).max() > 0
     assert np.array_equal(np.load(out + "_rec.npy"), rec1)
     assert np.array_equal(np.load(out + "_u.npy"), u1)
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_tti_peer_push_between_processes_matches_single_domain(tmp_path, world):
+@pytest.mark.parametrize("world,streamed", [(2, False), (3, False), (2, True)])
+def test_tti_peer_push_between_processes_matches_single_domain(tmp_path, world, streamed):
     import torch.multiprocessing as mp
     model, geom, fields = _tti_inputs()
     plan = make_plan(model, geom, 8)
@@ -117,7 +130,7 @@ def test_tti_peer_push_between_processes_matches_single_domain(tmp_path, world):
     r1 = plan.wavefield(geom.nt - 1, field=1)
     plan.close()
     out = str(tmp_path / "ipc_tti")
-    mp.spawn(_tti_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_tti_worker, args=(world, _free_port(), out, streamed), nprocs=world, join=True)
     assert np.abs(rec1).max() > 0
     assert np.array_equal(np.load(out + "_rec.npy"), rec1)
     assert np.array_equal(np.load(out + "_p.npy"), p1) and np.array_equal(np.load(out + "_r.npy"), r1)
