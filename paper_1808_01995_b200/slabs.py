@@ -271,16 +271,18 @@ class PeerPushDriver:
     def run(self, t_from: int, t_to: int, backward=False):
         """One update launch + one point launch per step (sfb_step_slab_fused: the first d0
         chunk sweeps up, the last one down, so both boundary plane groups are computed and
-        pushed first); SFB_SLAB_PROTOCOL=split runs the boundary / interior half-steps on two
-        streams instead (the protocol the NCCL fallback uses)."""
+        pushed first), the whole range in one library call (sfb_slab_run);
+        SFB_SLAB_PROTOCOL=split runs the boundary / interior half-steps on two streams instead
+        (the protocol the NCCL fallback uses), call by call."""
+        from . import capi
+        assert backward == (self.op in (capi.OP_ADJOINT, capi.OP_GRADIENT))
+        if os.environ.get("SFB_SLAB_PROTOCOL", "fused") != "split":
+            self.plan.slab_run(self.op, t_from, t_to)   # the loop inside the library
+            return
         steps = range(t_to - 1, t_from - 1, -1) if backward else range(t_from, t_to)
-        split = os.environ.get("SFB_SLAB_PROTOCOL", "fused") == "split"
         for t in steps:
-            if split:
-                self.plan.step_slab_boundary(self.op, t)
-                self.plan.step_slab_interior(self.op, t)
-            else:
-                self.plan.step_slab_fused(self.op, t)
+            self.plan.step_slab_boundary(self.op, t)
+            self.plan.step_slab_interior(self.op, t)
             self.plan.peer_wait_ipc()
 
 
@@ -302,7 +304,10 @@ class TtiPeerPushDriver(PeerPushDriver):
 
     def run(self, t_from: int, t_to: int, backward=False):
         assert not backward, "the TTI operator is forward-only"
-        for t in range(t_from, t_to):
+        if os.environ.get("SFB_SLAB_PROTOCOL", "fused") != "percall":
+            self.plan.slab_run(self.op, t_from, t_to)
+            return
+        for t in range(t_from, t_to):   # the same four calls per step, made from here
             self.plan.tti_step_rot_fused(t)
             self.plan.tti_peer_wait_g_ipc()
             self.plan.tti_step_update_fused(t)
