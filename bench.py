@@ -19,8 +19,10 @@ configuration the metric is quoted on):
   5  large-domain acoustic forward, order 16, 8 off-node sources, 1024 x 1024 receivers; weak
      scaling (default): 1024 x 1024 x (128 N) physical nodes, slab axis first
 At N > 1 the grid is cut into N slabs along the slowest axis; ghost planes are pushed into the
-neighbours' memory by the boundary kernels (CUDA IPC) with NCCL send/recv as the fallback
-(SFB_HALO=nccl forces it); the TTI pair exchanges over NCCL.
+neighbours' memory by the update kernels (CUDA IPC) with NCCL send/recv as the fallback
+(SFB_HALO=nccl forces it).  Every operator runs there: --op adjoint on config 2, --config 3
+(the gradient sweep against a history that a forward slab run of the same plans saved),
+--config 4 (the TTI pair pushes g, then the new p and r).
 
 One JSON line on stdout (rank 0).  `value`: device-timed (CUDA events on the plan's stream,
 max over ranks), inputs resident in HBM.  `e2e`: the same metric through the C-ABI with HOST
@@ -701,62 +703,88 @@ def single_gpu(args):
 # ---- our arm, N GPUs ----------------------------------------------------------------------
 
 class SlabJob:
-    """bench_core job over one capi.Plan on one GPU."""
+    """bench_core job over one capi.Plan on one GPU: forward (acoustic, TTI), adjoint, or the
+    gradient sweep against a history that a forward slab run of the same plans saved."""
 
-    def __init__(self, wl, plan, op, device, rank, world):
+    def __init__(self, wl, plan, op, device, rank, world, comm, resid=None, images_every=4):
         import torch
         from paper_1808_01995_b200 import capi, slabs
         self.torch, self.capi, self.wl, self.plan, self.op = torch, capi, wl, plan, op
         self.oid = op_ids(op)
+        self.backward = op in ("adjoint", "gradient")
         lo, hi = wl.bounds[rank]
         self.points_owned = float(hi - lo) * wl.N[1] * wl.N[2]
         self.halo = "none (one GPU)"
         self.drv = None
-        # the caller owns the sampled table; written once here so that its pages exist, as
-        # those of a long-lived buffer do (np.zeros alone maps them lazily)
-        self.rec = np.empty((wl.nt, wl.rec_base.shape[0]))
-        self.rec.fill(0.0)
+        # injected table (caller input) and sampled table (caller-owned output; written once
+        # here so that its pages exist, as those of a long-lived buffer do)
+        self.inj = resid if self.backward else wl.src
+        self.c_inj = capi.CLOUD_REC if self.backward else capi.CLOUD_SRC
+        self.c_smp = capi.CLOUD_SRC if self.backward else capi.CLOUD_REC
+        self.rec = None
+        if op != "gradient":
+            n_smp = wl.src_base.shape[0] if self.backward else wl.rec_base.shape[0]
+            self.rec = np.empty((wl.nt, n_smp))
+            self.rec.fill(0.0)
+        self.grad = None
         ex = slabs.HaloExchanger(rank, world)
+        push = os.environ.get("SFB_HALO", "push") == "push"
         if op == "tti":
             self.eng = slabs.TtiPlanEngine(plan, device)
             self._loop = lambda a, b: slabs.tti_step_loop(self.eng, ex, a, b)     # noqa: E731
-            if world > 1:
-                self.halo = "nccl send/recv (two exchanges per step: g, then p and r)"
-                if os.environ.get("SFB_HALO", "push") == "push":
-                    try:
-                        drv = slabs.TtiPeerPushDriver(plan, rank, world)
-                        self._loop, self.drv = drv.run, drv
-                        self.halo = ("fused peer push (CUDA IPC stores from both passes: g, then "
-                                     "the new p and r)")
-                    except RuntimeError as e:
-                        if rank == 0:
-                            log(f"[bench] {e}; falling back to NCCL send/recv")
+            make = lambda w: slabs.TtiPeerPushDriver(plan, rank, w)               # noqa: E731
+            names = ("nccl send/recv (two exchanges per step: g, then p and r)",
+                     "fused peer push (CUDA IPC stores from both passes: g, then the new p and r)")
         else:
             self.eng = slabs.PlanEngine(plan, self.oid, device)
-            self._loop = lambda a, b: slabs.step_loop(self.eng, ex, a, b)         # noqa: E731
-            if world > 1:
-                self.halo = "nccl send/recv"
-                if os.environ.get("SFB_HALO", "push") == "push":
-                    try:
-                        drv = slabs.PeerPushDriver(plan, self.oid, rank, world)
-                        self._loop, self.drv = drv.run, drv
-                        self.halo = "fused peer push (CUDA IPC stores from the boundary kernels)"
-                    except RuntimeError as e:
-                        if rank == 0:
-                            log(f"[bench] {e}; falling back to NCCL send/recv")
-        if world == 1 and os.environ.get("SFB_HALO", "push") == "push":
-            # one slab = the whole domain: the same single-launch step and streamed tables
-            self.drv = (slabs.TtiPeerPushDriver(plan, rank, 1) if op == "tti"
-                        else slabs.PeerPushDriver(plan, self.oid, rank, 1))
-            self._loop = self.drv.run
+            self._loop = lambda a, b: slabs.step_loop(self.eng, ex, a, b,         # noqa: E731
+                                                      backward=self.backward)
+            make = lambda w: slabs.PeerPushDriver(plan, self.oid, rank, w)        # noqa: E731
+            names = ("nccl send/recv", "fused peer push (CUDA IPC stores from the boundary kernels)")
+        if world > 1:
+            self.halo = names[0]
+        if push:   # world 1: one slab = the whole domain, same single-launch step and tables
+            try:
+                self.drv = make(world)
+                self._loop = lambda a, b: self.drv.run(a, b, backward=self.backward)   # noqa: E731
+                if world > 1:
+                    self.halo = names[1]
+            except RuntimeError as e:
+                if rank == 0:
+                    log(f"[bench] {e}; falling back to NCCL send/recv")
+        if op == "gradient":
+            # the history the sweep images against: a forward slab run of the same plans that
+            # keeps every images_every-th level in HBM (configs[2])
+            F = capi.OP_FORWARD
+            plan.upload_traces(capi.CLOUD_SRC, wl.src)
+            plan.step_begin(F, images_every)
+            self.sync()
+            comm.barrier()
+            if self.drv is not None:
+                self.drv.op = F
+                self.drv.run(1, wl.nt - 1)
+                self.drv.op = self.oid
+            else:
+                fwd = slabs.PlanEngine(plan, F, device)
+                slabs.step_loop(fwd, ex, 1, wl.nt - 1)
+                self.eng = slabs.PlanEngine(plan, self.oid, device)   # streams of the sweep
+            plan.step_end(F)
+            self.sync()
+            comm.barrier()
+            self.grad = np.empty(wl.N)
+            self.grad.fill(0.0)
         self.e0 = torch.cuda.Event(enable_timing=True)
         self.e1 = torch.cuda.Event(enable_timing=True)
+
+    def steps(self, a, b):
+        """bench_core counts steps upwards from 1; a backward sweep starts at the top level"""
+        return (self.wl.nt - b, self.wl.nt - a) if self.backward else (a, b)
 
     def begin(self):
         self.plan.step_begin(self.oid)
 
     def loop(self, a, b):
-        self._loop(a, b)
+        self._loop(*self.steps(a, b))
 
     def sync(self):
         self.torch.cuda.synchronize()
@@ -780,22 +808,37 @@ class SlabJob:
         return self.plan.launch_count()
 
     def upload(self):
-        self.plan.upload_traces(self.capi.CLOUD_SRC, self.wl.src)
-        return float(self.wl.src.nbytes)
+        if self.drv is not None and self.backward:
+            return 0.0      # the receiver table is fed while the sweep runs (run_e2e counts it)
+        self.plan.upload_traces(self.c_inj, self.inj)
+        return float(self.inj.nbytes)
 
     def download(self):
-        rec = self.plan.download_traces(self.capi.CLOUD_REC)
-        self.rec = rec
-        return float(rec.nbytes)
+        if self.op == "gradient":
+            import ctypes as C
+            self.plan._chk(self.capi.lib.sfb_get_gradient(self.plan.h, C.byref(self.capi._view(self.grad))))
+            return self.points_owned * 8.0
+        self.rec = self.plan.download_traces(self.c_smp)
+        return float(self.rec.nbytes)
 
     def run_e2e(self, a, b):
-        """the K steps with the sampled rows streaming into the host table while they run
-        (sfb_slab_run); the send/recv fallback steps from Python and downloads afterwards"""
+        """the K steps with the trace tables moving while they run (sfb_slab_run): sampled
+        rows into the host table, the receiver table of a backward sweep to the device; the
+        send/recv fallback steps from Python and moves the tables before / afterwards"""
         if self.drv is None:
             self.loop(a, b)
             return self.download()
-        self.drv.run_tables(a, b, smp=self.rec)
-        return float((b - a) * self.rec.shape[1] * 8)
+        lo, hi = self.steps(a, b)
+        self.drv.run_tables(lo, hi, inj=self.inj if self.backward else None, smp=self.rec)
+        moved = float((b - a) * self.rec.shape[1] * 8) if self.rec is not None else 0.0
+        if self.backward:
+            self.fed = float((b - a) * self.inj.shape[1] * 8)
+        if self.op == "gradient":
+            moved += self.download()
+        return moved
+
+    def result(self):
+        return self.grad if self.op == "gradient" else self.rec
 
 
 def multi_gpu(args):
@@ -831,14 +874,19 @@ def multi_gpu(args):
     plan = wl.make_plan(local)
     tile = plan.autotune() if op != "tti" else {}
     sep = bool(plan.get_tile()["sep"])
-    plan.upload_traces(capi.CLOUD_SRC, wl.src)
-    job = SlabJob(wl, plan, op, local, rank, world)
     comm = slabs.Comm(rank, world, torch.device(f"cuda:{local}") if backend == "nccl" else None)
+    resid = None
+    if op in ("adjoint", "gradient"):
+        resid = wl.residual_traces()           # of the rank's own receivers
+        plan.upload_traces(capi.CLOUD_REC, resid)
+    else:
+        plan.upload_traces(capi.CLOUD_SRC, wl.src)
+    job = SlabJob(wl, plan, op, local, rank, world, comm, resid)
     with ClockSampler(local) as clk:
         meas = slabs.bench_core(comm, job, K, W)
     clocks = clk.summary()
     plan.step_end(op_ids(op))
-    assert np.isfinite(job.rec).all()
+    assert np.isfinite(job.result()).all()
     log(f"[bench] rank {rank}: {meas['per_rank_ms_per_step'][rank]:.4f} ms/step on its slab "
         f"{wl.bounds[rank]}, halo: {job.halo}")
     halo_bytes = int(plan.halo_blocks(capi.OP_FORWARD, 1)["count"] * 4) * (4 if op == "tti" else 1)
@@ -853,7 +901,7 @@ def multi_gpu(args):
         line = slabs.scaling_line(
             meas, metric=METRIC[op], world=world, K=K, W=W, scaling=args.scaling,
             config=workload_config(config, op, world, args.scaling, {"tile": tile or None}),
-            bytes_per_point=actual_bytes(op, sep), contract_bytes=CONTRACT_BYTES[op], peak=peak,
+            bytes_per_point=actual_bytes(op, sep, 4), contract_bytes=CONTRACT_BYTES[op], peak=peak,
             peak_kind=kind, halo=job.halo, halo_bytes=halo_bytes,
             extra={"cpu_baseline": cpu, "clocks": clocks})
         print(json.dumps(line), flush=True)
@@ -870,9 +918,6 @@ def ours(args):
     if not torch.cuda.is_available() or capi.device_count() < 1:
         raise SystemExit("bench.py needs a CUDA device: there is no CPU fallback")
     if world > 1 or os.environ.get("SFB_BENCH_FORCE_DIST"):
-        if args.op in ("adjoint", "gradient"):
-            raise SystemExit("N > 1 runs time the forward operators (acoustic, TTI); the backward sweeps "
-                             "decompose the same way (tests/test_gpu_acoustic.py) but have no bench loop")
         return multi_gpu(args)
     return single_gpu(args)
 

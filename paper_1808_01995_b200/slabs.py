@@ -384,6 +384,7 @@ def bench_core(comm: Comm, job, K: int, W: int):
         comm.barrier()   # as above: no push may land in a field its owner is still zeroing
         if hasattr(job, "run_e2e"):     # loop and table traffic in one library call per rank
             d2h = job.run_e2e(1, 1 + K)
+            h2d += getattr(job, "fed", 0.0)   # injected rows fed while the loop ran
         else:
             job.loop(1, 1 + K)
             d2h = job.download()
