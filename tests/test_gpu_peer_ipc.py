@@ -52,6 +52,47 @@ def _worker(rank, world, port, out, streamed=False):
     dist.destroy_process_group()
 
 
+def _adjoint_data(geom):
+    rng = np.random.default_rng(21)
+    data = rng.standard_normal((geom.nt, geom.n_rec)) * np.hanning(geom.nt)[:, None]
+    data[[0, geom.nt - 1]] = 0.0
+    return data
+
+
+def _adjoint_worker(rank, world, port, out):
+    """the backward sweep of each rank as one sfb_slab_run: receiver table fed while it runs,
+    source-side trace streamed out"""
+    import torch
+    import torch.distributed as dist
+    from paper_1808_01995_b200 import capi, slabs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    model, geom = make_problem(SHAPE, 10.0, 8, ORDER, NSTEPS)
+    data = _adjoint_data(geom)
+    bounds = slabs.split_slabs(model.N[0], world, ORDER // 2)
+    plan = make_plan(model, geom, ORDER, slab=bounds[rank])
+    drv = slabs.PeerPushDriver(plan, capi.OP_ADJOINT, rank, world)
+    plan.step_begin(capi.OP_ADJOINT)
+    plan.sync()
+    dist.barrier()
+    table = np.full((geom.nt, geom.n_src), np.nan)
+    drv.run_tables(1, geom.nt - 1, inj=data, smp=table)
+    plan.step_end(capi.OP_ADJOINT)
+    srca = torch.from_numpy(table)
+    v = np.zeros(model.N)
+    plan.wavefield(0, out=v)
+    v = torch.from_numpy(v)
+    dist.all_reduce(srca)
+    dist.all_reduce(v)
+    dist.barrier()
+    if rank == 0:
+        np.save(out + "_srca.npy", srca.numpy())
+        np.save(out + "_v.npy", v.numpy())
+    plan.close()
+    dist.destroy_process_group()
+
+
 def _tti_inputs():
     from tests.test_gpu_tti import tti_fields, tti_problem
     model, geom = tti_problem([44, 26, 30], 8, 30)
@@ -134,3 +175,18 @@ def test_tti_peer_push_between_processes_matches_single_domain(tmp_path, world, 
     assert np.abs(rec1).max() > 0
     assert np.array_equal(np.load(out + "_rec.npy"), rec1)
     assert np.array_equal(np.load(out + "_p.npy"), p1) and np.array_equal(np.load(out + "_r.npy"), r1)
+
+
+def test_adjoint_sweep_with_streamed_tables_between_processes(tmp_path):
+    import torch.multiprocessing as mp
+    model, geom = make_problem(SHAPE, 10.0, 8, ORDER, NSTEPS)
+    data = _adjoint_data(geom)
+    plan = make_plan(model, geom, ORDER)
+    srca1, _ = plan.adjoint(data)
+    v1 = plan.wavefield(0)
+    plan.close()
+    out = str(tmp_path / "ipc_adj")
+    mp.spawn(_adjoint_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    assert np.abs(srca1).max() > 0
+    assert np.array_equal(np.load(out + "_srca.npy"), srca1)
+    assert np.array_equal(np.load(out + "_v.npy"), v1)
