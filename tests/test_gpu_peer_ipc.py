@@ -93,6 +93,46 @@ def _adjoint_worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
+def _gradient_worker(rank, world, port, out):
+    """forward slab run that keeps every 2nd level, then the gradient sweep as one
+    sfb_slab_run per rank with the residual table fed while it runs"""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_1808_01995_b200 import capi, slabs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    model, geom = make_problem(SHAPE, 10.0, 8, ORDER, NSTEPS)
+    data = _adjoint_data(geom)
+    bounds = slabs.split_slabs(model.N[0], world, ORDER // 2)
+    plan = make_plan(model, geom, ORDER, slab=bounds[rank])
+    plan.upload_traces(capi.CLOUD_SRC, geom.src)
+    drv = slabs.PeerPushDriver(plan, capi.OP_FORWARD, rank, world)
+    plan.step_begin(capi.OP_FORWARD, 2)
+    plan.sync()
+    dist.barrier()
+    drv.run(1, geom.nt - 1)
+    plan.step_end(capi.OP_FORWARD)
+    plan.sync()
+    dist.barrier()
+    drv.op = capi.OP_GRADIENT
+    plan.step_begin(capi.OP_GRADIENT)
+    plan.sync()
+    dist.barrier()
+    drv.run_tables(1, geom.nt - 1, inj=data)
+    plan.step_end(capi.OP_GRADIENT)
+    grad = np.zeros(model.N)
+    plan._chk(capi.lib.sfb_get_gradient(plan.h, C.byref(capi._view(grad))))
+    grad = torch.from_numpy(grad)
+    dist.all_reduce(grad)
+    dist.barrier()
+    if rank == 0:
+        np.save(out + "_grad.npy", grad.numpy())
+    plan.close()
+    dist.destroy_process_group()
+
+
 def _tti_inputs():
     from tests.test_gpu_tti import tti_fields, tti_problem
     model, geom = tti_problem([44, 26, 30], 8, 30)
@@ -190,3 +230,17 @@ def test_adjoint_sweep_with_streamed_tables_between_processes(tmp_path):
     assert np.abs(srca1).max() > 0
     assert np.array_equal(np.load(out + "_srca.npy"), srca1)
     assert np.array_equal(np.load(out + "_v.npy"), v1)
+
+
+def test_gradient_sweep_between_processes_matches_single_domain(tmp_path):
+    import torch.multiprocessing as mp
+    model, geom = make_problem(SHAPE, 10.0, 8, ORDER, NSTEPS)
+    data = _adjoint_data(geom)
+    plan = make_plan(model, geom, ORDER)
+    plan.forward(geom.src, save_every=2)
+    g1, _ = plan.gradient(data)
+    plan.close()
+    out = str(tmp_path / "ipc_grad")
+    mp.spawn(_gradient_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert np.abs(g1).max() > 0
+    assert np.array_equal(np.load(out + "_grad.npy"), g1)
