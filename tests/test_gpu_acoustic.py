@@ -669,3 +669,23 @@ def test_slab_run_of_a_single_slab_equals_the_whole_domain_calls():
     with pytest.raises(capi.SfbError):
         plan.slab_run(capi.OP_FORWARD, 0, 5)
     plan.close()
+
+
+def test_slab_run_refuses_plans_linked_inside_one_process():
+    """plans linked with sfb_link_peers are ordered by each other's events: every plan must
+    make each call before any plan makes the next, so the per-plan loop is refused"""
+    from paper_1808_01995_b200 import capi
+    model, geom = make_problem([40, 24, 26], 10.0, 6, 8, 12)
+    lo = make_plan(model, geom, 8, slab=(0, 26))
+    hi = make_plan(model, geom, 8, slab=(26, model.N[0]))
+    lo.link_peers(None, hi)
+    hi.link_peers(lo, None)
+    lo.upload_traces(capi.CLOUD_SRC, geom.src)
+    lo.step_begin(capi.OP_FORWARD)
+    with pytest.raises(capi.SfbError) as e:
+        lo.slab_run(capi.OP_FORWARD, 1, 5)
+    assert e.value.code == capi.ERR_CAPABILITY
+    lo.link_peers(None, None)
+    hi.link_peers(None, None)
+    lo.close()
+    hi.close()
